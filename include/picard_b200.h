@@ -1,0 +1,268 @@
+/*
+ * picard_b200.h — C ABI of the B200-native Picard-iteration policy simulator.
+ *
+ * This is the drop-in boundary for the reference's serial and Picard
+ * simulation paths (arXiv 2406.01939 artifact, /root/reference/proj):
+ *
+ *   reference C++ entry point (file:line)                   replaced by
+ *   ------------------------------------------------------   ---------------------
+ *   picard::sequential_simulate      engine.hpp:237-267      pcd_sequential
+ *   picard::picard_iterate_once      engine.hpp:358-444      pcd_iterate_once
+ *   picard::picard_simulate          engine.hpp:458-590      pcd_simulate
+ *                                                             (pcd_picard_simulate = one-shot)
+ *   picard::compare_to_oracle        engine.hpp:601-614      pcd_compare_actions
+ *   picard::make_uniform_time_partition engine.hpp:99-114    pcd_uniform_partition
+ *   picard::fo::make_product_partition  instance.cpp:142-186 pcd_product_partition
+ *   picard::fo::generate_instance       instance.cpp:80-140  pcd_generate_instance
+ *   picard::fo::MlpParams::seeded_uniform mlp.cpp:117-129     pcd_seeded_mlp
+ *   picard::fo::fo_total_reward         env.hpp:298-310      pcd_total_reward
+ *   Policy::evaluate (Greedy / CapacityPenalized / DualNetwork, policies.hpp:24-174)
+ *                                                             pcd_policy (kind + params)
+ *
+ * Conventions
+ *  - All pointers are caller-owned HOST memory; the library owns every device
+ *    buffer behind a pcd_handle.  Nothing here takes or returns torch types.
+ *  - Actions are int32 node indices, -1 = decline (fo/types.hpp:15-22).
+ *  - Inventory is dense row-major [products x nodes]; an all-zero row is the
+ *    reference's "absent row" (fo/types.hpp:45-51, 65-71).
+ *  - Rewards are a table [reward_rows x nodes] plus reward_row[t]; generated
+ *    instances use one row per origin node (instance.cpp:100-105), loaded
+ *    instances may use one row per order.
+ *  - Status codes mirror the reference's exception types:
+ *      PCD_OK                 0
+ *      PCD_INVALID_ARGUMENT   1  (std::invalid_argument)
+ *      PCD_CONTRACT_VIOLATION 2  (picard::ContractViolation, errors.hpp:11-20;
+ *                                 result->error_time_step carries time_step())
+ *      PCD_ITERATION_LIMIT    3  (picard::IterationLimitError, engine.hpp:140-156;
+ *                                 result->iterations_run + partial trace)
+ *      PCD_CUDA_ERROR         4  (device / NCCL failure; no CPU fallback exists)
+ *    pcd_last_error() returns the message of the last failure on this thread.
+ *  - One handle per host thread; no callbacks.
+ */
+#ifndef PICARD_B200_H_
+#define PICARD_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PCD_OK = 0,
+  PCD_INVALID_ARGUMENT = 1,
+  PCD_CONTRACT_VIOLATION = 2,
+  PCD_ITERATION_LIMIT = 3,
+  PCD_CUDA_ERROR = 4
+};
+
+/* Policy kinds (fo/policies.hpp). PCD_POLICY_NULL is the always-decline
+ * policy the reference tests use (test_engine.cpp:17-22). */
+enum {
+  PCD_POLICY_GREEDY = 0,    /* GreedyPolicy            policies.hpp:24-44  */
+  PCD_POLICY_CAPACITY = 1,  /* CapacityPenalizedPolicy policies.hpp:50-75  */
+  PCD_POLICY_DUAL = 2,      /* DualNetworkPolicy       policies.hpp:88-174 */
+  PCD_POLICY_NULL = 3
+};
+
+/* Sweep engine selection for pcd_simulate / pcd_iterate_once. */
+enum {
+  PCD_ENGINE_AUTO = 0,     /* closed form when the plan is a product partition */
+  PCD_ENGINE_REPLAY = 1,   /* exact per-process window replay (any plan)        */
+  PCD_ENGINE_PRODUCT = 2   /* closed-form product-partition sweep (checked)     */
+};
+
+/* A fulfillment-optimization instance (fo/instance.hpp:25-37). */
+typedef struct pcd_instance {
+  int32_t nodes;              /* J */
+  int32_t products;           /* I */
+  int64_t horizon;            /* T */
+  const int32_t* product;     /* [T] Order::product */
+  const int32_t* order_t;     /* [T] Order::t, or NULL meaning order_t[t] == t */
+  const int32_t* reward_row;  /* [T] row of reward_table holding Order::rewards */
+  const double* reward_table; /* [reward_rows * J] */
+  int64_t reward_rows;
+  const int32_t* capacity;    /* [J] initial FoState::capacity */
+  const int32_t* inventory;   /* [I * J] initial FoState::inventory (dense) */
+} pcd_instance;
+
+/* A policy. For PCD_POLICY_DUAL the MLP is {2J+1, hidden, hidden, 2J}
+ * (fo/mlp.hpp:13-36) with row-major weights; init_* and horizon are the
+ * DualNetworkPolicy's normalisation state (policies.hpp:92-96, 136-148). */
+typedef struct pcd_policy {
+  int32_t kind;
+  int32_t hidden;               /* 64 in the reference */
+  double gamma;                 /* CapacityPenalizedPolicy::gamma */
+  const double* w1;             /* [hidden * (2J+1)] */
+  const double* b1;             /* [hidden] */
+  const double* w2;             /* [hidden * hidden] */
+  const double* b2;             /* [hidden] */
+  const double* w3;             /* [2J * hidden] */
+  const double* b3;             /* [2J] */
+  const int32_t* init_capacity; /* [J]   NULL -> instance capacity  */
+  const int32_t* init_inventory;/* [I*J] NULL -> instance inventory */
+  int64_t horizon;              /* <0 -> instance horizon */
+} pcd_policy;
+
+/* PicardConfig (engine.hpp:120-126) plus B200 engine knobs. */
+typedef struct pcd_config {
+  int32_t processes;       /* 0 = take M from the plan */
+  int32_t record_trace;    /* bool */
+  int64_t max_steps;       /* window width; 0 = whole horizon */
+  int64_t max_iterations;  /* 0 = 2T + 4 */
+  int32_t threads;         /* accepted for API parity; the device ignores it */
+  int32_t engine;          /* PCD_ENGINE_* */
+} pcd_config;
+
+/* PicardTraceRow (engine.hpp:128-134). */
+typedef struct pcd_trace_row {
+  int64_t chunk;
+  int64_t iteration;
+  int64_t changed_slots;
+  int64_t max_process_evals;
+  int64_t t_reset;
+} pcd_trace_row;
+
+/* PicardResult (engine.hpp:158-176) minus the action vector and trace, which
+ * are written into caller buffers. */
+typedef struct pcd_result {
+  int64_t iterations_to_converged;
+  int64_t iterations_to_correct;   /* -1 = not measured / never correct */
+  int64_t conflicts;
+  int64_t policy_eval_count_sequential_equivalent;
+  int64_t total_policy_evals;
+  int64_t trace_rows;              /* rows produced (may exceed trace_cap) */
+  int64_t iterations_run;          /* == iterations_to_converged unless a cap fired */
+  int64_t error_time_step;         /* ContractViolation::time_step(), -1 if none */
+} pcd_result;
+
+/* Device-side timing of the last pcd_simulate (CUDA events, milliseconds). */
+typedef struct pcd_timing {
+  double total_ms;        /* first kernel of iteration 1 .. last scalar read */
+  double sweep_ms;        /* sum over iterations of the sweep kernel(s) */
+  double prep_ms;         /* eff / checkpoint-count kernels */
+  double publish_ms;      /* publish / convergence kernels (replay engine) */
+  double advance_ms;      /* checkpoint-advance kernels */
+  int64_t iterations;
+  int64_t kernel_launches;
+  int64_t sweep_launches;
+  int64_t steps_critical; /* sum over iterations of max per-process evals */
+  int64_t total_evals;
+  int32_t engine_used;    /* PCD_ENGINE_REPLAY / PCD_ENGINE_PRODUCT */
+  int32_t device;
+} pcd_timing;
+
+typedef struct pcd_handle pcd_handle;
+
+/* ---------------------------------------------------------------- misc */
+const char* pcd_version(void);
+const char* pcd_last_error(void);
+/* Number of CUDA devices visible (0 on a CPU-only host; never fails). */
+int pcd_device_count(void);
+
+/* ------------------------------------------------------- host-side inputs
+ * These run on the host CPU (they are serial-RNG bound and must reproduce the
+ * reference's mt19937_64 streams bit for bit). */
+
+/* generate_instance (instance.cpp:80-140). geometry 0 = the reference's
+ * 30-city table (default_geometry, geometry.cpp:93-102, J <= 30);
+ * geometry 1 = the seeded synthetic J-node geometry used for J > 30
+ * (mt19937_64(12345), lat U(25,49), lon U(-124,-67),
+ * population U(1e6,4e7), drawn per node in that order).
+ * Outputs: product[T], origin[T] (== reward_row), reward_table[J*J],
+ * capacity[J], inventory[I*J]. */
+int pcd_generate_instance(int32_t nodes, int32_t products, int64_t horizon,
+                          double beta, double coverage, uint64_t seed,
+                          int32_t geometry, int32_t* product, int32_t* origin,
+                          double* reward_table, int32_t* capacity,
+                          int32_t* inventory);
+
+/* make_product_partition (instance.cpp:142-186): owner[T]. */
+int pcd_product_partition(const pcd_instance* inst, int32_t processes,
+                          uint64_t seed, int32_t* owner);
+/* make_uniform_time_partition (engine.hpp:99-114): owner[T]. */
+int pcd_uniform_partition(int64_t horizon, int32_t processes, uint64_t seed,
+                          int32_t* owner);
+/* MlpParams::seeded_uniform (mlp.cpp:117-129). */
+int pcd_seeded_mlp(int32_t input, int32_t output, uint64_t seed, int32_t hidden,
+                   double* w1, double* b1, double* w2, double* b2, double* w3,
+                   double* b3);
+/* fo_total_reward (env.hpp:298-310). */
+int pcd_total_reward(const pcd_instance* inst, const int32_t* actions,
+                     double* total);
+/* compare_to_oracle (engine.hpp:601-614): *first_mismatch = -1 when equal. */
+int pcd_compare_actions(const int32_t* a, const int32_t* b, int64_t n,
+                        int64_t* first_mismatch);
+
+/* Multi-GPU sharding of processes: LPT over per-process
+ * owned-slot loads onto `ranks` shards; rank_of[M]. Pure host logic. */
+int pcd_shard_processes(const int32_t* owner, int64_t horizon, int32_t processes,
+                        int32_t ranks, int32_t* rank_of);
+
+/* --------------------------------------------------------- device engine */
+int pcd_create(const pcd_instance* inst, const pcd_policy* policy, int32_t device,
+               pcd_handle** out);
+void pcd_destroy(pcd_handle* h);
+
+/* Uploads a partition plan (PartitionPlan, engine.hpp:74-96) and builds the
+ * per-process slot CSR on the device. Validates like PartitionPlan::validate. */
+int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t processes);
+
+/* picard_simulate (engine.hpp:458-590). initial_cache / reference may be NULL.
+ * actions_out[T] receives the converged actions; trace[trace_cap] the rows. */
+int pcd_simulate(pcd_handle* h, const pcd_config* cfg,
+                 const int32_t* initial_cache, const int32_t* reference,
+                 int32_t* actions_out, pcd_result* result, pcd_trace_row* trace,
+                 int64_t trace_cap);
+
+/* Same, but with the cache / reference already resident (no host copies);
+ * the converged actions stay on the device until pcd_download_actions. Used
+ * by bench.py for the HBM-resident throughput number. */
+int pcd_simulate_resident(pcd_handle* h, const pcd_config* cfg,
+                          int32_t use_initial_cache, int32_t use_reference,
+                          pcd_result* result, pcd_trace_row* trace,
+                          int64_t trace_cap);
+int pcd_upload_cache(pcd_handle* h, const int32_t* initial_cache,
+                     const int32_t* reference);
+int pcd_download_actions(pcd_handle* h, int32_t* actions_out);
+
+/* picard_iterate_once (engine.hpp:358-444) over [t_lo, t_hi) from the given
+ * checkpoint state. cache[T] is read and updated in place (host memory).
+ * evals_per_process[M]; changed_slots receives ascending time indices
+ * (capacity T), *n_changed their count. */
+int pcd_iterate_once(pcd_handle* h, int32_t engine, int32_t* cache, int64_t t_lo,
+                     int64_t t_hi, const int32_t* ckpt_capacity,
+                     const int32_t* ckpt_inventory, int64_t* evals_per_process,
+                     int64_t* changed_slots, int64_t* n_changed);
+
+/* sequential_simulate (engine.hpp:237-267): the serial trajectory. Computed on
+ * the device as the Picard fixed point of a product partition over
+ * min(I, 8192) processes (Prop. 1: identical actions); policy_evals = T. */
+int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* policy_evals);
+
+int pcd_last_timing(const pcd_handle* h, pcd_timing* out);
+
+/* One-shot convenience mirroring the reference call shape. */
+int pcd_picard_simulate(const pcd_instance* inst, const pcd_policy* policy,
+                        const int32_t* owner, int32_t processes,
+                        const pcd_config* cfg, const int32_t* initial_cache,
+                        const int32_t* reference, int32_t* actions_out,
+                        pcd_result* result, pcd_trace_row* trace,
+                        int64_t trace_cap);
+
+/* ----------------------------------------------- multi-GPU (NCCL, NVLink)
+ * One process per GPU. Rank 0 calls pcd_nccl_unique_id and broadcasts the
+ * 128 bytes (e.g. via torch.distributed); every rank then attaches. After
+ * attaching, pcd_simulate runs only the processes with rank_of[m] == rank and
+ * exchanges fresh cache slices with ncclAllGather plus one ncclAllReduce of
+ * the convergence scalars per iteration; every rank returns identical results. */
+int pcd_nccl_unique_id(unsigned char out[128]);
+int pcd_attach_comm(pcd_handle* h, const unsigned char id[128], int32_t rank,
+                    int32_t nranks);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* PICARD_B200_H_ */

@@ -1,0 +1,330 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes front-end to the two CPU oracles.
+
+``ORC``  : oracle/liboracle.so — plain-C restatement of the reference hot path
+           (oracle/picard_oracle.c), pinned by tests/test_oracle.py.
+``REF``  : oracle/_ref/libpicard_ref.so — the unmodified reference library
+           (/root/reference/proj) + oracle/ref_harness.cpp; ``None`` when it
+           was not built (e.g. the reference tree is absent and no prebuilt
+           copy travelled with the repo).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU legs import this
+module.  It duck-types instances/policies (any object with the attributes of
+``paper_2406_01939_b200.api.Instance`` / ``Policy``) so it never imports the
+product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+_F64P = C.POINTER(C.c_double)
+
+
+class CInstance(C.Structure):
+    _fields_ = [("nodes", C.c_int32), ("products", C.c_int32), ("horizon", C.c_int64),
+                ("product", _I32P), ("order_t", _I32P), ("reward_row", _I32P),
+                ("reward_table", _F64P), ("reward_rows", C.c_int64),
+                ("capacity", _I32P), ("inventory", _I32P)]
+
+
+class CPolicy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("hidden", C.c_int32), ("gamma", C.c_double),
+                ("w1", _F64P), ("b1", _F64P), ("w2", _F64P), ("b2", _F64P),
+                ("w3", _F64P), ("b3", _F64P), ("init_capacity", _I32P),
+                ("init_inventory", _I32P), ("horizon", C.c_int64)]
+
+
+class CConfig(C.Structure):
+    _fields_ = [("processes", C.c_int32), ("record_trace", C.c_int32),
+                ("max_steps", C.c_int64), ("max_iterations", C.c_int64),
+                ("threads", C.c_int32), ("engine", C.c_int32)]
+
+
+class CTraceRow(C.Structure):
+    _fields_ = [("chunk", C.c_int64), ("iteration", C.c_int64), ("changed_slots", C.c_int64),
+                ("max_process_evals", C.c_int64), ("t_reset", C.c_int64)]
+
+
+class CResult(C.Structure):
+    _fields_ = [("iterations_to_converged", C.c_int64), ("iterations_to_correct", C.c_int64),
+                ("conflicts", C.c_int64),
+                ("policy_eval_count_sequential_equivalent", C.c_int64),
+                ("total_policy_evals", C.c_int64), ("trace_rows", C.c_int64),
+                ("iterations_run", C.c_int64), ("error_time_step", C.c_int64)]
+
+
+def _p(a, ctype):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str, time_step: int = -1):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.time_step = time_step
+
+
+@dataclass
+class OracleResult:
+    actions: np.ndarray
+    iterations_to_converged: int
+    iterations_to_correct: Optional[int]
+    conflicts: int
+    policy_eval_count_sequential_equivalent: int
+    total_policy_evals: int
+    trace: list
+    history: Optional[np.ndarray]
+
+
+def _keep(*arrays):
+    return [np.ascontiguousarray(a) if a is not None else None for a in arrays]
+
+
+class _Lib:
+    def __init__(self, path: str, prefix: str):
+        self.path = path
+        self.prefix = prefix
+        self.lib = C.CDLL(path)
+        L = self.lib
+        f = lambda n: getattr(L, f"{prefix}_{n}")
+        f("last_error").restype = C.c_char_p
+        f("tanh").restype = C.c_double
+        f("tanh").argtypes = [C.c_double]
+
+    def fn(self, name):
+        return getattr(self.lib, f"{self.prefix}_{name}")
+
+    def err(self) -> str:
+        return self.fn("last_error")().decode()
+
+    def check(self, rc, time_step=-1):
+        if rc != 0:
+            raise OracleError(rc, self.err(), time_step)
+
+    # -------------------------------------------------------------- inputs
+    def _inst(self, inst):
+        arrays = dict(product=np.ascontiguousarray(inst.product, np.int32),
+                      order_t=None if getattr(inst, "order_t", None) is None
+                      else np.ascontiguousarray(inst.order_t, np.int32),
+                      reward_row=np.ascontiguousarray(inst.reward_row, np.int32),
+                      reward_table=np.ascontiguousarray(inst.reward_table, np.float64),
+                      capacity=np.ascontiguousarray(inst.capacity, np.int32),
+                      inventory=np.ascontiguousarray(inst.inventory, np.int32))
+        c = CInstance(int(inst.nodes), int(inst.products), int(inst.horizon),
+                      _p(arrays["product"], C.c_int32), _p(arrays["order_t"], C.c_int32),
+                      _p(arrays["reward_row"], C.c_int32), _p(arrays["reward_table"], C.c_double),
+                      int(arrays["reward_table"].size // max(1, int(inst.nodes))),
+                      _p(arrays["capacity"], C.c_int32), _p(arrays["inventory"], C.c_int32))
+        return c, arrays
+
+    def _pol(self, pol):
+        keep = {}
+        def arr(name, dt):
+            v = getattr(pol, name, None)
+            if v is None:
+                return None
+            keep[name] = np.ascontiguousarray(v, dt)
+            return keep[name]
+        c = CPolicy(int(pol.kind), int(getattr(pol, "hidden", 64)), float(getattr(pol, "gamma", 0.0)),
+                    _p(arr("w1", np.float64), C.c_double), _p(arr("b1", np.float64), C.c_double),
+                    _p(arr("w2", np.float64), C.c_double), _p(arr("b2", np.float64), C.c_double),
+                    _p(arr("w3", np.float64), C.c_double), _p(arr("b3", np.float64), C.c_double),
+                    _p(arr("init_capacity", np.int32), C.c_int32),
+                    _p(arr("init_inventory", np.int32), C.c_int32),
+                    int(getattr(pol, "horizon", -1) if getattr(pol, "horizon", None) is not None else -1))
+        return c, keep
+
+    def tanh(self, x: float) -> float:
+        return self.fn("tanh")(float(x))
+
+    def demand_counts(self, products, horizon, beta):
+        out = np.zeros(products, np.int64)
+        self.check(self.fn("demand_counts")(C.c_int32(products), C.c_int64(horizon),
+                                            C.c_double(beta), _p(out, C.c_int64)))
+        return out
+
+    def apportion(self, weights, total):
+        w = np.ascontiguousarray(weights, np.float64)
+        out = np.zeros(len(w), np.int64)
+        self.check(self.fn("apportion")(_p(w, C.c_double), C.c_int64(len(w)), C.c_int64(total),
+                                        _p(out, C.c_int64)))
+        return out
+
+    def generate_instance_arrays(self, J, I, T, beta, coverage=0.8, seed=0, geometry=0):
+        product = np.zeros(T, np.int32)
+        origin = np.zeros(T, np.int32)
+        table = np.zeros(J * J, np.float64)
+        cap = np.zeros(J, np.int32)
+        inv = np.zeros(I * J, np.int32)
+        self.check(self.fn("generate_instance")(
+            C.c_int32(J), C.c_int32(I), C.c_int64(T), C.c_double(beta), C.c_double(coverage),
+            C.c_uint64(seed), C.c_int32(geometry), _p(product, C.c_int32), _p(origin, C.c_int32),
+            _p(table, C.c_double), _p(cap, C.c_int32), _p(inv, C.c_int32)))
+        return dict(nodes=J, products=I, horizon=T, product=product, order_t=None,
+                    reward_row=origin, reward_table=table, capacity=cap, inventory=inv)
+
+    def small_random_params(self, seed):
+        n = C.c_int32(); p = C.c_int32(); h = C.c_int64(); b = C.c_double(); cv = C.c_double()
+        s = C.c_uint64()
+        self.fn("small_random_params")(C.c_uint64(seed), C.byref(n), C.byref(p), C.byref(h),
+                                       C.byref(b), C.byref(cv), C.byref(s))
+        return n.value, p.value, h.value, b.value, cv.value, s.value
+
+    def product_partition(self, inst, M, seed):
+        c, keep = self._inst(inst)
+        owner = np.zeros(int(inst.horizon), np.int32)
+        self.check(self.fn("product_partition")(C.byref(c), C.c_int32(M), C.c_uint64(seed),
+                                                _p(owner, C.c_int32)))
+        return owner
+
+    def uniform_partition(self, T, M, seed):
+        owner = np.zeros(int(T), np.int32)
+        self.check(self.fn("uniform_partition")(C.c_int64(T), C.c_int32(M), C.c_uint64(seed),
+                                                _p(owner, C.c_int32)))
+        return owner
+
+    def seeded_mlp(self, inp, out, seed, hidden=64):
+        a = [np.zeros(hidden * inp), np.zeros(hidden), np.zeros(hidden * hidden), np.zeros(hidden),
+             np.zeros(out * hidden), np.zeros(out)]
+        self.check(self.fn("seeded_mlp")(C.c_int32(inp), C.c_int32(out), C.c_uint64(seed),
+                                         C.c_int32(hidden), *[_p(x, C.c_double) for x in a]))
+        return a
+
+    def mlp_forward(self, pol, x):
+        c, keep = self._pol(pol)
+        x = np.ascontiguousarray(x, np.float64)
+        nout = len(pol.b3)
+        out = np.zeros(nout)
+        self.check(self.fn("mlp_forward")(C.byref(c), C.c_int32(len(x)), C.c_int32(nout),
+                                          _p(x, C.c_double), _p(out, C.c_double)))
+        return out
+
+    def policy_evaluate(self, inst, pol, cap, inv, t):
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        cap = np.ascontiguousarray(cap, np.int32)
+        inv = np.ascontiguousarray(inv, np.int32)
+        a = C.c_int32()
+        self.check(self.fn("policy_evaluate")(C.byref(ci), C.byref(cp), _p(cap, C.c_int32),
+                                              _p(inv, C.c_int32), C.c_int64(t), C.byref(a)))
+        return a.value
+
+    # -------------------------------------------------------------- engine
+    def sequential(self, inst, pol):
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        actions = np.zeros(int(inst.horizon), np.int32)
+        ev = C.c_int64()
+        et = C.c_int64(-1)
+        rc = self.fn("sequential")(C.byref(ci), C.byref(cp), _p(actions, C.c_int32), C.byref(ev),
+                                   C.byref(et))
+        self.check(rc, et.value)
+        return actions, ev.value
+
+    def picard(self, inst, pol, owner, M, max_steps=0, max_iterations=0, record_trace=False,
+               threads=1, initial_cache=None, reference=None, history=False, processes=0):
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        T = int(inst.horizon)
+        owner, initial_cache, reference = _keep(np.asarray(owner, np.int32),
+                                                None if initial_cache is None else np.asarray(initial_cache, np.int32),
+                                                None if reference is None else np.asarray(reference, np.int32))
+        cfg = CConfig(processes, 1 if record_trace else 0, max_steps, max_iterations, threads, 0)
+        actions = np.zeros(max(T, 1), np.int32)
+        res = CResult()
+        cap = 4 * T + 16
+        trace = (CTraceRow * cap)()
+        hist = np.zeros((cap if history else 0, T), np.int32) if history else None
+        rc = self.fn("picard")(C.byref(ci), C.byref(cp), _p(owner, C.c_int32), C.c_int32(M),
+                               C.byref(cfg), _p(initial_cache, C.c_int32), _p(reference, C.c_int32),
+                               _p(actions, C.c_int32), C.byref(res), trace, C.c_int64(cap),
+                               _p(hist, C.c_int32) if history else None,
+                               C.c_int64(cap if history else 0))
+        rows = [(r.chunk, r.iteration, r.changed_slots, r.max_process_evals, r.t_reset)
+                for r in trace[:min(res.trace_rows, cap)]]
+        if rc != 0:
+            e = OracleError(rc, self.err(), res.error_time_step)
+            e.iterations_run = res.iterations_run
+            e.partial_trace = rows
+            raise e
+        k = res.iterations_run
+        return OracleResult(actions[:T].copy(), res.iterations_to_converged,
+                            None if res.iterations_to_correct < 0 else res.iterations_to_correct,
+                            res.conflicts, res.policy_eval_count_sequential_equivalent,
+                            res.total_policy_evals, rows, hist[:k].copy() if history else None)
+
+    def iterate_once(self, inst, pol, owner, M, cache, lo, hi, ck_cap=None, ck_inv=None):
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        T = int(inst.horizon)
+        owner = np.ascontiguousarray(owner, np.int32)
+        cache = np.array(cache, np.int32, copy=True)
+        ck_cap = np.ascontiguousarray(inst.capacity if ck_cap is None else ck_cap, np.int32)
+        ck_inv = np.ascontiguousarray(inst.inventory if ck_inv is None else ck_inv, np.int32)
+        evals = np.zeros(M, np.int64)
+        changed = np.zeros(max(T, 1), np.int64)
+        n = C.c_int64()
+        et = C.c_int64(-1)
+        rc = self.fn("iterate_once")(C.byref(ci), C.byref(cp), _p(owner, C.c_int32), C.c_int32(M),
+                                     _p(cache, C.c_int32), C.c_int64(lo), C.c_int64(hi),
+                                     _p(ck_cap, C.c_int32), _p(ck_inv, C.c_int32),
+                                     _p(evals, C.c_int64), _p(changed, C.c_int64), C.byref(n),
+                                     C.byref(et))
+        self.check(rc, et.value)
+        return cache, evals, changed[:n.value].copy()
+
+    def naive_fixed_point(self, inst, pol, owner, M):
+        assert self.prefix == "orc"
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        T = int(inst.horizon)
+        owner = np.ascontiguousarray(owner, np.int32)
+        cap = 2 * T + 4
+        hist = np.zeros((cap, max(T, 1)), np.int32)
+        k = C.c_int64()
+        self.check(self.fn("naive_fixed_point")(C.byref(ci), C.byref(cp), _p(owner, C.c_int32),
+                                                C.c_int32(M), _p(hist, C.c_int32), C.c_int64(cap),
+                                                C.byref(k)))
+        return hist[:k.value, :T].copy()
+
+    def total_reward(self, inst, actions):
+        ci, k1 = self._inst(inst)
+        a = np.ascontiguousarray(actions, np.int32)
+        out = C.c_double()
+        self.check(self.fn("total_reward")(C.byref(ci), _p(a, C.c_int32), C.byref(out)))
+        return out.value
+
+
+def build(quiet=True):
+    """Builds liboracle.so (+ _ref when the reference tree exists)."""
+    subprocess.run(["make", "-C", HERE], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+def _load(path, prefix):
+    return _Lib(path, prefix) if os.path.exists(path) else None
+
+
+_orc_path = os.path.join(HERE, "liboracle.so")
+if not os.path.exists(_orc_path):
+    build()
+ORC = _load(_orc_path, "orc")
+REF = _load(os.path.join(HERE, "_ref", "libpicard_ref.so"), "ref")
+if ORC is not None:
+    ORC.lib.orc_tanh_nofma.restype = C.c_double
+    ORC.lib.orc_tanh_nofma.argtypes = [C.c_double]
+    ORC.lib.orc_expm1.restype = C.c_double
+    ORC.lib.orc_expm1.argtypes = [C.c_double]
+    ORC.lib.orc_expm1_nofma.restype = C.c_double
+    ORC.lib.orc_expm1_nofma.argtypes = [C.c_double]
+    ORC.lib.orc_tanh_variant.restype = C.c_int
