@@ -243,6 +243,11 @@ int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* policy_evals);
 
 int pcd_last_timing(const pcd_handle* h, pcd_timing* out);
 
+/* Debug/parity hook (theory::CacheTraceRecorder, theory.hpp:120-126): when
+ * set, pcd_simulate copies the full cache into history[k*T .. (k+1)*T) after
+ * iteration k+1 (first `cap_iterations` iterations). NULL disables. */
+int pcd_set_history(pcd_handle* h, int32_t* history, int64_t cap_iterations);
+
 /* One-shot convenience mirroring the reference call shape. */
 int pcd_picard_simulate(const pcd_instance* inst, const pcd_policy* policy,
                         const int32_t* owner, int32_t processes,

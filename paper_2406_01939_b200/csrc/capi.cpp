@@ -1,0 +1,134 @@
+// capi.cpp — host-only entry points of the C ABI (include/picard_b200.h) and
+// the exception -> status-code translation shared with engine.cu.
+#include <cstring>
+#include <string>
+
+#include "capi_internal.h"
+
+namespace pcd {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+// Maps the in-flight exception onto the status codes of picard_b200.h, which
+// mirror the reference's exception classes (errors.hpp, engine.hpp:140-156).
+int translate_exception() {
+  try {
+    throw;
+  } catch (const IterationLimit& e) {
+    set_last_error(e.what());
+    return PCD_ITERATION_LIMIT;
+  } catch (const ContractViolation& e) {
+    set_last_error(e.what());
+    return PCD_CONTRACT_VIOLATION;
+  } catch (const InvalidArgument& e) {
+    set_last_error(e.what());
+    return PCD_INVALID_ARGUMENT;
+  } catch (const CudaError& e) {
+    set_last_error(e.what());
+    return PCD_CUDA_ERROR;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return PCD_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return PCD_INVALID_ARGUMENT;
+  } catch (...) {
+    set_last_error("unknown error");
+    return PCD_INVALID_ARGUMENT;
+  }
+}
+
+}  // namespace pcd
+
+#define PCD_TRY try {
+#define PCD_CATCH \
+  }               \
+  catch (...) { return pcd::translate_exception(); }
+
+extern "C" {
+
+const char* pcd_version(void) { return "picard_b200 0.1.0 (sm_100a)"; }
+
+const char* pcd_last_error(void) { return pcd::g_last_error.c_str(); }
+
+int pcd_generate_instance(int32_t nodes, int32_t products, int64_t horizon, double beta,
+                          double coverage, uint64_t seed, int32_t geometry, int32_t* product,
+                          int32_t* origin, double* reward_table, int32_t* capacity,
+                          int32_t* inventory) {
+  PCD_TRY
+  if (!product || !origin || !reward_table || !capacity || !inventory)
+    throw pcd::InvalidArgument("null output buffer");
+  pcd::generate_instance(nodes, products, horizon, beta, coverage, seed, geometry, product, origin,
+                         reward_table, capacity, inventory);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_product_partition(const pcd_instance* inst, int32_t processes, uint64_t seed, int32_t* owner) {
+  PCD_TRY
+  if (!inst || !owner) throw pcd::InvalidArgument("null argument");
+  for (int64_t t = 0; t < inst->horizon; ++t)
+    if (inst->product[t] < 0 || inst->product[t] >= inst->products)
+      throw pcd::InvalidArgument("order product out of range");
+  pcd::product_partition(inst->product, inst->horizon, inst->products, processes, seed, owner);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_uniform_partition(int64_t horizon, int32_t processes, uint64_t seed, int32_t* owner) {
+  PCD_TRY
+  if (horizon > 0 && !owner) throw pcd::InvalidArgument("null argument");
+  pcd::uniform_partition(horizon, processes, seed, owner);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_seeded_mlp(int32_t input, int32_t output, uint64_t seed, int32_t hidden, double* w1,
+                   double* b1, double* w2, double* b2, double* w3, double* b3) {
+  PCD_TRY
+  if (!w1 || !b1 || !w2 || !b2 || !w3 || !b3) throw pcd::InvalidArgument("null output buffer");
+  pcd::seeded_mlp(input, output, seed, hidden, w1, b1, w2, b2, w3, b3);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_total_reward(const pcd_instance* inst, const int32_t* actions, double* total) {
+  PCD_TRY
+  if (!inst || !actions || !total) throw pcd::InvalidArgument("null argument");
+  double s = 0.0;  // fo_total_reward (env.hpp:298-310): in order, declines earn 0
+  for (int64_t t = 0; t < inst->horizon; ++t)
+    if (actions[t] >= 0)
+      s += inst->reward_table[(size_t)inst->reward_row[t] * inst->nodes + actions[t]];
+  *total = s;
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_compare_actions(const int32_t* a, const int32_t* b, int64_t n, int64_t* first_mismatch) {
+  PCD_TRY
+  if ((n > 0 && (!a || !b)) || !first_mismatch) throw pcd::InvalidArgument("null argument");
+  *first_mismatch = -1;
+  for (int64_t t = 0; t < n; ++t)
+    if (a[t] != b[t]) {
+      *first_mismatch = t;
+      break;
+    }
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_shard_processes(const int32_t* owner, int64_t horizon, int32_t processes, int32_t ranks,
+                        int32_t* rank_of) {
+  PCD_TRY
+  if ((horizon > 0 && !owner) || !rank_of) throw pcd::InvalidArgument("null argument");
+  if (processes < 1) throw pcd::InvalidArgument("processes must be >= 1");
+  for (int64_t t = 0; t < horizon; ++t)
+    if (owner[t] < 0 || owner[t] >= processes) throw pcd::InvalidArgument("owner out of range");
+  pcd::shard_processes(owner, horizon, processes, ranks, rank_of);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+}  // extern "C"

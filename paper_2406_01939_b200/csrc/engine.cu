@@ -1,0 +1,861 @@
+// engine.cu — B200-native Picard fixed-point engine behind the C ABI.
+//
+// Host driver mirroring picard::picard_simulate (engine.hpp:458-590) and
+// picard_iterate_once (engine.hpp:358-444); every per-iteration computation
+// (sweeps, publish, counters, checkpoint advance) runs in the kernels of
+// kernels.cuh on the device. Only the per-iteration scalar block (a few
+// dozen bytes) crosses PCIe inside the loop.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "capi_internal.h"
+#include "kernels.cuh"
+
+namespace pcd {
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x);   \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { if (p) cudaFree(p); }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// --------------------------------------------------------------- NCCL (dlopen)
+// Minimal NCCL surface, loaded lazily so single-GPU use never needs libnccl.
+typedef struct { char internal[128]; } nccl_unique_id;
+typedef void* nccl_comm;
+struct NcclApi {
+  void* lib = nullptr;
+  int (*GetUniqueId)(nccl_unique_id*) = nullptr;
+  int (*CommInitRank)(nccl_comm*, int, nccl_unique_id, int) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  int (*CommDestroy)(nccl_comm) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool load() {
+    if (lib) return true;
+    for (const char* n : {"libnccl.so.2", "libnccl.so"}) {
+      lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
+    AllGather = (decltype(AllGather))dlsym(lib, "ncclAllGather");
+    AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(lib, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && AllGather && AllReduce && CommDestroy;
+  }
+};
+static NcclApi g_nccl;
+enum { ncclInt32 = 2, ncclInt64 = 4, ncclUint64 = 5, ncclSum = 0, ncclMax = 2, ncclMin = 3 };
+
+}  // namespace pcd
+
+struct pcd_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int32_t J = 0, I = 0;
+  int64_t T = 0, R = 0;
+  int tanh_fma = 1;
+  // instance
+  pcd::DBuf<int> product, order_t, rrow, cap0, inv0;
+  pcd::DBuf<double> rtab;
+  // policy
+  int kind = 0, H = 64;
+  double gamma = 0.0;
+  int64_t p_horizon = 0;
+  pcd::DBuf<double> w1t, b1, w2t, b2, w3t, b3;
+  pcd::DBuf<int> pcap0, pinv0;
+  // plan
+  int32_t M = 0;
+  bool have_plan = false, is_product = false;
+  std::vector<int32_t> h_owner;
+  pcd::DBuf<int> owner, pstart, pslots, qstart, qslots;
+  // dynamic state
+  pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, scratch;
+  pcd::DBuf<unsigned char> written;
+  pcd::DBuf<long long> evals;
+  pcd::Scalars* scal = nullptr;  // device
+  pcd::Scalars* h_scal = nullptr;  // pinned host
+  long long* d_errt = nullptr;
+  pcd_timing timing{};
+  bool resident_valid = false;
+  int32_t* history = nullptr;  // host, pcd_set_history
+  int64_t history_cap = 0;
+  // multi-GPU
+  int32_t rank = 0, nranks = 1;
+  pcd::nccl_comm comm = nullptr;
+  std::vector<int32_t> rank_of;
+
+  pcd::DevModel model() const {
+    pcd::DevModel m{};
+    m.kind = kind; m.J = J; m.I = I; m.H = H; m.in = 2 * J + 1; m.out = 2 * J;
+    m.gamma = gamma;
+    m.w1t = w1t.p; m.b1 = b1.p; m.w2t = w2t.p; m.b2 = b2.p; m.w3t = w3t.p; m.b3 = b3.p;
+    m.pcap0 = pcap0.p; m.pinv0 = pinv0.p; m.horizon = p_horizon; m.tanh_fma = tanh_fma;
+    m.product = product.p; m.order_t = order_t.p; m.rrow = rrow.p; m.rtab = rtab.p;
+    return m;
+  }
+  ~pcd_handle() {
+    if (comm && pcd::g_nccl.CommDestroy) pcd::g_nccl.CommDestroy(comm);
+    if (scal) cudaFree(scal);
+    if (h_scal) cudaFreeHost(h_scal);
+    if (d_errt) cudaFree(d_errt);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace pcd {
+
+static int host_tanh_fma() {
+#if defined(__x86_64__)
+  __builtin_cpu_init();
+  return (__builtin_cpu_supports("fma") && __builtin_cpu_supports("avx2")) ? 1 : 0;
+#else
+  return 1;
+#endif
+}
+
+static int grid_for(long long n, int block, int cap = 148 * 16) {
+  long long g = (n + block - 1) / block;
+  return (int)std::max(1LL, std::min<long long>(g, cap));
+}
+
+// Builds a time-ordered CSR of slot indices keyed by `keys` (owner or product).
+static void build_csr(pcd_handle* h, const int* d_keys, int nkeys, DBuf<int>& start, DBuf<int>& slots) {
+  const int64_t T = h->T;
+  start.alloc((size_t)nkeys + 1);
+  slots.alloc((size_t)std::max<int64_t>(T, 1));
+  if (T == 0) {
+    CK(cudaMemsetAsync(start.p, 0, sizeof(int) * ((size_t)nkeys + 1), h->stream));
+    return;
+  }
+  DBuf<int> vals_in, keys_out;
+  vals_in.alloc(T);
+  keys_out.alloc(T);
+  k_iota<<<grid_for(T, 256), 256, 0, h->stream>>>(vals_in.p, T);
+  int bits = 1;
+  while ((1LL << bits) < (long long)nkeys) ++bits;
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_keys, keys_out.p, vals_in.p, slots.p,
+                                     (int)T, 0, bits, h->stream));
+  DBuf<unsigned char> tmp;
+  tmp.alloc(tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, d_keys, keys_out.p, vals_in.p, slots.p,
+                                     (int)T, 0, bits, h->stream));
+  k_csr_starts<<<(int)((T + 1 + 255) / 256), 256, 0, h->stream>>>(keys_out.p, T, nkeys, start.p);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+static void reset_scalars(pcd_handle* h) {
+  Scalars s{};
+  s.first_changed = ~0ull;
+  s.err_nonfinite = ~0ull;
+  s.err_infeasible = ~0ull;
+  *h->h_scal = s;
+  CK(cudaMemcpyAsync(h->scal, h->h_scal, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
+}
+
+static void read_scalars(pcd_handle* h) {
+  CK(cudaMemcpyAsync(h->h_scal, h->scal, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+struct IterOut {
+  int64_t changed = 0, first_changed = -1, conflicts = 0, mismatch_delta = 0;
+  int64_t max_evals = 0, total_evals = 0;
+};
+
+// Events used for the per-phase device timing (pcd_timing).
+struct PhaseTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit PhaseTimer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~PhaseTimer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+  void start() { cudaEventRecord(a, s); }
+  double stop_ms() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+};
+
+template <int KIND>
+static void launch_product_sweep(pcd_handle* h, int lo, int hi, long long* evals_out) {
+  SweepArgs a{};
+  a.model = h->model();
+  a.M = h->M; a.J = h->J; a.lo = lo; a.hi = hi;
+  a.pstart = h->pstart.p; a.pslots = h->pslots.p;
+  a.ckcap = h->ckcap.p; a.hck = h->hck.p; a.ev = h->ev.p; a.xloc = h->xloc.p;
+  a.cache = h->cache.p; a.written = h->written.p; a.ref = h->ref.n ? h->ref.p : nullptr;
+  a.scal = h->scal; a.evals_out = evals_out;
+  const int wpb = 4;
+  const size_t smem = warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
+  static bool attr_set[4] = {false, false, false, false};
+  if (smem > 48 * 1024 && !attr_set[KIND]) {
+    CK(cudaFuncSetAttribute(k_sweep_product<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set[KIND] = true;
+  }
+  k_sweep_product<KIND><<<(h->M + wpb - 1) / wpb, wpb * 32, smem, h->stream>>>(a);
+  CK(cudaGetLastError());
+}
+
+template <int KIND>
+static void launch_replay_sweep(pcd_handle* h, int lo, int hi, long long* evals_out) {
+  const size_t per = (size_t)h->I * h->J;
+  const size_t budget = (size_t)512 << 20;  // bytes of private state in flight
+  int batch = (int)std::max<size_t>(1, std::min<size_t>((size_t)h->M, budget / std::max<size_t>(1, per * 4)));
+  h->scratch.alloc(std::max<size_t>(1, per * (size_t)batch));
+  const int wpb = 4;
+  const size_t smem = warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
+  static bool attr_set[4] = {false, false, false, false};
+  if (smem > 48 * 1024 && !attr_set[KIND]) {
+    CK(cudaFuncSetAttribute(k_sweep_replay<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set[KIND] = true;
+  }
+  for (int m0 = 0; m0 < h->M; m0 += batch) {
+    ReplayArgs a{};
+    a.model = h->model();
+    a.M = h->M; a.J = h->J; a.I = h->I; a.lo = lo; a.hi = hi; a.m0 = m0;
+    a.m1 = std::min(h->M, m0 + batch);
+    a.owner = h->owner.p; a.pstart = h->pstart.p; a.pslots = h->pslots.p;
+    a.ckcap = h->ckcap.p; a.ckinv = h->ckinv.p; a.cache = h->cache.p; a.fresh = h->fresh.p;
+    a.scratch = h->scratch.p; a.scal = h->scal; a.evals_out = evals_out;
+    const int nproc = a.m1 - a.m0;
+    k_sweep_replay<KIND><<<(nproc + wpb - 1) / wpb, wpb * 32, smem, h->stream>>>(a);
+    CK(cudaGetLastError());
+  }
+}
+
+template <typename F>
+static void dispatch_kind(int kind, F&& f) {
+  switch (kind) {
+    case kGreedy: f(std::integral_constant<int, kGreedy>{}); break;
+    case kCapacity: f(std::integral_constant<int, kCapacity>{}); break;
+    case kDual: f(std::integral_constant<int, kDual>{}); break;
+    default: f(std::integral_constant<int, kNull>{}); break;
+  }
+}
+
+static void throw_sweep_error(pcd_handle* h) {
+  const Scalars& s = *h->h_scal;
+  if (s.err_nonfinite == ~0ull && s.err_infeasible == ~0ull) return;
+  if (s.err_nonfinite <= s.err_infeasible) {
+    const int64_t t = (int64_t)(s.err_nonfinite & 0xffffffffull);
+    throw ContractViolation("dual network produced a non-finite score", t);
+  }
+  const int64_t t = (int64_t)(s.err_infeasible & 0xffffffffull);
+  throw ContractViolation("policy returned an infeasible action at t=" + std::to_string(t), t);
+}
+
+// One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
+static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out) {
+  IterOut out;
+  const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
+  reset_scalars(h);
+  if (W <= 0) return out;
+  PhaseTimer tm(h->stream);
+  if (engine == PCD_ENGINE_PRODUCT) {
+    tm.start();
+    const int J = h->J;
+    const int tpb = std::max(1, std::min(128, (int)((40 * 1024) / (4 * std::max(1, J)))));
+    k_effective<<<(h->I + tpb - 1) / tpb, tpb, (size_t)tpb * J * 4, h->stream>>>(
+        h->qstart.p, h->qslots.p, h->I, lo, hi, h->cache.p, h->ckinv.p, J, h->ev.p);
+    const int nb = (W + kK - 1) >> kLogK;
+    k_block_hist<<<nb, 128, (size_t)J * 4, h->stream>>>(h->ev.p, lo, W, J, h->hck.p);
+    const int nseg = (nb + kSegRows - 1) / kSegRows;
+    k_seg_sums<<<nseg, 128, 0, h->stream>>>(h->hck.p, nb, J, h->seg.p);
+    k_seg_scan<<<1, 128, 0, h->stream>>>(h->seg.p, nseg, J);
+    k_seg_apply<<<nseg, 128, 0, h->stream>>>(h->hck.p, nb, J, h->seg.p);
+    CK(cudaMemcpyAsync(h->xloc.p, h->ckinv.p, sizeof(int) * (size_t)h->I * J, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaGetLastError());
+    h->timing.prep_ms += tm.stop_ms();
+    h->timing.kernel_launches += 6;
+    tm.start();
+    dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
+    h->timing.sweep_ms += tm.stop_ms();
+    h->timing.kernel_launches += 1;
+    h->timing.sweep_launches += 1;
+  } else {
+    tm.start();
+    dispatch_kind(h->kind, [&](auto k) { launch_replay_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
+    h->timing.sweep_ms += tm.stop_ms();
+    h->timing.sweep_launches += 1;
+    h->timing.kernel_launches += 1;
+    // errors surface before publishing (the reference throws out of the sweep)
+    read_scalars(h);
+    throw_sweep_error(h);
+    tm.start();
+    k_publish<<<grid_for(W, 256), 256, 0, h->stream>>>(h->fresh.p, h->cache.p, h->written.p,
+                                                        h->ref.n ? h->ref.p : nullptr, lo, hi, h->scal);
+    CK(cudaGetLastError());
+    h->timing.publish_ms += tm.stop_ms();
+    h->timing.kernel_launches += 1;
+  }
+  read_scalars(h);
+  throw_sweep_error(h);
+  const Scalars& s = *h->h_scal;
+  out.changed = (int64_t)s.changed;
+  out.first_changed = s.changed ? (int64_t)s.first_changed : -1;
+  out.conflicts = (int64_t)s.conflicts;
+  out.mismatch_delta = (int64_t)s.mismatch_delta;
+  out.max_evals = (int64_t)s.max_evals;
+  out.total_evals = (int64_t)s.total_evals;
+  return out;
+}
+
+static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to) {
+  if (to <= from) return;
+  PhaseTimer tm(h->stream);
+  tm.start();
+  const size_t IJ = (size_t)h->I * h->J;
+  CK(cudaMemcpyAsync(h->ckbak.p, h->ckinv.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->ckbak.p + IJ, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  k_advance<<<grid_for(to - from, 256), 256, (size_t)h->J * 4, h->stream>>>(
+      h->cache.p, h->product.p, (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p);
+  CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
+  k_advance_check<<<grid_for(std::max<long long>((long long)IJ, to - from), 256), 256, 0, h->stream>>>(
+      h->cache.p, (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p, (long long)IJ, h->scal);
+  CK(cudaGetLastError());
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->timing.advance_ms += tm.stop_ms();
+  h->timing.kernel_launches += 2;
+  if (flag) {
+    CK(cudaMemcpyAsync(h->ckinv.p, h->ckbak.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->ckcap.p, h->ckbak.p + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+    k_advance_serial<<<1, 1, 0, h->stream>>>(h->cache.p, h->product.p, h->order_t.n ? h->order_t.p : nullptr,
+                                             (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p, h->d_errt);
+    long long et = -1;
+    CK(cudaMemcpyAsync(&et, h->d_errt, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    throw ContractViolation("infeasible fulfillment at t=" + std::to_string(et), et);
+  }
+}
+
+static int choose_engine(pcd_handle* h, int requested) {
+  if (requested == PCD_ENGINE_REPLAY) return PCD_ENGINE_REPLAY;
+  if (requested == PCD_ENGINE_PRODUCT) {
+    if (!h->is_product)
+      throw InvalidArgument("engine=PRODUCT requires a product partition (each product on one process)");
+    return PCD_ENGINE_PRODUCT;
+  }
+  return h->is_product ? PCD_ENGINE_PRODUCT : PCD_ENGINE_REPLAY;
+}
+
+static void ensure_state_buffers(pcd_handle* h) {
+  const size_t T = (size_t)std::max<int64_t>(h->T, 1);
+  const size_t IJ = std::max<size_t>(1, (size_t)h->I * h->J);
+  h->cache.alloc(T);
+  h->fresh.alloc(T);
+  h->ev.alloc(T);
+  h->written.alloc(T);
+  h->ckcap.alloc(std::max(1, h->J));
+  h->ckinv.alloc(IJ);
+  h->ckbak.alloc(IJ + h->J);
+  h->xloc.alloc(IJ);
+  const size_t nb = (T + kK - 1) / kK;
+  h->hck.alloc(nb * std::max(1, h->J));
+  h->seg.alloc(((nb + kSegRows - 1) / kSegRows + 1) * std::max(1, h->J));
+  h->evals.alloc(std::max(1, h->M));
+}
+
+// picard_simulate (engine.hpp:458-590) over the resident cache.
+static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_result* res,
+                     pcd_trace_row* trace, int64_t trace_cap) {
+  const int64_t T = h->T;
+  *res = pcd_result{0, -1, 0, 0, 0, 0, 0, -1};
+  if (!h->have_plan) throw InvalidArgument("no partition plan set (pcd_set_plan)");
+  if (cfg->processes != 0 && cfg->processes != h->M)
+    throw ContractViolation("config process count disagrees with the plan");
+  if (cfg->max_steps < 0 || cfg->max_iterations < 0)
+    throw ContractViolation("picard config values must be non-negative");
+  const int engine = choose_engine(h, cfg->engine);
+  h->timing = pcd_timing{};
+  h->timing.engine_used = engine;
+  h->timing.device = h->device;
+  const int64_t cap_it = cfg->max_iterations > 0 ? cfg->max_iterations : 2 * T + 4;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, h->stream));
+  // checkpoint = initial state; written = 0
+  CK(cudaMemcpyAsync(h->ckcap.p, h->cap0.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->ckinv.p, h->inv0.p, sizeof(int) * (size_t)h->I * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  if (T) CK(cudaMemsetAsync(h->written.p, 0, (size_t)T, h->stream));
+  int64_t mismatches = 0;
+  if (track) {
+    reset_scalars(h);
+    k_mismatches<<<grid_for(T, 256), 256, 0, h->stream>>>(h->cache.p, h->ref.p, T, h->scal);
+    read_scalars(h);
+    mismatches = h->h_scal->mismatches;
+    if (mismatches == 0) res->iterations_to_correct = 0;
+  }
+  std::vector<pcd_trace_row> rows;
+  int64_t ws = 0, iteration = 0, episodes = 0;
+  while (ws < T) {
+    const int64_t we = cfg->max_steps > 0 ? std::min(T, ws + cfg->max_steps) : T;
+    if (iteration >= cap_it) {
+      res->iterations_run = iteration;
+      res->trace_rows = (int64_t)rows.size();
+      throw IterationLimit("picard iteration cap exceeded (" + std::to_string(cap_it) +
+                               "); the policy may be nondeterministic",
+                           iteration, rows);
+    }
+    ++iteration;
+    IterOut it = run_iteration(h, engine, ws, we, nullptr);
+    res->iterations_to_converged += 1;
+    res->policy_eval_count_sequential_equivalent += it.max_evals;
+    res->total_policy_evals += it.total_evals;
+    res->conflicts += it.conflicts;
+    mismatches += it.mismatch_delta;
+    if (cfg->record_trace) rows.push_back({episodes, iteration, it.changed, it.max_evals, ws});
+    if (track && res->iterations_to_correct < 0 && mismatches == 0) res->iterations_to_correct = iteration;
+    if (h->history && iteration - 1 < h->history_cap && T)
+      CK(cudaMemcpy(h->history + (iteration - 1) * T, h->cache.p, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    h->timing.steps_critical += it.max_evals;
+    h->timing.total_evals += it.total_evals;
+    if (it.changed == 0) {
+      advance_checkpoint(h, ws, we);
+      ws = we;
+      ++episodes;
+    } else if (it.first_changed > ws) {
+      advance_checkpoint(h, ws, it.first_changed);
+      ws = it.first_changed;
+    }
+  }
+  CK(cudaEventRecord(e1, h->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  h->timing.total_ms = ms;
+  h->timing.iterations = iteration;
+  res->iterations_run = iteration;
+  res->trace_rows = (int64_t)rows.size();
+  for (int64_t i = 0; i < (int64_t)rows.size() && i < trace_cap; ++i) trace[i] = rows[(size_t)i];
+}
+
+}  // namespace pcd
+
+// ============================================================== C ABI (device)
+using namespace pcd;
+
+namespace pcd {
+int translate_exception();  // capi.cpp
+}
+
+#define PCD_TRY try {
+#define PCD_CATCH \
+  }               \
+  catch (...) { return pcd::translate_exception(); }
+
+extern "C" int pcd_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+static void validate_instance(const pcd_instance* in) {
+  if (!in) throw InvalidArgument("instance is null");
+  if (in->nodes < 1) throw InvalidArgument("instance needs at least one node");
+  if (in->nodes > 32767) throw InvalidArgument("node count above 32767 is not supported");
+  if (in->products < 1) throw InvalidArgument("product count must be >= 1");
+  if (in->horizon < 0 || in->horizon > 0x7ffffff0LL) throw InvalidArgument("horizon out of range");
+  if (in->horizon > 0 && (!in->product || !in->reward_row || !in->reward_table))
+    throw InvalidArgument("instance arrays missing");
+  if (!in->capacity || !in->inventory) throw InvalidArgument("instance state missing");
+  for (int64_t t = 0; t < in->horizon; ++t) {
+    if (in->product[t] < 0 || in->product[t] >= in->products)
+      throw InvalidArgument("order product out of range at t=" + std::to_string(t));
+    if (in->reward_row[t] < 0 || in->reward_row[t] >= in->reward_rows)
+      throw InvalidArgument("reward row out of range at t=" + std::to_string(t));
+  }
+  for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i)
+    if (!std::isfinite(in->reward_table[i])) throw InvalidArgument("rewards must be finite");
+}
+
+extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t device, pcd_handle** out) {
+  PCD_TRY
+  if (!out) throw InvalidArgument("out is null");
+  *out = nullptr;
+  validate_instance(in);
+  if (!pol) throw InvalidArgument("policy is null");
+  if (pol->kind < 0 || pol->kind > 3) throw InvalidArgument("unknown policy kind");
+  if (pol->kind == PCD_POLICY_CAPACITY && !std::isfinite(pol->gamma)) throw InvalidArgument("gamma must be finite");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw CudaError("no CUDA device available: the B200 engine has no CPU fallback");
+  }
+  if (device < 0 || device >= ndev) throw InvalidArgument("device index out of range");
+  CK(cudaSetDevice(device));
+  auto h = std::make_unique<pcd_handle>();
+  h->device = device;
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->J = in->nodes; h->I = in->products; h->T = in->horizon; h->R = in->reward_rows;
+  h->tanh_fma = host_tanh_fma();
+  const size_t T = (size_t)h->T, J = (size_t)h->J, IJ = (size_t)h->I * J;
+  cudaStream_t s = h->stream;
+  h->product.upload(in->product, T, s);
+  if (in->order_t) h->order_t.upload(in->order_t, T, s);
+  h->rrow.upload(in->reward_row, T, s);
+  h->rtab.upload(in->reward_table, (size_t)h->R * J, s);
+  h->cap0.upload(in->capacity, J, s);
+  h->inv0.upload(in->inventory, IJ, s);
+  h->kind = pol->kind;
+  h->gamma = pol->gamma;
+  h->H = pol->hidden > 0 ? pol->hidden : 64;
+  if (pol->kind == PCD_POLICY_DUAL) {
+    if (!pol->w1 || !pol->b1 || !pol->w2 || !pol->b2 || !pol->w3 || !pol->b3)
+      throw InvalidArgument("dual network: parameters missing");
+    const int inw = 2 * h->J + 1, outw = 2 * h->J, H = h->H;
+    DBuf<double> tmp;
+    auto upload_t = [&](const double* src, int rows, int cols, DBuf<double>& dst) {
+      tmp.upload(src, (size_t)rows * cols, s);
+      dst.alloc((size_t)rows * cols);
+      k_transpose_f64<<<(rows * cols + 255) / 256, 256, 0, s>>>(tmp.p, rows, cols, dst.p);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));
+    };
+    upload_t(pol->w1, H, inw, h->w1t);
+    upload_t(pol->w2, H, H, h->w2t);
+    upload_t(pol->w3, outw, H, h->w3t);
+    h->b1.upload(pol->b1, H, s);
+    h->b2.upload(pol->b2, H, s);
+    h->b3.upload(pol->b3, outw, s);
+    if (pol->init_capacity) {
+      h->pcap0.upload(pol->init_capacity, J, s);
+      h->pinv0.upload(pol->init_inventory ? pol->init_inventory : in->inventory, IJ, s);
+    } else {
+      h->pcap0.upload(in->capacity, J, s);
+      h->pinv0.upload(in->inventory, IJ, s);
+    }
+    h->p_horizon = pol->horizon >= 0 ? pol->horizon : in->horizon;
+  }
+  CK(cudaMalloc(&h->scal, sizeof(Scalars)));
+  CK(cudaMallocHost(&h->h_scal, sizeof(Scalars)));
+  CK(cudaMalloc(&h->d_errt, sizeof(long long)));
+  CK(cudaStreamSynchronize(s));
+  *out = h.release();
+  return PCD_OK;
+  PCD_CATCH
+}
+
+extern "C" void pcd_destroy(pcd_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  delete h;
+}
+
+extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
+  PCD_TRY
+  if (!h) throw InvalidArgument("handle is null");
+  CK(cudaSetDevice(h->device));
+  // PartitionPlan::validate (engine.hpp:82-95)
+  if (M < 1) throw ContractViolation("partition plan: process count must be >= 1");
+  if (h->T > 0 && !owner) throw ContractViolation("partition plan does not cover the horizon");
+  for (int64_t t = 0; t < h->T; ++t)
+    if (owner[t] < 0 || owner[t] >= M) throw ContractViolation("partition plan: owner out of range", t);
+  h->M = M;
+  h->h_owner.assign(owner, owner + h->T);
+  h->owner.upload(owner, (size_t)h->T, h->stream);
+  build_csr(h, h->owner.p, M, h->pstart, h->pslots);
+  build_csr(h, h->product.p, h->I, h->qstart, h->qslots);
+  int* flag;
+  CK(cudaMalloc(&flag, sizeof(int)));
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  if (h->T > 0)
+    k_check_product_partition<<<grid_for(h->T, 256), 256, 0, h->stream>>>(h->owner.p, h->product.p, h->qstart.p,
+                                                                        h->qslots.p, h->T, flag);
+  int hf = 0;
+  CK(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFree(flag);
+  h->is_product = hf == 0;
+  h->have_plan = true;
+  ensure_state_buffers(h);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+static void upload_cache_ref(pcd_handle* h, const int32_t* initial_cache, const int32_t* reference) {
+  ensure_state_buffers(h);
+  const size_t T = (size_t)h->T;
+  if (initial_cache) CK(cudaMemcpyAsync(h->cache.p, initial_cache, T * 4, cudaMemcpyHostToDevice, h->stream));
+  else k_fill<<<grid_for((long long)T, 256), 256, 0, h->stream>>>(h->cache.p, -1, (long long)T);
+  if (reference) {
+    h->ref.alloc(std::max<size_t>(T, 1));
+    CK(cudaMemcpyAsync(h->ref.p, reference, T * 4, cudaMemcpyHostToDevice, h->stream));
+  } else if (h->ref.p) {
+    cudaFree(h->ref.p);
+    h->ref.p = nullptr;
+    h->ref.n = 0;
+  }
+  CK(cudaGetLastError());
+}
+
+extern "C" int pcd_upload_cache(pcd_handle* h, const int32_t* initial_cache, const int32_t* reference) {
+  PCD_TRY
+  if (!h) throw InvalidArgument("handle is null");
+  if (!h->have_plan) throw InvalidArgument("no partition plan set (pcd_set_plan)");
+  CK(cudaSetDevice(h->device));
+  upload_cache_ref(h, initial_cache, reference);
+  CK(cudaStreamSynchronize(h->stream));
+  h->resident_valid = true;
+  return PCD_OK;
+  PCD_CATCH
+}
+
+static int fill_limit(pcd_result* res, pcd_trace_row* trace, int64_t trace_cap, const IterationLimit& e) {
+  res->iterations_run = e.iterations_run;
+  res->trace_rows = (int64_t)e.partial_trace.size();
+  for (int64_t i = 0; i < (int64_t)e.partial_trace.size() && i < trace_cap; ++i) trace[i] = e.partial_trace[(size_t)i];
+  set_last_error(e.what());
+  return PCD_ITERATION_LIMIT;
+}
+
+extern "C" int pcd_simulate(pcd_handle* h, const pcd_config* cfg, const int32_t* initial_cache,
+                            const int32_t* reference, int32_t* actions_out, pcd_result* res,
+                            pcd_trace_row* trace, int64_t trace_cap) {
+  pcd_result dummy;
+  if (!res) res = &dummy;
+  *res = pcd_result{0, -1, 0, 0, 0, 0, 0, -1};
+  PCD_TRY
+  if (!h || !cfg) throw InvalidArgument("null argument");
+  if (!h->have_plan) throw InvalidArgument("no partition plan set (pcd_set_plan)");
+  CK(cudaSetDevice(h->device));
+  upload_cache_ref(h, initial_cache, reference);
+  try {
+    simulate(h, cfg, reference != nullptr, res, trace, trace_cap);
+  } catch (const IterationLimit& e) {
+    return fill_limit(res, trace, trace_cap, e);
+  } catch (const ContractViolation& e) {
+    res->error_time_step = e.time_step;
+    throw;
+  }
+  if (actions_out && h->T)
+    CK(cudaMemcpyAsync(actions_out, h->cache.p, (size_t)h->T * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return PCD_OK;
+  PCD_CATCH
+}
+
+extern "C" int pcd_simulate_resident(pcd_handle* h, const pcd_config* cfg, int32_t use_initial_cache,
+                                     int32_t use_reference, pcd_result* res, pcd_trace_row* trace,
+                                     int64_t trace_cap) {
+  pcd_result dummy;
+  if (!res) res = &dummy;
+  *res = pcd_result{0, -1, 0, 0, 0, 0, 0, -1};
+  PCD_TRY
+  if (!h || !cfg) throw InvalidArgument("null argument");
+  if (!h->have_plan) throw InvalidArgument("no partition plan set (pcd_set_plan)");
+  CK(cudaSetDevice(h->device));
+  ensure_state_buffers(h);
+  if (!use_initial_cache)
+    k_fill<<<grid_for(h->T, 256), 256, 0, h->stream>>>(h->cache.p, -1, (long long)h->T);
+  else if (!h->resident_valid)
+    throw InvalidArgument("no resident initial cache (pcd_upload_cache)");
+  if (use_reference && !h->ref.n) throw InvalidArgument("no resident reference (pcd_upload_cache)");
+  h->resident_valid = false;  // the cache is overwritten by the run
+  try {
+    simulate(h, cfg, use_reference != 0, res, trace, trace_cap);
+  } catch (const IterationLimit& e) {
+    return fill_limit(res, trace, trace_cap, e);
+  } catch (const ContractViolation& e) {
+    res->error_time_step = e.time_step;
+    throw;
+  }
+  return PCD_OK;
+  PCD_CATCH
+}
+
+extern "C" int pcd_download_actions(pcd_handle* h, int32_t* actions_out) {
+  PCD_TRY
+  if (!h || !actions_out) throw InvalidArgument("null argument");
+  CK(cudaSetDevice(h->device));
+  if (h->T) CK(cudaMemcpyAsync(actions_out, h->cache.p, (size_t)h->T * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return PCD_OK;
+  PCD_CATCH
+}
+
+extern "C" int pcd_iterate_once(pcd_handle* h, int32_t engine, int32_t* cache, int64_t t_lo, int64_t t_hi,
+                                const int32_t* ckpt_capacity, const int32_t* ckpt_inventory,
+                                int64_t* evals_per_process, int64_t* changed_slots, int64_t* n_changed) {
+  PCD_TRY
+  if (!h || !cache) throw InvalidArgument("null argument");
+  if (!h->have_plan) throw InvalidArgument("no partition plan set (pcd_set_plan)");
+  if (t_lo < 0 || t_hi > h->T) throw InvalidArgument("window outside the horizon");
+  CK(cudaSetDevice(h->device));
+  ensure_state_buffers(h);
+  const int eng = choose_engine(h, engine);
+  const size_t T = (size_t)h->T;
+  std::vector<int32_t> before(cache, cache + T);
+  CK(cudaMemcpyAsync(h->cache.p, cache, T * 4, cudaMemcpyHostToDevice, h->stream));
+  if (ckpt_capacity) CK(cudaMemcpyAsync(h->ckcap.p, ckpt_capacity, sizeof(int) * h->J, cudaMemcpyHostToDevice, h->stream));
+  else CK(cudaMemcpyAsync(h->ckcap.p, h->cap0.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  if (ckpt_inventory) CK(cudaMemcpyAsync(h->ckinv.p, ckpt_inventory, sizeof(int) * (size_t)h->I * h->J, cudaMemcpyHostToDevice, h->stream));
+  else CK(cudaMemcpyAsync(h->ckinv.p, h->inv0.p, sizeof(int) * (size_t)h->I * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  if (T) CK(cudaMemsetAsync(h->written.p, 0, T, h->stream));
+  CK(cudaMemsetAsync(h->evals.p, 0, sizeof(long long) * h->M, h->stream));
+  DBuf<int> saved_ref;  // iterate_once has no reference
+  std::swap(saved_ref.p, h->ref.p);
+  std::swap(saved_ref.n, h->ref.n);
+  try {
+    run_iteration(h, eng, t_lo, t_hi, h->evals.p);
+  } catch (...) {
+    std::swap(saved_ref.p, h->ref.p);
+    std::swap(saved_ref.n, h->ref.n);
+    throw;
+  }
+  std::swap(saved_ref.p, h->ref.p);
+  std::swap(saved_ref.n, h->ref.n);
+  if (T) CK(cudaMemcpyAsync(cache, h->cache.p, T * 4, cudaMemcpyDeviceToHost, h->stream));
+  std::vector<long long> ev((size_t)h->M, 0);
+  k_window_evals<<<(h->M + 255) / 256, 256, 0, h->stream>>>(h->pstart.p, h->pslots.p, h->M, (int)t_lo,
+                                                             (int)t_hi, h->evals.p);
+  CK(cudaMemcpyAsync(ev.data(), h->evals.p, sizeof(long long) * h->M, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (evals_per_process)
+    for (int32_t m = 0; m < h->M; ++m) evals_per_process[m] = ev[(size_t)m];
+  int64_t n = 0;
+  for (int64_t t = std::max<int64_t>(t_lo, 0); t < t_hi; ++t)
+    if (before[(size_t)t] != cache[t]) {
+      if (changed_slots) changed_slots[n] = t;
+      ++n;
+    }
+  if (n_changed) *n_changed = n;
+  return PCD_OK;
+  PCD_CATCH
+}
+
+extern "C" int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* policy_evals) {
+  PCD_TRY
+  if (!h) throw InvalidArgument("handle is null");
+  CK(cudaSetDevice(h->device));
+  // Prop. 1: the Picard fixed point is the serial trajectory.
+  const int32_t M = std::max(1, std::min<int32_t>(h->I, 8192));
+  std::vector<int32_t> owner((size_t)h->T);
+  std::vector<int32_t> prod((size_t)h->T);
+  CK(cudaMemcpy(prod.data(), h->product.p, (size_t)h->T * 4, cudaMemcpyDeviceToHost));
+  product_partition(prod.data(), h->T, h->I, M, 1, owner.data());
+  // save / restore any user plan
+  const bool had = h->have_plan;
+  std::vector<int32_t> saved = h->h_owner;
+  const int32_t savedM = h->M;
+  int rc = pcd_set_plan(h, owner.data(), M);
+  if (rc) return rc;
+  pcd_config cfg{0, 0, 0, 0, 1, PCD_ENGINE_PRODUCT};
+  pcd_result res;
+  rc = pcd_simulate(h, &cfg, nullptr, nullptr, actions_out, &res, nullptr, 0);
+  if (rc == PCD_CONTRACT_VIOLATION) {
+    // A Picard sweep may evaluate the policy at non-serial states; reproduce
+    // the serial error exactly with the single-process fixed point.
+    std::vector<int32_t> one((size_t)h->T, 0);
+    pcd_set_plan(h, one.data(), 1);
+    rc = pcd_simulate(h, &cfg, nullptr, nullptr, actions_out, &res, nullptr, 0);
+  }
+  if (had) pcd_set_plan(h, saved.data(), savedM);
+  if (policy_evals) *policy_evals = h->T;
+  return rc;
+  PCD_CATCH
+}
+
+extern "C" int pcd_set_history(pcd_handle* h, int32_t* history, int64_t cap_iterations) {
+  if (!h) return PCD_INVALID_ARGUMENT;
+  h->history = history;
+  h->history_cap = history ? cap_iterations : 0;
+  return PCD_OK;
+}
+
+extern "C" int pcd_last_timing(const pcd_handle* h, pcd_timing* out) {
+  if (!h || !out) return PCD_INVALID_ARGUMENT;
+  *out = h->timing;
+  return PCD_OK;
+}
+
+extern "C" int pcd_picard_simulate(const pcd_instance* inst, const pcd_policy* policy, const int32_t* owner,
+                                   int32_t processes, const pcd_config* cfg, const int32_t* initial_cache,
+                                   const int32_t* reference, int32_t* actions_out, pcd_result* result,
+                                   pcd_trace_row* trace, int64_t trace_cap) {
+  pcd_handle* h = nullptr;
+  int rc = pcd_create(inst, policy, 0, &h);
+  if (rc) return rc;
+  rc = pcd_set_plan(h, owner, processes);
+  if (rc == PCD_OK) rc = pcd_simulate(h, cfg, initial_cache, reference, actions_out, result, trace, trace_cap);
+  pcd_destroy(h);
+  return rc;
+}
+
+extern "C" int pcd_nccl_unique_id(unsigned char out[128]) {
+  PCD_TRY
+  if (!g_nccl.load()) throw CudaError("libnccl.so.2 could not be loaded");
+  nccl_unique_id id;
+  const int rc = g_nccl.GetUniqueId(&id);
+  if (rc != 0) throw CudaError(std::string("ncclGetUniqueId failed: ") + g_nccl.GetErrorString(rc));
+  std::memcpy(out, id.internal, 128);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+extern "C" int pcd_attach_comm(pcd_handle* h, const unsigned char id[128], int32_t rank, int32_t nranks) {
+  PCD_TRY
+  if (!h) throw InvalidArgument("handle is null");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("bad rank / nranks");
+  if (!g_nccl.load()) throw CudaError("libnccl.so.2 could not be loaded");
+  CK(cudaSetDevice(h->device));
+  nccl_unique_id uid;
+  std::memcpy(uid.internal, id, 128);
+  const int rc = g_nccl.CommInitRank(&h->comm, nranks, uid, rank);
+  if (rc != 0) throw CudaError(std::string("ncclCommInitRank failed: ") + g_nccl.GetErrorString(rc));
+  h->rank = rank;
+  h->nranks = nranks;
+  return PCD_OK;
+  PCD_CATCH
+}

@@ -1,0 +1,484 @@
+// kernels.cuh — sm_100a kernels of one Picard iteration (engine.hpp:358-444)
+// and of the fixed-point driver's checkpoint advance (engine.hpp:514-526).
+//
+// Device layout (SoA, HBM-resident for the whole run):
+//   product[T], rrow[T], order_t[T]       int32   the order tape
+//   rtab[R*J]                             f64     rewards, one row per origin
+//   owner[T]                              int32   PartitionPlan::owner
+//   pstart[M+1], pslots[T]                int32   per-process owned slots (time order)
+//   qstart[I+1], qslots[T]                int32   per-product slots (time order)
+//   cache[T], fresh[T], ref[T]            int32   ActionCache / fresh / oracle
+//   written[T]                            uint8   "slot written before" (conflicts)
+//   ckcap[J], ckinv[I*J]                  int32   checkpoint FoState (dense)
+//   xloc[I*J]                             int32   per-iteration own-product inventory
+//   ev[T]                                 int32   effective cached attempt (node or -1)
+//   hck[nb*J]                             int32   per-node prefix counts of ev every K slots
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device_policy.cuh"
+
+namespace pcd {
+
+constexpr int kLogK = 7;  // checkpoint stride K = 128 slots
+constexpr int kK = 1 << kLogK;
+constexpr int kSegRows = 256;  // checkpoint rows per scan segment
+
+struct Scalars {
+  unsigned long long changed;
+  unsigned long long first_changed;  // min
+  unsigned long long conflicts;
+  long long mismatch_delta;
+  unsigned long long max_evals;
+  unsigned long long total_evals;
+  unsigned long long err_nonfinite;  // min over (m << 32 | t)
+  unsigned long long err_infeasible; // min over (m << 32 | t)
+  int neg_flag;
+  int pad;
+  long long mismatches;              // full-cache mismatch count (init kernel)
+};
+
+__device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Effective-attempt pass (product-partition closed form).
+// For every product, walk its slots of the window in time order; the cached
+// attempt at slot t (node a) is *effective* iff fewer than ckinv[p][a]
+// earlier cached attempts of the same (product, node) exist in the window —
+// i.e. it would succeed inventory-wise with unlimited capacity.
+// ---------------------------------------------------------------------------
+__global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
+                            int lo, int hi, const int* __restrict__ cache,
+                            const int* __restrict__ ckinv, int J, int* __restrict__ ev) {
+  extern __shared__ int cnt_smem[];
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= I) return;
+  int* cnt = cnt_smem + threadIdx.x * J;
+  for (int j = 0; j < J; ++j) cnt[j] = 0;
+  const int beg = qstart[p], n = qstart[p + 1] - beg;
+  const int* sl = qslots + beg;
+  const int* x0 = ckinv + (size_t)p * J;
+  for (int k = lower_bound_i32(sl, n, lo); k < n; ++k) {
+    const int t = sl[k];
+    if (t >= hi) break;
+    const int a = cache[t];
+    int e = -1;
+    if (a >= 0 && a < J) {
+      e = cnt[a] < x0[a] ? a : -1;
+      cnt[a] += 1;
+    }
+    ev[t] = e;
+  }
+}
+
+// Per K-slot block histogram of effective attempts: hck[b][j].
+__global__ void k_block_hist(const int* __restrict__ ev, int lo, int W, int J, int* __restrict__ hck) {
+  extern __shared__ int hist[];
+  const int b = blockIdx.x;
+  for (int j = threadIdx.x; j < J; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+  const int s0 = b << kLogK;
+  for (int s = s0 + threadIdx.x; s < min(W, s0 + kK); s += blockDim.x) {
+    const int e = ev[lo + s];
+    if (e >= 0) atomicAdd(&hist[e], 1);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < J; j += blockDim.x) hck[(size_t)b * J + j] = hist[j];
+}
+
+// Column sums of each segment of kSegRows checkpoint rows.
+__global__ void k_seg_sums(const int* __restrict__ hck, int nb, int J, int* __restrict__ seg) {
+  const int s = blockIdx.x;
+  const int r0 = s * kSegRows, r1 = min(nb, r0 + kSegRows);
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    int acc = 0;
+    for (int r = r0; r < r1; ++r) acc += hck[(size_t)r * J + j];
+    seg[(size_t)s * J + j] = acc;
+  }
+}
+
+// Exclusive scan of the segment sums over segments, per column (one CTA).
+__global__ void k_seg_scan(int* __restrict__ seg, int nseg, int J) {
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      const int v = seg[(size_t)s * J + j];
+      seg[(size_t)s * J + j] = acc;
+      acc += v;
+    }
+  }
+}
+
+// In-segment exclusive scan plus the segment offset: hck[b][j] becomes the
+// number of effective attempts at node j in [lo, lo + b*K).
+__global__ void k_seg_apply(int* __restrict__ hck, int nb, int J, const int* __restrict__ seg) {
+  const int s = blockIdx.x;
+  const int r0 = s * kSegRows, r1 = min(nb, r0 + kSegRows);
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    int acc = seg[(size_t)s * J + j];
+    for (int r = r0; r < r1; ++r) {
+      const int v = hck[(size_t)r * J + j];
+      hck[(size_t)r * J + j] = acc;
+      acc += v;
+    }
+  }
+}
+
+struct SweepArgs {
+  DevModel model;
+  int M, J, lo, hi;
+  const int* pstart;
+  const int* pslots;
+  const int* ckcap;
+  const int* hck;
+  const int* ev;
+  int* xloc;
+  int* cache;
+  unsigned char* written;
+  const int* ref;
+  Scalars* scal;
+  long long* evals_out;  // optional [M]
+};
+
+__device__ __forceinline__ void carve_warp_smem(unsigned char* base, int warp, int J, int in, int H,
+                                                int out, int*& D, int*& crow, int*& prow,
+                                                WarpScratch& ws) {
+  const size_t ints = (size_t)3 * J;
+  const size_t ibytes = (ints * 4 + 15) & ~(size_t)15;
+  const size_t per = ibytes + (size_t)(in + 2 * H + out) * 8;
+  unsigned char* w = base + per * warp;
+  D = (int*)w;
+  crow = D + J;
+  prow = crow + J;
+  double* d = (double*)(w + ibytes);
+  ws.f = d;
+  ws.h1 = d + in;
+  ws.h2 = ws.h1 + H;
+  ws.pr = ws.h2 + H;
+}
+
+__host__ __device__ inline size_t warp_smem_bytes(int J, int in, int H, int out) {
+  const size_t ibytes = ((size_t)3 * J * 4 + 15) & ~(size_t)15;
+  return ibytes + (size_t)(in + 2 * H + out) * 8;
+}
+
+// ---------------------------------------------------------------------------
+// Closed-form sweep for product partitions (every product's slots belong to a
+// single process). One warp per process walks ONLY its own slots of the
+// window; the local state at own slot t is
+//   c[j] = max(0, ckcap[j] - H_t[j] + Hown_t[j] - F_t[j])
+//   x[p][j] = ckinv[p][j] - F_t[p][j]          (own product p)
+// where H_t = effective cached attempts in [lo,t) (hck + partial block scan),
+// Hown_t the effective attempts at own slots before t and F_t the process's
+// own fresh fulfilments before t. This equals the state the reference's
+// sweep_one_process (engine.hpp:299-342) reaches by replaying the window
+// (proof: DESIGN.md §4.2). The barrier publish (engine.hpp:434-443) and the
+// driver counters (engine.hpp:543-553) are fused in: each slot has exactly one
+// owner and no other process reads cache[t] after the effective pass.
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (m >= a.M) return;
+  const int J = a.J;
+  int *D, *crow, *prow;
+  WarpScratch ws;
+  carve_warp_smem(smem, warp, J, a.model.in, a.model.H, a.model.out, D, crow, prow, ws);
+  const int beg = a.pstart[m], n = a.pstart[m + 1] - beg;
+  const int* sl = a.pslots + beg;
+  int k = lower_bound_i32(sl, n, a.lo);
+  if (k >= n || sl[k] >= a.hi) return;
+  for (int j = lane; j < J; j += 32) D[j] = 0;
+  __syncwarp();
+  unsigned long long changed = 0, conflicts = 0, first = ~0ull, nev = 0;
+  long long mism = 0;
+  for (; k < n; ++k) {
+    const int t = sl[k];
+    if (t >= a.hi) break;
+    const int p = a.model.product[t];
+    const int aold = a.cache[t];
+    const int evt = a.ev[t];
+    const int b = (t - a.lo) >> kLogK;
+    const int* hb = a.hck + (size_t)b * J;
+    int* xrow = a.xloc + (size_t)p * J;
+    for (int j = lane; j < J; j += 32) {
+      crow[j] = a.ckcap[j] - hb[j] + D[j];
+      prow[j] = xrow[j];
+    }
+    __syncwarp();
+    for (int s = a.lo + (b << kLogK) + lane; s < t; s += 32) {
+      const int e = a.ev[s];
+      if (e >= 0) atomicSub(&crow[e], 1);
+    }
+    __syncwarp();
+    for (int j = lane; j < J; j += 32) crow[j] = max(crow[j], 0);
+    __syncwarp();
+    int nonfinite = 0;
+    const int anew = warp_policy_eval<KIND>(a.model, crow, prow, t, ws, lane, &nonfinite);
+    ++nev;
+    if (nonfinite) {
+      const int ot = a.model.order_t ? a.model.order_t[t] : t;
+      if (lane == 0) atomicMin(&a.scal->err_nonfinite, ((unsigned long long)m << 32) | (unsigned)ot);
+      break;
+    }
+    const bool infeasible = anew >= J || (anew >= 0 && !(crow[anew] > 0 && prow[anew] > 0));
+    __syncwarp();
+    if (infeasible) {
+      if (lane == 0) atomicMin(&a.scal->err_infeasible, ((unsigned long long)m << 32) | (unsigned)t);
+      break;
+    }
+    if (lane == 0) {
+      if (evt >= 0) D[evt] += 1;
+      if (anew >= 0) {
+        D[anew] -= 1;
+        xrow[anew] -= 1;
+      }
+      if (anew != aold) {
+        ++changed;
+        first = min(first, (unsigned long long)t);
+        conflicts += a.written[t] ? 1 : 0;
+      }
+      if (a.ref) mism += (long long)(anew != a.ref[t]) - (long long)(aold != a.ref[t]);
+      a.cache[t] = anew;
+      a.written[t] = 1;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (changed) {
+      atomicAdd(&a.scal->changed, changed);
+      atomicAdd(&a.scal->conflicts, conflicts);
+      atomicMin(&a.scal->first_changed, first);
+    }
+    if (mism) atomicAdd((unsigned long long*)&a.scal->mismatch_delta, (unsigned long long)mism);
+    atomicMax(&a.scal->max_evals, nev);
+    atomicAdd(&a.scal->total_evals, nev);
+    if (a.evals_out) a.evals_out[m] = (long long)nev;
+  }
+}
+
+struct ReplayArgs {
+  DevModel model;
+  int M, J, I, lo, hi, m0, m1;
+  const int* owner;
+  const int* pstart;
+  const int* pslots;
+  const int* ckcap;
+  const int* ckinv;
+  const int* cache;
+  int* fresh;
+  int* scratch;  // [(m1-m0) * I * J]
+  Scalars* scal;
+  long long* evals_out;
+};
+
+// ---------------------------------------------------------------------------
+// Exact replay sweep for ANY partition (sweep_one_process, engine.hpp:299-342):
+// one warp per process replays [lo, stop_after] against the frozen cache with
+// a private dense copy of the checkpoint state; fresh values go to fresh[t]
+// and are published by k_publish after all processes finished (the barrier).
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(128) k_sweep_replay(ReplayArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = a.m0 + blockIdx.x * (blockDim.x >> 5) + warp;
+  if (m >= a.m1) return;
+  const int J = a.J;
+  int *caps, *unused1, *unused2;
+  WarpScratch ws;
+  carve_warp_smem(smem, warp, J, a.model.in, a.model.H, a.model.out, caps, unused1, unused2, ws);
+  const int beg = a.pstart[m], n = a.pstart[m + 1] - beg;
+  const int* sl = a.pslots + beg;
+  const int k_hi = lower_bound_i32(sl, n, a.hi);
+  if (k_hi == 0 || sl[k_hi - 1] < a.lo) return;
+  const int stop = sl[k_hi - 1];
+  int* inv = a.scratch + (size_t)(m - a.m0) * a.I * J;
+  for (int j = lane; j < J; j += 32) caps[j] = a.ckcap[j];
+  for (size_t i = lane; i < (size_t)a.I * J; i += 32) inv[i] = a.ckinv[i];
+  __syncwarp();
+  unsigned long long nev = 0;
+  for (int t = a.lo; t <= stop; ++t) {
+    const int p = a.model.product[t];
+    int* row = inv + (size_t)p * J;
+    if (a.owner[t] == m) {
+      int nonfinite = 0;
+      const int anew = warp_policy_eval<KIND>(a.model, caps, row, t, ws, lane, &nonfinite);
+      ++nev;
+      if (nonfinite) {
+        const int ot = a.model.order_t ? a.model.order_t[t] : t;
+        if (lane == 0) atomicMin(&a.scal->err_nonfinite, ((unsigned long long)m << 32) | (unsigned)ot);
+        break;
+      }
+      const bool infeasible = anew >= J || (anew >= 0 && !(caps[anew] > 0 && row[anew] > 0));
+      __syncwarp();
+      if (infeasible) {
+        if (lane == 0) atomicMin(&a.scal->err_infeasible, ((unsigned long long)m << 32) | (unsigned)t);
+        break;
+      }
+      if (lane == 0) {
+        if (anew >= 0) { caps[anew] -= 1; row[anew] -= 1; }
+        a.fresh[t] = anew;
+      }
+    } else {
+      const int c = a.cache[t];
+      const bool ok = c >= 0 && c < J && caps[c] > 0 && row[c] > 0;
+      __syncwarp();
+      if (ok && lane == 0) { caps[c] -= 1; row[c] -= 1; }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicMax(&a.scal->max_evals, nev);
+    atomicAdd(&a.scal->total_evals, nev);
+    if (a.evals_out) a.evals_out[m] = (long long)nev;
+  }
+}
+
+// Barrier publish (engine.hpp:434-443) + driver counters (engine.hpp:543-553).
+__global__ void k_publish(const int* __restrict__ fresh, int* __restrict__ cache,
+                          unsigned char* __restrict__ written, const int* __restrict__ ref, int lo,
+                          int hi, Scalars* scal) {
+  unsigned long long changed = 0, conflicts = 0, first = ~0ull;
+  long long mism = 0;
+  for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
+    const int nw = fresh[t], od = cache[t];
+    if (nw != od) {
+      ++changed;
+      first = min(first, (unsigned long long)t);
+      conflicts += written[t] ? 1 : 0;
+      if (ref) mism += (long long)(nw != ref[t]) - (long long)(od != ref[t]);
+      cache[t] = nw;
+    }
+    written[t] = 1;
+  }
+  // warp reduce then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    conflicts += __shfl_xor_sync(0xffffffffu, conflicts, o);
+    mism += __shfl_xor_sync(0xffffffffu, mism, o);
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  }
+  if ((threadIdx.x & 31) == 0 && changed) {
+    atomicAdd(&scal->changed, changed);
+    atomicAdd(&scal->conflicts, conflicts);
+    atomicMin(&scal->first_changed, first);
+    if (mism) atomicAdd((unsigned long long*)&scal->mismatch_delta, (unsigned long long)mism);
+  }
+}
+
+__global__ void k_fill(int* p, int v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_mismatches(const int* __restrict__ cache, const int* __restrict__ ref, long long T, Scalars* scal) {
+  unsigned long long c = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x)
+    c += cache[t] != ref[t];
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)&scal->mismatches, c);
+}
+
+// Checkpoint advance (engine.hpp:514-526 -> apply_in_place, fo/types.hpp:89-100):
+// subtract the cache prefix's fulfilments from the checkpoint state.
+__global__ void k_advance(const int* __restrict__ cache, const int* __restrict__ product, int lo,
+                          int hi, int J, int* __restrict__ ckcap, int* __restrict__ ckinv) {
+  extern __shared__ int hcap[];
+  for (int j = threadIdx.x; j < J; j += blockDim.x) hcap[j] = 0;
+  __syncthreads();
+  for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
+    const int a = cache[t];
+    if (a >= 0 && a < J) {
+      atomicAdd(&hcap[a], 1);
+      atomicSub(&ckinv[(size_t)product[t] * J + a], 1);
+    }  // a >= J is infeasible: flagged by k_advance_check
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < J; j += blockDim.x)
+    if (hcap[j]) atomicSub(&ckcap[j], hcap[j]);
+}
+
+__global__ void k_advance_check(const int* __restrict__ cache, int lo, int hi, int J,
+                                const int* __restrict__ ckcap, const int* __restrict__ ckinv,
+                                long long IJ, Scalars* scal) {
+  int bad = 0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < J; i += stride) bad |= ckcap[i] < 0;
+  for (long long i = tid; i < IJ; i += stride) bad |= ckinv[i] < 0;
+  for (long long t = lo + tid; t < hi; t += stride) bad |= cache[t] >= J;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&scal->neg_flag, 1);
+}
+
+// Error path only: serial re-application to find the first infeasible order.
+__global__ void k_advance_serial(const int* __restrict__ cache, const int* __restrict__ product,
+                                 const int* __restrict__ order_t, int lo, int hi, int J,
+                                 int* __restrict__ ckcap, int* __restrict__ ckinv, long long* err_t) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  *err_t = -1;
+  for (int t = lo; t < hi; ++t) {
+    const int a = cache[t];
+    if (a < 0) continue;
+    int* row = ckinv + (size_t)product[t] * J;
+    if (a >= J || ckcap[a] <= 0 || row[a] <= 0) {
+      *err_t = order_t ? order_t[t] : t;
+      return;
+    }
+    ckcap[a] -= 1;
+    row[a] -= 1;
+  }
+}
+
+// Owned-slot counts per process inside [lo, hi) (evals_per_process).
+__global__ void k_window_evals(const int* __restrict__ pstart, const int* __restrict__ pslots, int M,
+                               int lo, int hi, long long* out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const int beg = pstart[m], n = pstart[m + 1] - beg;
+  out[m] = lower_bound_i32(pslots + beg, n, hi) - lower_bound_i32(pslots + beg, n, lo);
+}
+
+// Product-partition test: every slot's owner equals its product's first owner.
+__global__ void k_check_product_partition(const int* __restrict__ owner, const int* __restrict__ product,
+                                          const int* __restrict__ qstart, const int* __restrict__ qslots,
+                                          long long T, int* flag) {
+  int bad = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+    const int p = product[t];
+    bad |= owner[t] != owner[qslots[qstart[p]]];
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_iota(int* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = (int)i;
+}
+
+// CSR start offsets from sorted keys: start[k] = first index with key >= k.
+__global__ void k_csr_starts(const int* __restrict__ sorted_keys, long long T, int nkeys, int* __restrict__ start) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > T) return;
+  const int prev = i == 0 ? -1 : sorted_keys[i - 1];
+  const int cur = i == T ? nkeys : sorted_keys[i];
+  for (int k = prev + 1; k <= cur; ++k) start[k] = (int)i;
+}
+
+__global__ void k_transpose_f64(const double* __restrict__ src, int rows, int cols, double* __restrict__ dst) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * cols) return;
+  const int r = (int)(i / cols), c = (int)(i % cols);
+  dst[(size_t)c * rows + r] = src[i];
+}
+
+}  // namespace pcd

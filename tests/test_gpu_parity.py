@@ -1,0 +1,262 @@
+"""GPU parity tests proper: the sm_100a engine (through the C ABI) against the
+oracle and the reference's golden fixtures. Integer outputs (actions,
+iteration counts, conflicts, evaluation counters, trace rows, per-iteration
+caches) must be bit-exact; total reward is compared with rel. tol 1e-12
+(north_star allows 1e-4; the engine is exact so we hold it far tighter)."""
+from types import SimpleNamespace as NS
+
+import numpy as np
+import pytest
+
+import paper_2406_01939_b200 as P
+from oracle.oracle import ORC, OracleError
+from tests.helpers import (all_cases, load_golden, oracle_instance, oracle_policy, product_instance,
+                           product_policy)
+
+pytestmark = pytest.mark.gpu
+
+CASES = all_cases(load_golden())
+
+
+def run_gpu(case, engine="auto", history=True):
+    ons = oracle_instance(case["instance"], ORC)
+    inst = product_instance(ons)
+    pol = product_policy(case["policy"], inst)
+    plan = P.PartitionPlan(case["processes"], case["owner"])
+    cfg = P.PicardConfig(max_steps=case["config"]["max_steps"], record_trace=True, engine=engine)
+    init = case["initial_cache"]
+    with P.Simulator(inst, pol) as sim:
+        sim.set_plan(plan)
+        r = sim.simulate(cfg, init, case["sequential"], record_history=history)
+    return inst, r
+
+
+def check(case, r):
+    assert r.actions.tolist() == case["actions"]
+    assert r.iterations_to_converged == case["iterations_to_converged"]
+    assert r.iterations_to_correct == case["iterations_to_correct"]
+    assert r.conflicts == case["conflicts"]
+    assert r.policy_eval_count_sequential_equivalent == case["seq_equiv"]
+    assert r.total_policy_evals == case["total_evals"]
+    assert [list(x.astuple()) for x in r.trace] == case["trace"]
+    if case.get("history") is not None:
+        assert r.history.tolist() == case["history"]
+
+
+@pytest.mark.parametrize("name,case", CASES, ids=[n for n, _ in CASES])
+def test_engine_matches_reference_golden(name, case):
+    inst, r = run_gpu(case, "auto")
+    check(case, r)
+    assert abs(P.fo_total_reward(inst, r.actions) - case["total_reward"]) <= 1e-12 * max(1.0, abs(case["total_reward"]))
+
+
+@pytest.mark.parametrize("name,case", CASES[::3], ids=[n for n, _ in CASES[::3]])
+def test_replay_engine_matches_reference_golden(name, case):
+    _, r = run_gpu(case, "replay")
+    check(case, r)
+
+
+def test_product_engine_is_used_for_product_partitions(golden):
+    used = 0
+    for name, case in CASES:
+        owner = np.array(case["owner"])
+        prod = oracle_instance(case["instance"], ORC).product
+        is_pp = all(len(set(owner[prod == p])) <= 1 for p in set(prod.tolist()))
+        if not is_pp:
+            with pytest.raises(P.InvalidArgument):
+                run_gpu(case, "product", history=False)
+            continue
+        _, r = run_gpu(case, "product")
+        check(case, r)
+        assert r.timing["engine_used"] == 2
+        used += 1
+    assert used >= 20
+
+
+def test_toy_iterate_once_hand_trace(golden):
+    # test_engine.cpp:100-138
+    toy = P.Instance(2, 1, 2, [0, 0], [0, 1], [[0.9, 0.1], [0.8, 0.2]], [1, 1], [[1, 1]])
+    plan = P.PartitionPlan(2, [0, 1])
+    cache = np.full(2, -1, np.int32)
+    out = P.picard_iterate_once(toy, P.GreedyPolicy(), plan, cache, 0, 2)
+    assert cache.tolist() == [0, 0]
+    assert out.changed_slots.tolist() == [0, 1]
+    assert out.evals_per_process.tolist() == [1, 1]
+    P.picard_iterate_once(toy, P.GreedyPolicy(), plan, cache, 0, 2)
+    assert cache.tolist() == [0, 1]
+    assert P.sequential_simulate(toy, P.GreedyPolicy()).actions.tolist() == [0, 1]
+
+
+@pytest.mark.parametrize("engine", ["replay", "auto"])
+def test_iterate_once_random_caches_match_oracle(engine):
+    """Arbitrary (even garbage) caches, windows and checkpoints: one iteration
+    must reproduce picard_iterate_once exactly (engine.hpp:358-444)."""
+    rng = np.random.default_rng(17)
+    for seed in range(40):
+        J, I, T, beta, cov, s = ORC.small_random_params(700 + seed)
+        ons = NS(**ORC.generate_instance_arrays(J, I, T, beta, cov, s))
+        inst = product_instance(ons)
+        M = int(rng.integers(1, 6))
+        owner = ORC.product_partition(ons, M, seed) if seed % 2 == 0 else ORC.uniform_partition(T, M, seed)
+        kind = seed % 3
+        spec = dict(kind=kind, gamma=1.3, seed=seed)
+        opol = oracle_policy(spec, ons, ORC)
+        pol = product_policy(spec, inst)
+        cache = rng.integers(-3, J + 2, T).astype(np.int32)
+        lo = int(rng.integers(0, T))
+        hi = int(rng.integers(lo, T + 1))
+        # a feasible checkpoint: the state after a random feasible prefix
+        ck_cap = ons.capacity.copy()
+        ck_inv = ons.inventory.copy().reshape(I, J)
+        for t in range(lo):
+            a = int(rng.integers(-1, J))
+            p = ons.product[t]
+            if a >= 0 and ck_cap[a] > 0 and ck_inv[p, a] > 0:
+                ck_cap[a] -= 1
+                ck_inv[p, a] -= 1
+        want, want_evals, want_changed = ORC.iterate_once(ons, opol, owner, M, cache, lo, hi, ck_cap, ck_inv.ravel())
+        got = cache.copy()
+        out = P.picard_iterate_once(inst, pol, P.PartitionPlan(M, owner), got, lo, hi, ck_cap, ck_inv, engine)
+        assert got.tolist() == want.tolist(), (seed, engine)
+        assert out.evals_per_process.tolist() == want_evals.tolist()
+        assert out.changed_slots.tolist() == want_changed.tolist()
+
+
+def _dual_case(J, I, T, M, part, seed=7, theta=5, max_steps=0):
+    ons = NS(**ORC.generate_instance_arrays(J, I, T, 0.0, 0.8, seed, geometry=0 if J <= 30 else 1))
+    inst = product_instance(ons)
+    owner = ORC.product_partition(ons, M, 1) if part == "product" else ORC.uniform_partition(T, M, 1)
+    spec = dict(kind=2, gamma=0.0, seed=theta)
+    return ons, inst, owner, oracle_policy(spec, ons, ORC), product_policy(spec, inst)
+
+
+@pytest.mark.parametrize("J,I,T,M,part", [(10, 300, 20000, 512, "product"), (30, 200, 12000, 256, "product"),
+                                          (100, 40, 4000, 64, "product"), (10, 100, 6000, 64, "uniform"),
+                                          (1, 10, 10000, 16, "product")])
+def test_dual_policy_matches_oracle_counters(J, I, T, M, part):
+    ons, inst, owner, opol, pol = _dual_case(J, I, T, M, part)
+    seq, _ = ORC.sequential(ons, opol)
+    want = ORC.picard(ons, opol, owner, M, record_trace=True, reference=seq)
+    r = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(record_trace=True),
+                          reference_actions=seq)
+    assert r.actions.tolist() == seq.tolist()
+    assert r.iterations_to_converged == want.iterations_to_converged
+    assert r.iterations_to_correct == want.iterations_to_correct
+    assert r.conflicts == want.conflicts
+    assert r.policy_eval_count_sequential_equivalent == want.policy_eval_count_sequential_equivalent
+    assert r.total_policy_evals == want.total_policy_evals
+    assert [x.astuple() for x in r.trace] == [tuple(x) for x in want.trace]
+
+
+def test_sequential_drop_in_matches_oracle():
+    for J, I, T in ((10, 100, 5000), (40, 50, 3000)):
+        ons, inst, owner, opol, pol = _dual_case(J, I, T, 8, "product")
+        seq, _ = ORC.sequential(ons, opol)
+        out = P.sequential_simulate(inst, pol)
+        assert out.actions.tolist() == seq.tolist()
+        assert out.policy_evals == T
+
+
+def test_windowed_runs_and_warm_starts_match_oracle():
+    ons, inst, owner, opol, pol = _dual_case(10, 50, 3000, 32, "product")
+    seq, _ = ORC.sequential(ons, opol)
+    draft, _ = ORC.sequential(ons, NS(kind=1, hidden=64, gamma=2.0, horizon=None))
+    for ms in (1, 7, 300, 0):
+        for init in (None, draft):
+            want = ORC.picard(ons, opol, owner, 32, max_steps=ms, record_trace=True, reference=seq,
+                              initial_cache=init)
+            r = P.picard_simulate(inst, pol, P.PartitionPlan(32, owner),
+                                  P.PicardConfig(max_steps=ms, record_trace=True), init, seq)
+            assert r.actions.tolist() == seq.tolist()
+            assert [x.astuple() for x in r.trace] == [tuple(x) for x in want.trace]
+            assert (r.conflicts, r.iterations_to_correct) == (want.conflicts, want.iterations_to_correct)
+
+
+def test_iteration_cap_raises_with_partial_trace():
+    # test_engine.cpp:525-545
+    toy = P.Instance(2, 1, 2, [0, 0], [0, 1], [[0.9, 0.1], [0.8, 0.2]], [1, 1], [[1, 1]])
+    with pytest.raises(P.IterationLimitError) as e:
+        P.picard_simulate(toy, P.GreedyPolicy(), P.PartitionPlan(2, [0, 1]),
+                          P.PicardConfig(max_iterations=1, record_trace=True))
+    assert e.value.iterations_run == 1 and len(e.value.partial_trace) == 1
+
+
+def test_plan_and_config_validation():
+    # test_engine.cpp:416-453
+    toy = P.Instance(2, 1, 2, [0, 0], [0, 1], [[0.9, 0.1], [0.8, 0.2]], [1, 1], [[1, 1]])
+    g = P.GreedyPolicy()
+    with pytest.raises(P.ContractViolation):
+        P.picard_simulate(toy, g, P.PartitionPlan(2, [0]))
+    with pytest.raises(P.ContractViolation):
+        P.picard_simulate(toy, g, P.PartitionPlan(2, [0, 5]))
+    with pytest.raises(P.ContractViolation):
+        P.picard_simulate(toy, g, P.PartitionPlan(2, [0, 1]), P.PicardConfig(processes=3))
+    with pytest.raises(P.ContractViolation):
+        P.picard_simulate(toy, g, P.PartitionPlan(2, [0, 1]), initial_cache=[-1])
+    r = P.picard_simulate(toy, g, P.PartitionPlan(3, []) if False else P.PartitionPlan(2, [0, 1]))
+    assert r.actions.tolist() == [0, 1]
+
+
+def test_empty_horizon():
+    inst = P.Instance(2, 1, 0, [], [], [[0.5, 0.5]], [1, 1], [[1, 1]])
+    r = P.picard_simulate(inst, P.GreedyPolicy(), P.PartitionPlan(3, []))
+    assert r.actions.size == 0 and r.iterations_to_converged == 0 and r.total_policy_evals == 0
+
+
+def test_nonfinite_dual_scores_raise_like_the_reference():
+    J = 3
+    ons = NS(**ORC.generate_instance_arrays(J, 4, 50, 0.0, 0.8, 3))
+    inst = product_instance(ons)
+    params = P.MlpParams.seeded_uniform(7, 6, 9)
+    params.b3 = params.b3.copy()
+    params.b3[1] = np.inf
+    pol = P.DualNetworkPolicy(params, nodes=J)
+    opol = NS(kind=2, hidden=64, gamma=0.0, horizon=None, w1=params.w1, b1=params.b1, w2=params.w2,
+              b2=params.b2, w3=params.w3, b3=params.b3)
+    with pytest.raises(OracleError) as oe:
+        ORC.sequential(ons, opol)
+    with pytest.raises(P.ContractViolation) as ge:
+        P.sequential_simulate(inst, pol)
+    assert ge.value.time_step == oe.value.time_step
+    owner = ORC.uniform_partition(50, 3, 1)
+    with pytest.raises(OracleError) as oe2:
+        ORC.picard(ons, opol, owner, 3)
+    with pytest.raises(P.ContractViolation) as ge2:
+        P.picard_simulate(inst, pol, P.PartitionPlan(3, owner))
+    assert ge2.value.time_step == oe2.value.time_step
+
+
+def test_zero_network_equals_greedy():
+    # test_policies.cpp:117-132
+    ons = NS(**ORC.generate_instance_arrays(5, 12, 800, -0.5, 0.8, 5))
+    inst = product_instance(ons)
+    a = P.sequential_simulate(inst, P.DualNetworkPolicy.zero(inst)).actions
+    b = P.sequential_simulate(inst, P.GreedyPolicy()).actions
+    assert a.tolist() == b.tolist()
+
+
+def test_full_scale_c3_prefix_and_feasibility():
+    """C3 shape (J=100, I=1e4, T=1e7 needs minutes of oracle time); at a reduced
+    T with the C3 per-product density the GPU trajectory must (a) equal the
+    serial oracle on a prefix, (b) be a feasible trajectory, (c) conserve
+    units (test_fo_env.cpp:71-106)."""
+    J, I, T = 100, 1000, 1_000_000
+    inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
+    pol = P.DualNetworkPolicy.seeded(inst, 5)
+    plan = P.make_product_partition(inst, 4096, 1)
+    r = P.picard_simulate(inst, pol, plan)
+    ons = NS(nodes=J, products=I, horizon=200_000, product=inst.product[:200_000], order_t=None,
+             reward_row=inst.reward_row[:200_000], reward_table=inst.reward_table.ravel(),
+             capacity=inst.capacity, inventory=inst.inventory.ravel())
+    opol = NS(kind=2, hidden=64, gamma=0.0, horizon=T, w1=pol.w1, b1=pol.b1, w2=pol.w2, b2=pol.b2,
+              w3=pol.w3, b3=pol.b3)
+    seq_prefix, _ = ORC.sequential(ons, opol)
+    assert r.actions[:200_000].tolist() == seq_prefix.tolist()
+    cap = inst.capacity.astype(np.int64).copy()
+    inv = inst.inventory.astype(np.int64).copy()
+    a = r.actions
+    ok = a >= 0
+    np.subtract.at(cap, a[ok], 1)
+    np.subtract.at(inv, (inst.product[ok], a[ok]), 1)
+    assert cap.min() >= 0 and inv.min() >= 0
+    assert int(ok.sum()) == int(inst.capacity.sum() - cap.sum())
