@@ -1,0 +1,314 @@
+#!/usr/bin/env python3
+"""bench.py — simulated time-steps/s to convergence of ONE trajectory
+(BASELINE.json "metric"), B200 Picard engine vs the reference's CPU paths.
+
+Workload (default "c3", BASELINE.json configs[2], the north-star target and the
+largest config; it fits one B200): SCO with J=100 nodes, I=10^4 products,
+T=10^7 orders (generate_instance recipe, seed 7, beta 0, coverage 0.8, the
+seeded synthetic 100-node geometry), dual-price MLP policy {201,64,64,200}
+with theta seed 5, M=65536 processes under make_product_partition (seed 1),
+max_steps = 300*M (whole horizon, cli.cpp:225-227). One "step" = one full
+picard_simulate to convergence. Synthetic data, random-init weights.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c3|c2|c1]
+
+N>1 runs under torchrun, one rank per GPU: processes are sharded over ranks and
+every iteration exchanges fresh cache slices with NCCL (strong scaling of one
+trajectory). Timing: CUDA events around exactly K steps, barrier+sync on both
+sides, max over ranks. The L2 (126 MB) is flushed with a 512 MiB write before
+every step; the working set (orders 80 MB, cache 40 MB, ...) exceeds L2 anyway.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (J, I, T, M, theta seed) — BASELINE.json configs
+    "c1": (1, 10, 10_000, 16, 5),
+    "c2": (10, 1_000, 1_000_000, 4096, 5),
+    "c3": (100, 10_000, 10_000_000, 65536, 5),
+}
+METRIC = "simulated time-steps/sec to convergence (1 trajectory); speedup vs serial CPU ref"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def flops_per_eval(J: int, H: int = 64) -> int:
+    """Algorithmic FLOPs of one dual-policy evaluation: the three GEMV layers of
+    MlpParams::forward (mlp.cpp:141-169), 2 per MAC."""
+    return 2 * (H * (2 * J + 1) + H * H + 2 * J * H)
+
+
+def load_peaks():
+    try:
+        with open(PEAKS) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_workload(name: str):
+    import paper_2406_01939_b200 as P
+    J, I, T, M, theta = WORKLOADS[name]
+    inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
+    pol = P.DualNetworkPolicy.seeded(inst, theta)
+    plan = P.make_product_partition(inst, M, 1)
+    return inst, pol, plan, dict(J=J, I=I, T=T, M=M, theta=theta)
+
+
+def cpu_baseline(inst, pol, budget_s: float = 12.0):
+    """The UNMODIFIED reference's sequential_simulate (oracle/_ref) on the first
+    T' orders of the same instance, 1 host core (the path is inherently
+    serial). T' is sized for ~budget_s of CPU time."""
+    from types import SimpleNamespace as NS
+    from oracle.oracle import REF, ORC
+    lib, kind = (REF, "reference") if REF is not None else (ORC, "port")
+    J = inst.nodes
+
+    def prefix(n):
+        return NS(nodes=J, products=inst.products, horizon=n, product=inst.product[:n], order_t=None,
+                  reward_row=inst.reward_row[:n], reward_table=inst.reward_table.ravel(),
+                  capacity=inst.capacity, inventory=inst.inventory.ravel())
+
+    opol = NS(kind=2, hidden=pol.hidden, gamma=0.0, horizon=int(inst.horizon), w1=pol.w1, b1=pol.b1,
+              w2=pol.w2, b2=pol.b2, w3=pol.w3, b3=pol.b3)
+    n = min(int(inst.horizon), 20_000)
+    while True:
+        if kind == "reference":
+            actions, sec = lib.sequential_timed(prefix(n), opol)
+        else:
+            t0 = time.perf_counter()
+            actions, _ = lib.sequential(prefix(n), opol)
+            sec = time.perf_counter() - t0
+        if sec >= budget_s / 4 or n >= inst.horizon:
+            break
+        n = min(int(inst.horizon), int(n * max(2.0, budget_s / max(sec, 1e-3) * 0.9)))
+    return dict(value=n / sec, unit="steps/s", cores=1, kind=kind,
+                sample=f"sequential_simulate on the first {n} of {inst.horizon} orders of the same "
+                       f"instance ({sec:.2f} s, 1 core); the serial path cannot use more threads"), actions
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    inst, pol, plan, w = make_workload(args.workload)
+    from oracle.oracle import REF
+    steps = []
+    for _ in range(args.warmup + args.steps):
+        cb, _ = cpu_baseline(inst, pol, budget_s=8.0)
+        steps.append(cb)
+    timed = steps[args.warmup:]
+    value = statistics.mean(s["value"] for s in timed)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * w["T"] / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, **w, "policy": "dual MLP seeded", "partition": "product"},
+            "cpu_baseline": {**timed[-1], "value": value},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference has no GPU path; the serial CPU path is the reference's fastest way to the "
+                    "trajectory (its CPU Picard path is slower in wall time, BASELINE.md §2)"}
+    if REF is None:
+        line["note"] += "; oracle/_ref unavailable -> C restatement timed"
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2406_01939_b200 as P
+    inst, pol, plan, w = make_workload(args.workload)
+    T = w["T"]
+    cfg = P.PicardConfig(max_steps=300 * w["M"])
+    sim = P.Simulator(inst, pol, device=local)
+    sim.set_plan(plan)
+    if world > 1:
+        uid = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sim.attach_comm(uid[0], rank, world)
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up (untimed)
+    res = None
+    for _ in range(args.warmup):
+        res = sim.simulate_resident(cfg)
+    # ---- timed: exactly K steps
+    timings = []
+    with ClockSampler(local) as clocks:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            flush.zero_()
+            res = sim.simulate_resident(cfg)
+            timings.append(res.timing)
+        t1.record()
+        barrier()
+    ms = t0.elapsed_time(t1)
+    # the engine runs on its own stream; its own events bracket each step too
+    eng_ms = sum(t["total_ms"] for t in timings)
+    ms = max(ms, eng_ms)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    value = T / (ms_per_step / 1000.0)
+    actions = sim.download_actions()
+
+    # ---- roofline of the dominant kernel (the sweep)
+    tm = timings[-1]
+    peaks, peak_src = load_peaks()
+    F = flops_per_eval(w["J"])
+    sweep_ms = tm["sweep_ms"]
+    achieved_tflops = tm["total_evals"] * F / (sweep_ms / 1000.0) / 1e12 if sweep_ms > 0 else 0.0
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    roofline = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved_tflops / peak, "traffic": None,
+                "kernel": "k_sweep_product<kDual> (FP64 SIMT, exact op order)",
+                "per_launch": {"launches": tm["sweep_launches"], "avg_ms": sweep_ms / max(1, tm["sweep_launches"]),
+                               "flops_per_eval": F, "evals": tm["total_evals"]},
+                "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+                "note": "FP64 exact-order path; fraction is against the bf16 tensor peak the "
+                        "tcgen05 path targets (B200 FP64 nominal ~37 TF/s)"}
+
+    # ---- e2e through the public one-shot API from pinned host memory
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        pinst = P.Instance(inst.nodes, inst.products, inst.horizon, pin(inst.product), pin(inst.reward_row),
+                           pin(inst.reward_table), pin(inst.capacity), pin(inst.inventory))
+        pplan = P.PartitionPlan(plan.processes, pin(plan.owner))
+        P.picard_simulate(pinst, pol, pplan, cfg)  # warm-up
+        torch.cuda.synchronize()
+        t_e = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            r = P.picard_simulate(pinst, pol, pplan, cfg)
+        e2e_s = (time.perf_counter() - t_e) / args.e2e_steps
+        assert np.array_equal(r.actions, actions)
+        h2d = sum(a.nbytes for a in (inst.product, inst.reward_row, inst.reward_table, inst.capacity,
+                                     inst.inventory, plan.owner, pol.w1, pol.b1, pol.w2, pol.b2, pol.w3, pol.b3))
+        e2e = {"value": T / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(actions.nbytes), "seconds_per_step": e2e_s,
+               "api": "paper_2406_01939_b200.picard_simulate (pcd_picard_simulate: upload, plan CSR, "
+                      "fixed point, download)"}
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu, ref_prefix = cpu_baseline(inst, pol)
+        n = ref_prefix.size
+        cpu["prefix_equal"] = bool(np.array_equal(ref_prefix, actions[:n]))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.workload, **w, "policy": "dual MLP {2J+1,64,64,2J} seeded",
+                           "partition": "product", "max_steps": 300 * w["M"],
+                           "l2": "512 MiB flush before every step; working set > L2",
+                           "parallelism": f"processes sharded over {world} GPU(s)"},
+                "iterations": res.iterations_to_converged,
+                "steps_critical": tm["steps_critical"], "total_evals": tm["total_evals"],
+                "us_per_critical_step": 1000.0 * ms_per_step / max(1, tm["steps_critical"]),
+                "phase_ms": {k: tm[k] for k in ("sweep_ms", "prep_ms", "publish_ms", "advance_ms")},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(sum(t["kernel_launches"] for t in timings)),
+                "clocks": clocks.summary()}
+        if cpu:
+            line["speedup_vs_cpu_serial"] = value / cpu["value"]
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    sim.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -158,6 +158,9 @@ typedef struct pcd_handle pcd_handle;
 /* ---------------------------------------------------------------- misc */
 const char* pcd_version(void);
 const char* pcd_last_error(void);
+/* ContractViolation::time_step() of the last PCD_CONTRACT_VIOLATION on this
+ * thread (-1 if none / not applicable). */
+int64_t pcd_last_error_time_step(void);
 /* Number of CUDA devices visible (0 on a CPU-only host; never fails). */
 int pcd_device_count(void);
 

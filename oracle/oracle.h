@@ -166,6 +166,12 @@ int ref_iterate_once(const orc_instance* inst, const orc_policy* pol,
                      int64_t* changed, int64_t* n_changed, int64_t* error_t);
 int ref_total_reward(const orc_instance* inst, const int32_t* actions,
                      double* total);
+int ref_sequential_timed(const orc_instance* inst, const orc_policy* pol,
+                         int32_t* actions, double* seconds);
+int ref_picard_timed(const orc_instance* inst, const orc_policy* pol,
+                     const int32_t* owner, int32_t processes, int64_t max_steps,
+                     int32_t threads, int32_t* actions, int64_t* iterations,
+                     int64_t* seq_equiv, double* seconds);
 
 #ifdef __cplusplus
 }

@@ -297,6 +297,29 @@ class _Lib:
                                                 C.byref(k)))
         return hist[:k.value, :T].copy()
 
+    def sequential_timed(self, inst, pol):
+        """REF only: (actions, seconds of sequential_simulate alone)."""
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        actions = np.zeros(max(int(inst.horizon), 1), np.int32)
+        sec = C.c_double()
+        self.check(self.fn("sequential_timed")(C.byref(ci), C.byref(cp), _p(actions, C.c_int32), C.byref(sec)))
+        return actions[:int(inst.horizon)], sec.value
+
+    def picard_timed(self, inst, pol, owner, M, max_steps=0, threads=1):
+        """REF only: (actions, iterations, seq_equiv, seconds of picard_simulate alone)."""
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        owner = np.ascontiguousarray(owner, np.int32)
+        actions = np.zeros(max(int(inst.horizon), 1), np.int32)
+        it = C.c_int64()
+        se = C.c_int64()
+        sec = C.c_double()
+        self.check(self.fn("picard_timed")(C.byref(ci), C.byref(cp), _p(owner, C.c_int32), C.c_int32(M),
+                                           C.c_int64(max_steps), C.c_int32(threads), _p(actions, C.c_int32),
+                                           C.byref(it), C.byref(se), C.byref(sec)))
+        return actions[:int(inst.horizon)], it.value, se.value, sec.value
+
     def total_reward(self, inst, actions):
         ci, k1 = self._inst(inst)
         a = np.ascontiguousarray(actions, np.int32)

@@ -18,6 +18,7 @@
 // generate_instance does (instance.cpp:95-138), and (b) the fixture recipe of
 // test_helpers.hpp:31-41 (small_random_instance parameters).
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -373,6 +374,48 @@ int ref_sequential(const orc_instance* in, const orc_policy* pol, int32_t* actio
         });
       },
       error_t);
+}
+
+// Wall-clock of sequential_simulate alone (instance marshalling excluded), the
+// CPU-baseline leg of bench.py (BASELINE.md §4 protocol step 3).
+int ref_sequential_timed(const orc_instance* in, const orc_policy* pol, int32_t* actions,
+                         double* seconds) {
+  return guarded([&] {
+    Instance inst = make_instance(in);
+    auto env = inst.make_env();
+    return with_policy(in, pol, inst, [&](const auto& policy) {
+      const auto t0 = std::chrono::steady_clock::now();
+      auto out = sequential_simulate(env, policy, std::span<const Order>(inst.orders));
+      const auto t1 = std::chrono::steady_clock::now();
+      *seconds = std::chrono::duration<double>(t1 - t0).count();
+      for (size_t t = 0; t < out.actions.size(); ++t) actions[t] = out.actions[t].node;
+      return 0;
+    });
+  });
+}
+
+// Wall-clock of picard_simulate alone with PicardConfig::threads = `threads`.
+int ref_picard_timed(const orc_instance* in, const orc_policy* pol, const int32_t* owner,
+                     int32_t M, int64_t max_steps, int32_t threads, int32_t* actions,
+                     int64_t* iterations, int64_t* seq_equiv, double* seconds) {
+  return guarded([&] {
+    Instance inst = make_instance(in);
+    auto env = inst.make_env();
+    auto plan = make_plan(owner, in->horizon, M);
+    PicardConfig config;
+    config.max_steps = max_steps;
+    config.threads = threads;
+    return with_policy(in, pol, inst, [&](const auto& policy) {
+      const auto t0 = std::chrono::steady_clock::now();
+      auto r = picard_simulate(env, policy, std::span<const Order>(inst.orders), plan, config);
+      const auto t1 = std::chrono::steady_clock::now();
+      *seconds = std::chrono::duration<double>(t1 - t0).count();
+      *iterations = r.iterations_to_converged;
+      *seq_equiv = r.policy_eval_count_sequential_equivalent;
+      for (size_t t = 0; t < r.actions.size(); ++t) actions[t] = r.actions[t].node;
+      return 0;
+    });
+  });
 }
 
 int ref_picard(const orc_instance* in, const orc_policy* pol, const int32_t* owner,

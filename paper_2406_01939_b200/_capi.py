@@ -64,6 +64,7 @@ class pcd_timing(C.Structure):
 SIGNATURES = {
     "pcd_version": (C.c_char_p, []),
     "pcd_last_error": (C.c_char_p, []),
+    "pcd_last_error_time_step": (C.c_int64, []),
     "pcd_device_count": (C.c_int, []),
     "pcd_generate_instance": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_double,
                                         C.c_uint64, C.c_int32, I32P, I32P, F64P, I32P, I32P]),

@@ -81,6 +81,8 @@ def _check(rc: int, time_step: int = -1):
         return
     msg = _err()
     if rc == K.PCD_CONTRACT_VIOLATION:
+        if time_step < 0:
+            time_step = int(LIB.pcd_last_error_time_step())
         raise ContractViolation(msg, time_step)
     if rc == K.PCD_INVALID_ARGUMENT:
         raise InvalidArgument(msg)

@@ -8,8 +8,12 @@
 namespace pcd {
 
 static thread_local std::string g_last_error;
+static thread_local int64_t g_last_time_step = -1;
 
-void set_last_error(const std::string& s) { g_last_error = s; }
+void set_last_error(const std::string& s) {
+  g_last_error = s;
+  g_last_time_step = -1;
+}
 
 // Maps the in-flight exception onto the status codes of picard_b200.h, which
 // mirror the reference's exception classes (errors.hpp, engine.hpp:140-156).
@@ -21,6 +25,7 @@ int translate_exception() {
     return PCD_ITERATION_LIMIT;
   } catch (const ContractViolation& e) {
     set_last_error(e.what());
+    g_last_time_step = e.time_step;
     return PCD_CONTRACT_VIOLATION;
   } catch (const InvalidArgument& e) {
     set_last_error(e.what());
@@ -52,6 +57,8 @@ extern "C" {
 const char* pcd_version(void) { return "picard_b200 0.1.0 (sm_100a)"; }
 
 const char* pcd_last_error(void) { return pcd::g_last_error.c_str(); }
+
+int64_t pcd_last_error_time_step(void) { return pcd::g_last_time_step; }
 
 int pcd_generate_instance(int32_t nodes, int32_t products, int64_t horizon, double beta,
                           double coverage, uint64_t seed, int32_t geometry, int32_t* product,
