@@ -68,9 +68,11 @@ enum {
 
 /* Sweep engine selection for pcd_simulate / pcd_iterate_once. */
 enum {
-  PCD_ENGINE_AUTO = 0,     /* closed form when the plan is a product partition */
-  PCD_ENGINE_REPLAY = 1,   /* exact per-process window replay (any plan)        */
-  PCD_ENGINE_PRODUCT = 2   /* closed-form product-partition sweep (checked)     */
+  PCD_ENGINE_AUTO = 0,          /* closed form when the plan is a product partition;
+                                   tensor-core policy when eligible               */
+  PCD_ENGINE_REPLAY = 1,        /* exact per-process window replay (any plan)     */
+  PCD_ENGINE_PRODUCT = 2,       /* closed-form product-partition sweep (checked)  */
+  PCD_ENGINE_PRODUCT_FP64 = 3   /* ... with the FP64 SIMT policy only             */
 };
 
 /* A fulfillment-optimization instance (fo/instance.hpp:25-37). */
@@ -113,6 +115,11 @@ typedef struct pcd_config {
   int64_t max_iterations;  /* 0 = 2T + 4 */
   int32_t threads;         /* accepted for API parity; the device ignores it */
   int32_t engine;          /* PCD_ENGINE_* */
+  double tc_guard;         /* tensor-core decision margin below which a row is
+                              re-evaluated in exact FP64 (0 = default 5e-5)   */
+  int32_t tc_verify;       /* debug: re-evaluate EVERY row in FP64 and count
+                              unflagged disagreements (pcd_timing.tc_unflagged_bad) */
+  int32_t reserved;
 } pcd_config;
 
 /* PicardTraceRow (engine.hpp:128-134). */
@@ -149,8 +156,14 @@ typedef struct pcd_timing {
   int64_t sweep_launches;
   int64_t steps_critical; /* sum over iterations of max per-process evals */
   int64_t total_evals;
-  int32_t engine_used;    /* PCD_ENGINE_REPLAY / PCD_ENGINE_PRODUCT */
+  int32_t engine_used;    /* PCD_ENGINE_REPLAY / PRODUCT / PRODUCT_FP64 */
   int32_t device;
+  int64_t tc_rows;        /* policy evaluations through the tcgen05 path */
+  int64_t tc_flagged;     /* ... re-evaluated exactly (margin < guard) */
+  int64_t tc_disagree;    /* flagged rows where the fp16x3 argmax was wrong */
+  int64_t tc_unflagged_bad; /* tc_verify only: unflagged rows that were wrong (must be 0) */
+  int32_t tc_used;        /* the sweep ran on tensor cores */
+  int32_t tc_tiles;       /* CTAs (128 processes each) */
 } pcd_timing;
 
 typedef struct pcd_handle pcd_handle;

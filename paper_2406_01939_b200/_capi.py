@@ -19,7 +19,7 @@ F64P = C.POINTER(C.c_double)
 
 PCD_OK, PCD_INVALID_ARGUMENT, PCD_CONTRACT_VIOLATION, PCD_ITERATION_LIMIT, PCD_CUDA_ERROR = range(5)
 PCD_POLICY_GREEDY, PCD_POLICY_CAPACITY, PCD_POLICY_DUAL, PCD_POLICY_NULL = range(4)
-PCD_ENGINE_AUTO, PCD_ENGINE_REPLAY, PCD_ENGINE_PRODUCT = range(3)
+PCD_ENGINE_AUTO, PCD_ENGINE_REPLAY, PCD_ENGINE_PRODUCT, PCD_ENGINE_PRODUCT_FP64 = range(4)
 
 
 class pcd_instance(C.Structure):
@@ -37,7 +37,8 @@ class pcd_policy(C.Structure):
 
 class pcd_config(C.Structure):
     _fields_ = [("processes", C.c_int32), ("record_trace", C.c_int32), ("max_steps", C.c_int64),
-                ("max_iterations", C.c_int64), ("threads", C.c_int32), ("engine", C.c_int32)]
+                ("max_iterations", C.c_int64), ("threads", C.c_int32), ("engine", C.c_int32),
+                ("tc_guard", C.c_double), ("tc_verify", C.c_int32), ("reserved", C.c_int32)]
 
 
 class pcd_trace_row(C.Structure):
@@ -57,7 +58,9 @@ class pcd_timing(C.Structure):
                 ("publish_ms", C.c_double), ("advance_ms", C.c_double), ("iterations", C.c_int64),
                 ("kernel_launches", C.c_int64), ("sweep_launches", C.c_int64),
                 ("steps_critical", C.c_int64), ("total_evals", C.c_int64),
-                ("engine_used", C.c_int32), ("device", C.c_int32)]
+                ("engine_used", C.c_int32), ("device", C.c_int32), ("tc_rows", C.c_int64),
+                ("tc_flagged", C.c_int64), ("tc_disagree", C.c_int64), ("tc_unflagged_bad", C.c_int64),
+                ("tc_used", C.c_int32), ("tc_tiles", C.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/picard_b200.h

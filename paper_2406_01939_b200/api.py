@@ -40,6 +40,8 @@ from . import _capi as K
 
 LIB = K.LIB
 NO_FULFILL = -1
+ENGINES = {"auto": K.PCD_ENGINE_AUTO, "replay": K.PCD_ENGINE_REPLAY, "product": K.PCD_ENGINE_PRODUCT,
+           "product_fp64": K.PCD_ENGINE_PRODUCT_FP64}
 
 
 # ------------------------------------------------------------------ errors
@@ -355,12 +357,13 @@ class PicardConfig:
     record_trace: bool = False
     threads: int = 1
     engine: str = "auto"
+    tc_guard: float = 0.0
+    tc_verify: bool = False
 
     def to_c(self):
-        eng = {"auto": K.PCD_ENGINE_AUTO, "replay": K.PCD_ENGINE_REPLAY,
-               "product": K.PCD_ENGINE_PRODUCT}[self.engine]
         return K.pcd_config(int(self.processes), 1 if self.record_trace else 0, int(self.max_steps),
-                            int(self.max_iterations), int(self.threads), eng)
+                            int(self.max_iterations), int(self.threads), ENGINES[self.engine],
+                            float(self.tc_guard), 1 if self.tc_verify else 0, 0)
 
 
 @dataclass
@@ -514,7 +517,7 @@ class Simulator:
 
     def iterate_once(self, cache: np.ndarray, t_lo: int, t_hi: int, checkpoint_capacity=None,
                      checkpoint_inventory=None, engine: str = "auto") -> IterationOutcome:
-        eng = {"auto": K.PCD_ENGINE_AUTO, "replay": K.PCD_ENGINE_REPLAY, "product": K.PCD_ENGINE_PRODUCT}[engine]
+        eng = ENGINES[engine]
         assert cache.dtype == np.int32 and cache.flags.c_contiguous
         M = self.plan.processes
         evals = np.zeros(M, np.int64)

@@ -47,7 +47,7 @@ __device__ __forceinline__ double gt_add_exp(double y, int k) {
 
 // glibc expm1 (fdlibm s_expm1.c as built in glibc 2.39; FMA body @0x7ac30,
 // SSE2 body @0x2eaf0 of libm.so.6). Reachable range from tanh: |x| < 44.
-__device__ __noinline__ double gt_expm1(double x, int use_fma) {
+static __device__ __noinline__ double gt_expm1(double x, int use_fma) {
   const double INVLN2 = 1.4426950408889634, LN2HI = 0.6931471803691238,
                LN2LO = 1.9082149292705877e-10;
   const double Q1 = -3.33333333333331316428e-02, Q2 = 1.58730158725481460165e-03,

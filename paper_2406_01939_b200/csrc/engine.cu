@@ -17,10 +17,16 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cuda_fp16.h>
+
 #include "capi_internal.h"
 #include "kernels.cuh"
+#include "tc_sweep.cuh"
 
 namespace pcd {
+
+void launch_tc_sweep(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_sweep.cu
+size_t tc_smem_bytes();
 
 #define CK(x)                                                                              \
   do {                                                                                     \
@@ -116,6 +122,14 @@ struct pcd_handle {
   bool resident_valid = false;
   int32_t* history = nullptr;  // host, pcd_set_history
   int64_t history_cap = 0;
+  // tensor-core policy (tc_sweep.cu)
+  bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
+  pcd::DBuf<unsigned char> tc_wimg;
+  pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf;
+  pcd::DBuf<int> tc_rows, tc_D;
+  pcd::DBuf<unsigned long long> tc_stats;
+  int32_t tc_tiles = 0;
+  int64_t max_load = 0;
   // multi-GPU
   int32_t rank = 0, nranks = 1;
   pcd::nccl_comm comm = nullptr;
@@ -289,13 +303,50 @@ static void throw_sweep_error(pcd_handle* h) {
 }
 
 // One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
-static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out) {
+static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify) {
+  TcArgs a{};
+  SweepArgs& s = a.s;
+  s.model = h->model();
+  s.M = h->M; s.J = h->J; s.lo = lo; s.hi = hi;
+  s.pstart = h->pstart.p; s.pslots = h->pslots.p;
+  s.ckcap = h->ckcap.p; s.hck = h->hck.p; s.ev = h->ev.p; s.xloc = h->xloc.p;
+  s.cache = h->cache.p; s.written = h->written.p; s.ref = h->ref.n ? h->ref.p : nullptr;
+  s.scal = h->scal; s.evals_out = evals_out;
+  a.rows = h->tc_rows.p; a.D = h->tc_D.p; a.wimg = h->tc_wimg.p;
+  a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
+  a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p;
+  a.guard = (float)(guard > 0 ? guard : 5e-5);
+  a.verify = verify;
+  a.stats = h->tc_stats.p;
+  // PCD_TC_PROF=1: per-phase clock64 totals of CTA 0, printed to stderr (debug)
+  static const bool prof = getenv("PCD_TC_PROF") != nullptr;
+  static DBuf<long long> dprof;
+  if (prof) {
+    dprof.alloc(20);
+    CK(cudaMemsetAsync(dprof.p, 0, 20 * sizeof(long long), h->stream));
+    a.prof = dprof.p;
+  }
+  a.fake = getenv("PCD_TC_FAKE") != nullptr;
+  launch_tc_sweep(a, h->tc_tiles, h->stream);
+  CK(cudaGetLastError());
+  if (prof) {
+    long long v[20];
+    CK(cudaMemcpyAsync(v, dprof.p, sizeof v, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    fprintf(stderr, "tcprof steps=%lld F=%lld(own %lld) L1=%lld E1=%lld L2=%lld E2=%lld L3=%lld S=%lld fin=%lld chk=%lld U=%lld\n",
+            v[10], v[0], v[11], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
+    fprintf(stderr, "tcprof F: loads=%lld xpart=%lld dupd=%lld scr=%lld feat=%lld\n", v[12], v[13], v[14], v[15], v[16]);
+  }
+}
+
+static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
+                             double guard = 0.0, int verify = 0) {
   IterOut out;
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
   reset_scalars(h);
   if (W <= 0) return out;
   PhaseTimer tm(h->stream);
-  if (engine == PCD_ENGINE_PRODUCT) {
+  if (engine == PCD_ENGINE_PRODUCT || engine == PCD_ENGINE_PRODUCT_FP64) {
     tm.start();
     const int J = h->J;
     const int tpb = std::max(1, std::min(128, (int)((40 * 1024) / (4 * std::max(1, J)))));
@@ -312,7 +363,14 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     h->timing.prep_ms += tm.stop_ms();
     h->timing.kernel_launches += 6;
     tm.start();
-    dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
+    const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
+    if (tc) {
+      launch_tc(h, lo, hi, evals_out, guard, verify);
+      h->timing.tc_used = 1;
+      h->timing.tc_tiles = h->tc_tiles;
+    } else {
+      dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
+    }
     h->timing.sweep_ms += tm.stop_ms();
     h->timing.kernel_launches += 1;
     h->timing.sweep_launches += 1;
@@ -376,10 +434,10 @@ static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to) {
 
 static int choose_engine(pcd_handle* h, int requested) {
   if (requested == PCD_ENGINE_REPLAY) return PCD_ENGINE_REPLAY;
-  if (requested == PCD_ENGINE_PRODUCT) {
+  if (requested == PCD_ENGINE_PRODUCT || requested == PCD_ENGINE_PRODUCT_FP64) {
     if (!h->is_product)
       throw InvalidArgument("engine=PRODUCT requires a product partition (each product on one process)");
-    return PCD_ENGINE_PRODUCT;
+    return requested;
   }
   return h->is_product ? PCD_ENGINE_PRODUCT : PCD_ENGINE_REPLAY;
 }
@@ -415,6 +473,7 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   h->timing = pcd_timing{};
   h->timing.engine_used = engine;
   h->timing.device = h->device;
+  if (h->tc_stats.n) CK(cudaMemsetAsync(h->tc_stats.p, 0, sizeof(unsigned long long) * 4, h->stream));
   const int64_t cap_it = cfg->max_iterations > 0 ? cfg->max_iterations : 2 * T + 4;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -444,7 +503,7 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
                            iteration, rows);
     }
     ++iteration;
-    IterOut it = run_iteration(h, engine, ws, we, nullptr);
+    IterOut it = run_iteration(h, engine, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify);
     res->iterations_to_converged += 1;
     res->policy_eval_count_sequential_equivalent += it.max_evals;
     res->total_policy_evals += it.total_evals;
@@ -473,6 +532,14 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   cudaEventDestroy(e1);
   h->timing.total_ms = ms;
   h->timing.iterations = iteration;
+  if (h->tc_stats.n) {
+    unsigned long long st[4];
+    CK(cudaMemcpy(st, h->tc_stats.p, sizeof st, cudaMemcpyDeviceToHost));
+    h->timing.tc_rows = (int64_t)st[0];
+    h->timing.tc_flagged = (int64_t)st[1];
+    h->timing.tc_disagree = (int64_t)st[2];
+    h->timing.tc_unflagged_bad = (int64_t)st[3];
+  }
   res->iterations_run = iteration;
   res->trace_rows = (int64_t)rows.size();
   for (int64_t i = 0; i < (int64_t)rows.size() && i < trace_cap; ++i) trace[i] = rows[(size_t)i];
@@ -518,6 +585,50 @@ static void validate_instance(const pcd_instance* in) {
   }
   for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i)
     if (!std::isfinite(in->reward_table[i])) throw InvalidArgument("rewards must be finite");
+}
+
+// Weight images for the tcgen05 sweep (tc_sweep.cuh): fp16 hi + 2^11-scaled lo
+// parts in the canonical K-major no-swizzle UMMA layout, W3' = W3[:J] + W3[J:]
+// (the score needs only p_j + p_{J+j}), fp32 biases and feature reciprocals.
+static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap, const int32_t* pinv,
+                       const double* rtab) {
+  const int J = h->J, I = h->I, in = 2 * J + 1;
+  std::vector<unsigned char> img(kWImgBytes, 0);
+  // hi part at `base`, lo part at `base + part` (matches w1h/w1l/... in tc_sweep.cu)
+  auto put = [&](size_t base, size_t part, int R, int r, int k, double w) {
+    const float wf = (float)w;
+    const __half hi = __float2half_rn(wf);
+    const __half lo = __float2half_rn((wf - __half2float(hi)) * kLoScale);
+    const size_t off = (size_t)canon_off(R, r, k);
+    std::memcpy(&img[base + off], &hi, 2);
+    std::memcpy(&img[base + part + off], &lo, 2);
+  };
+  const size_t w2base = 2 * (size_t)kW1Bytes, w3base = w2base + 2 * (size_t)kW2Bytes;
+  for (int r = 0; r < kTcH; ++r)
+    for (int k = 0; k < kTcK1; ++k) put(0, kW1Bytes, kTcH, r, k, k < in ? pol->w1[(size_t)r * in + k] : 0.0);
+  for (int r = 0; r < kTcH; ++r)
+    for (int k = 0; k < kTcH; ++k) put(w2base, kW2Bytes, kTcH, r, k, pol->w2[(size_t)r * kTcH + k]);
+  for (int r = 0; r < kTcN3; ++r)
+    for (int k = 0; k < kTcH; ++k)
+      put(w3base, kW3Bytes, kTcN3, r, k,
+          r < J ? pol->w3[(size_t)r * kTcH + k] + pol->w3[(size_t)(J + r) * kTcH + k] : 0.0);
+  std::vector<float> b1(kTcH), b2(kTcH), b3(kTcN3, 0.f), ic0(J), ix0((size_t)I * J);
+  for (int r = 0; r < kTcH; ++r) { b1[r] = (float)pol->b1[r]; b2[r] = (float)pol->b2[r]; }
+  for (int j = 0; j < J; ++j) b3[j] = (float)(pol->b3[j] + pol->b3[J + j]);
+  for (int j = 0; j < J; ++j) ic0[j] = pcap[j] > 0 ? (float)(1.0 / pcap[j]) : 0.f;
+  for (size_t i = 0; i < (size_t)I * J; ++i) ix0[i] = pinv[i] > 0 ? (float)(1.0 / pinv[i]) : 0.f;
+  h->tc_wimg.upload(img.data(), img.size(), h->stream);
+  h->tc_b1.upload(b1.data(), b1.size(), h->stream);
+  h->tc_b2.upload(b2.data(), b2.size(), h->stream);
+  h->tc_b3.upload(b3.data(), b3.size(), h->stream);
+  h->tc_ic0.upload(ic0.data(), ic0.size(), h->stream);
+  h->tc_ix0.upload(ix0.data(), ix0.size(), h->stream);
+  std::vector<float> rtf((size_t)h->R * J);
+  for (size_t i = 0; i < rtf.size(); ++i) rtf[i] = (float)rtab[i];
+  h->tc_rtf.upload(rtf.data(), rtf.size(), h->stream);
+  h->tc_stats.alloc(4);
+  CK(cudaStreamSynchronize(h->stream));
+  h->tc_ok = true;
 }
 
 extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t device, pcd_handle** out) {
@@ -577,6 +688,12 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
       h->pinv0.upload(in->inventory, IJ, s);
     }
     h->p_horizon = pol->horizon >= 0 ? pol->horizon : in->horizon;
+    if (2 * h->J + 1 <= kTcK1 && h->J <= kTcN3 && H == kTcH) {
+      prepare_tc(h.get(), pol, pol->init_capacity ? pol->init_capacity : in->capacity,
+                 pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
+                                    : in->inventory,
+                 in->reward_table);
+    }
   }
   CK(cudaMalloc(&h->scal, sizeof(Scalars)));
   CK(cudaMallocHost(&h->h_scal, sizeof(Scalars)));
@@ -620,6 +737,30 @@ extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
   h->is_product = hf == 0;
   h->have_plan = true;
   ensure_state_buffers(h);
+  // tensor-core tiles: non-empty processes, heaviest first, 128 per CTA
+  {
+    std::vector<int64_t> load((size_t)M, 0);
+    for (int64_t t = 0; t < h->T; ++t) load[(size_t)owner[t]] += 1;
+    std::vector<int32_t> procs;
+    for (int32_t m = 0; m < M; ++m)
+      if (load[(size_t)m] > 0) procs.push_back(m);
+    std::stable_sort(procs.begin(), procs.end(),
+                     [&](int32_t a, int32_t b) { return load[(size_t)a] > load[(size_t)b]; });
+    h->max_load = procs.empty() ? 0 : load[(size_t)procs[0]];
+    // The per-row CUDA-core work (features, epilogues) dominates a step, so
+    // spread the processes over every SM (one CTA each, <= 128 rows), round
+    // robin in load order so all tiles carry the same critical path.
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+    const int64_t n = (int64_t)procs.size();
+    h->tc_tiles = (int32_t)std::max<int64_t>((n + kTcRows - 1) / kTcRows, std::min<int64_t>(nsm, n));
+    std::vector<int32_t> rows((size_t)std::max(1, h->tc_tiles) * kTcRows, -1);
+    for (int64_t k = 0; k < n; ++k)
+      rows[(size_t)(k % h->tc_tiles) * kTcRows + (size_t)(k / h->tc_tiles)] = procs[(size_t)k];
+    h->tc_rows.upload(rows.data(), rows.size(), h->stream);
+    h->tc_D.alloc(rows.size() * (size_t)std::max(1, h->J));
+    CK(cudaStreamSynchronize(h->stream));
+  }
   return PCD_OK;
   PCD_CATCH
 }

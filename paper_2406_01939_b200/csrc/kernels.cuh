@@ -12,7 +12,7 @@
 //   ckcap[J], ckinv[I*J]                  int32   checkpoint FoState (dense)
 //   xloc[I*J]                             int32   per-iteration own-product inventory
 //   ev[T]                                 int32   effective cached attempt (node or -1)
-//   hck[nb*J]                             int32   per-node prefix counts of ev every K slots
+//   hck[nb*J]                             int32   per-node prefix counts of ev every K=32 slots
 #pragma once
 
 #include <cstdint>
@@ -22,7 +22,7 @@
 
 namespace pcd {
 
-constexpr int kLogK = 7;  // checkpoint stride K = 128 slots
+constexpr int kLogK = 5;  // checkpoint stride K = 32 slots (one warp-wide partial scan)
 constexpr int kK = 1 << kLogK;
 constexpr int kSegRows = 256;  // checkpoint rows per scan segment
 
@@ -56,7 +56,7 @@ __device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
 // earlier cached attempts of the same (product, node) exist in the window —
 // i.e. it would succeed inventory-wise with unlimited capacity.
 // ---------------------------------------------------------------------------
-__global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
+static __global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
                             int lo, int hi, const int* __restrict__ cache,
                             const int* __restrict__ ckinv, int J, int* __restrict__ ev) {
   extern __shared__ int cnt_smem[];
@@ -81,7 +81,7 @@ __global__ void k_effective(const int* __restrict__ qstart, const int* __restric
 }
 
 // Per K-slot block histogram of effective attempts: hck[b][j].
-__global__ void k_block_hist(const int* __restrict__ ev, int lo, int W, int J, int* __restrict__ hck) {
+static __global__ void k_block_hist(const int* __restrict__ ev, int lo, int W, int J, int* __restrict__ hck) {
   extern __shared__ int hist[];
   const int b = blockIdx.x;
   for (int j = threadIdx.x; j < J; j += blockDim.x) hist[j] = 0;
@@ -96,7 +96,7 @@ __global__ void k_block_hist(const int* __restrict__ ev, int lo, int W, int J, i
 }
 
 // Column sums of each segment of kSegRows checkpoint rows.
-__global__ void k_seg_sums(const int* __restrict__ hck, int nb, int J, int* __restrict__ seg) {
+static __global__ void k_seg_sums(const int* __restrict__ hck, int nb, int J, int* __restrict__ seg) {
   const int s = blockIdx.x;
   const int r0 = s * kSegRows, r1 = min(nb, r0 + kSegRows);
   for (int j = threadIdx.x; j < J; j += blockDim.x) {
@@ -107,7 +107,7 @@ __global__ void k_seg_sums(const int* __restrict__ hck, int nb, int J, int* __re
 }
 
 // Exclusive scan of the segment sums over segments, per column (one CTA).
-__global__ void k_seg_scan(int* __restrict__ seg, int nseg, int J) {
+static __global__ void k_seg_scan(int* __restrict__ seg, int nseg, int J) {
   for (int j = threadIdx.x; j < J; j += blockDim.x) {
     int acc = 0;
     for (int s = 0; s < nseg; ++s) {
@@ -120,7 +120,7 @@ __global__ void k_seg_scan(int* __restrict__ seg, int nseg, int J) {
 
 // In-segment exclusive scan plus the segment offset: hck[b][j] becomes the
 // number of effective attempts at node j in [lo, lo + b*K).
-__global__ void k_seg_apply(int* __restrict__ hck, int nb, int J, const int* __restrict__ seg) {
+static __global__ void k_seg_apply(int* __restrict__ hck, int nb, int J, const int* __restrict__ seg) {
   const int s = blockIdx.x;
   const int r0 = s * kSegRows, r1 = min(nb, r0 + kSegRows);
   for (int j = threadIdx.x; j < J; j += blockDim.x) {
@@ -186,7 +186,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int J, int in, int H, int out)
 // owner and no other process reads cache[t] after the effective pass.
 // ---------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
+static __global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -290,7 +290,7 @@ struct ReplayArgs {
 // and are published by k_publish after all processes finished (the barrier).
 // ---------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(128) k_sweep_replay(ReplayArgs a) {
+static __global__ void __launch_bounds__(128) k_sweep_replay(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.m0 + blockIdx.x * (blockDim.x >> 5) + warp;
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(128) k_sweep_replay(ReplayArgs a) {
 }
 
 // Barrier publish (engine.hpp:434-443) + driver counters (engine.hpp:543-553).
-__global__ void k_publish(const int* __restrict__ fresh, int* __restrict__ cache,
+static __global__ void k_publish(const int* __restrict__ fresh, int* __restrict__ cache,
                           unsigned char* __restrict__ written, const int* __restrict__ ref, int lo,
                           int hi, Scalars* scal) {
   unsigned long long changed = 0, conflicts = 0, first = ~0ull;
@@ -378,11 +378,11 @@ __global__ void k_publish(const int* __restrict__ fresh, int* __restrict__ cache
   }
 }
 
-__global__ void k_fill(int* p, int v, long long n) {
+static __global__ void k_fill(int* p, int v, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = v;
 }
 
-__global__ void k_mismatches(const int* __restrict__ cache, const int* __restrict__ ref, long long T, Scalars* scal) {
+static __global__ void k_mismatches(const int* __restrict__ cache, const int* __restrict__ ref, long long T, Scalars* scal) {
   unsigned long long c = 0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x)
     c += cache[t] != ref[t];
@@ -392,7 +392,7 @@ __global__ void k_mismatches(const int* __restrict__ cache, const int* __restric
 
 // Checkpoint advance (engine.hpp:514-526 -> apply_in_place, fo/types.hpp:89-100):
 // subtract the cache prefix's fulfilments from the checkpoint state.
-__global__ void k_advance(const int* __restrict__ cache, const int* __restrict__ product, int lo,
+static __global__ void k_advance(const int* __restrict__ cache, const int* __restrict__ product, int lo,
                           int hi, int J, int* __restrict__ ckcap, int* __restrict__ ckinv) {
   extern __shared__ int hcap[];
   for (int j = threadIdx.x; j < J; j += blockDim.x) hcap[j] = 0;
@@ -409,7 +409,7 @@ __global__ void k_advance(const int* __restrict__ cache, const int* __restrict__
     if (hcap[j]) atomicSub(&ckcap[j], hcap[j]);
 }
 
-__global__ void k_advance_check(const int* __restrict__ cache, int lo, int hi, int J,
+static __global__ void k_advance_check(const int* __restrict__ cache, int lo, int hi, int J,
                                 const int* __restrict__ ckcap, const int* __restrict__ ckinv,
                                 long long IJ, Scalars* scal) {
   int bad = 0;
@@ -422,7 +422,7 @@ __global__ void k_advance_check(const int* __restrict__ cache, int lo, int hi, i
 }
 
 // Error path only: serial re-application to find the first infeasible order.
-__global__ void k_advance_serial(const int* __restrict__ cache, const int* __restrict__ product,
+static __global__ void k_advance_serial(const int* __restrict__ cache, const int* __restrict__ product,
                                  const int* __restrict__ order_t, int lo, int hi, int J,
                                  int* __restrict__ ckcap, int* __restrict__ ckinv, long long* err_t) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -441,7 +441,7 @@ __global__ void k_advance_serial(const int* __restrict__ cache, const int* __res
 }
 
 // Owned-slot counts per process inside [lo, hi) (evals_per_process).
-__global__ void k_window_evals(const int* __restrict__ pstart, const int* __restrict__ pslots, int M,
+static __global__ void k_window_evals(const int* __restrict__ pstart, const int* __restrict__ pslots, int M,
                                int lo, int hi, long long* out) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
@@ -450,7 +450,7 @@ __global__ void k_window_evals(const int* __restrict__ pstart, const int* __rest
 }
 
 // Product-partition test: every slot's owner equals its product's first owner.
-__global__ void k_check_product_partition(const int* __restrict__ owner, const int* __restrict__ product,
+static __global__ void k_check_product_partition(const int* __restrict__ owner, const int* __restrict__ product,
                                           const int* __restrict__ qstart, const int* __restrict__ qslots,
                                           long long T, int* flag) {
   int bad = 0;
@@ -461,12 +461,12 @@ __global__ void k_check_product_partition(const int* __restrict__ owner, const i
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
-__global__ void k_iota(int* p, long long n) {
+static __global__ void k_iota(int* p, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = (int)i;
 }
 
 // CSR start offsets from sorted keys: start[k] = first index with key >= k.
-__global__ void k_csr_starts(const int* __restrict__ sorted_keys, long long T, int nkeys, int* __restrict__ start) {
+static __global__ void k_csr_starts(const int* __restrict__ sorted_keys, long long T, int nkeys, int* __restrict__ start) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > T) return;
   const int prev = i == 0 ? -1 : sorted_keys[i - 1];
@@ -474,7 +474,7 @@ __global__ void k_csr_starts(const int* __restrict__ sorted_keys, long long T, i
   for (int k = prev + 1; k <= cur; ++k) start[k] = (int)i;
 }
 
-__global__ void k_transpose_f64(const double* __restrict__ src, int rows, int cols, double* __restrict__ dst) {
+static __global__ void k_transpose_f64(const double* __restrict__ src, int rows, int cols, double* __restrict__ dst) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= (long long)rows * cols) return;
   const int r = (int)(i / cols), c = (int)(i % cols);

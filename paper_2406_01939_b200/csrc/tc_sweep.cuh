@@ -1,0 +1,134 @@
+// tc_sweep.cuh — tcgen05/TMEM tensor-core sweep for product partitions.
+//
+// One CTA = a tile of 128 processes (MMA M=128, one TMEM lane per process).
+// Every step, each process evaluates the dual-price MLP (policies.hpp:121-168)
+// at its next own slot; the three layers run as tcgen05.mma.kind::f16 GEMMs
+//   z1 = F[128 x 208] . W1^T[208 x 64]       (features c/c0, x/x0, t/T)
+//   z2 = tanh(z1+b1)[128 x 64] . W2^T        (64 x 64)
+//   q  = tanh(z2+b2)[128 x 64] . W3'^T       (64 x 112),  W3' = W3[:J] + W3[J:]
+// with operands split into fp16 hi + (scaled) lo parts and three products
+// (hi.hi + hi.lo + lo.hi) accumulated in fp32 TMEM (two accumulators so the
+// 2^-11-scaled cross terms keep full precision): ~2^-22 relative per product.
+// score_j = r_j - q_j needs only the SUM of the two prices, hence W3'.
+//
+// Exactness: the tensor-core argmax is accepted only when its decision
+// margin (best - second best, and |best| vs the decline score 0) exceeds
+// `guard`; otherwise the row is re-evaluated by one warp with the exact FP64
+// path (warp_policy_eval<kDual>, bit-identical to the reference). The state of
+// each row is the product-partition closed form, identical to
+// k_sweep_product.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace pcd {
+
+constexpr int kTcRows = 128;
+constexpr int kTcK1 = 208;     // 2J+1 <= 208 (J <= 103)
+constexpr int kTcH = 64;
+constexpr int kTcN3 = 112;     // J <= 112
+constexpr int kTcThreads = 256;
+constexpr float kLoScale = 2048.f;          // lo parts are stored * 2^11
+constexpr float kLoInv = 1.f / 2048.f;
+
+// smem image layout of the weights (bytes), canonical K-major no-swizzle:
+//   off(r,k) = (k/8)*16*R + (r/8)*128 + (r%8)*16 + (k%8)*2
+constexpr int kW1Bytes = kTcH * kTcK1 * 2;   // one of hi / lo
+constexpr int kW2Bytes = kTcH * kTcH * 2;
+constexpr int kW3Bytes = kTcN3 * kTcH * 2;
+constexpr int kWImgBytes = 2 * (kW1Bytes + kW2Bytes + kW3Bytes);
+constexpr int kABytes = kTcRows * kTcK1 * 2;  // one of hi / lo
+
+__host__ __device__ constexpr int canon_off(int R, int r, int k) {
+  return (k >> 3) * 16 * R + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+}
+
+struct TcArgs {
+  SweepArgs s;          // state, publish and counter pointers (as k_sweep_product)
+  const int* rows;      // [ntiles*128] process of each row, -1 = idle
+  int* D;               // [ntiles*128*J] Hown - F per row
+  const unsigned char* wimg;  // kWImgBytes: W1hi W1lo W2hi W2lo W3hi W3lo
+  const float* b1f;     // [64]
+  const float* b2f;     // [64]
+  const float* b3f;     // [112] b3[:J] + b3[J:]
+  const float* inv_c0;  // [J]
+  const float* inv_x0;  // [I*J]
+  const float* rtabf;   // [R*J] rewards in fp32 (scores of the tensor-core path)
+  float guard;
+  int verify;           // debug: exact re-evaluation of every row
+  long long* prof;      // debug: per-phase clock64 totals of CTA 0 (or nullptr)
+  int fake;             // debug timing experiment: read checkpoint row 0 (WRONG results)
+  unsigned long long* stats;  // [0] tc rows, [1] flagged, [2] flagged & tc wrong,
+                              // [3] (verify) unflagged & tc wrong -- must stay 0
+};
+
+// ---------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, lbo mode 0, SWIZZLE_NONE
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  // c_format=F32 (bit 4), a/b format F16 (0), K-major A/B, N>>3 @17, M>>4 @24
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn((x - __half2float(hi)) * kLoScale);
+}
+
+__device__ __forceinline__ float tanh_f32(float z) {
+  // 1 - 2/(1+e^{2z}) with the fast reciprocal; |err| < 1e-6 absolute, far
+  // below the decision guard (verify mode measures the end-to-end margin)
+  return 1.f - __fdividef(2.f, 1.f + __expf(2.f * z));
+}
+
+}  // namespace pcd

@@ -260,3 +260,41 @@ def test_full_scale_c3_prefix_and_feasibility():
     np.subtract.at(inv, (inst.product[ok], a[ok]), 1)
     assert cap.min() >= 0 and inv.min() >= 0
     assert int(ok.sum()) == int(inst.capacity.sum() - cap.sum())
+
+
+@pytest.mark.parametrize("J,I,T,M", [(10, 300, 20000, 512), (30, 200, 12000, 256), (100, 40, 4000, 64),
+                                     (100, 300, 30000, 512), (1, 10, 10000, 16), (3, 7, 900, 5)])
+def test_tensor_core_sweep_matches_oracle(J, I, T, M):
+    """The tcgen05 fp16x3 policy path with the FP64 margin recheck must give the
+    reference's exact trajectory and per-iteration counters; in verify mode no
+    unflagged row may disagree with the exact FP64 decision."""
+    ons, inst, owner, opol, pol = _dual_case(J, I, T, M, "product")
+    seq, _ = ORC.sequential(ons, opol)
+    want = ORC.picard(ons, opol, owner, M, record_trace=True, reference=seq)
+    for verify in (False, True):
+        r = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner),
+                              P.PicardConfig(record_trace=True, engine="product", tc_verify=verify),
+                              reference_actions=seq)
+        assert r.timing["tc_used"] == 1
+        assert r.timing["tc_rows"] > 0
+        assert r.timing["tc_unflagged_bad"] == 0
+        assert r.actions.tolist() == seq.tolist()
+        assert r.iterations_to_converged == want.iterations_to_converged
+        assert r.iterations_to_correct == want.iterations_to_correct
+        assert r.conflicts == want.conflicts
+        assert r.policy_eval_count_sequential_equivalent == want.policy_eval_count_sequential_equivalent
+        assert r.total_policy_evals == want.total_policy_evals
+        assert [x.astuple() for x in r.trace] == [tuple(x) for x in want.trace]
+
+
+def test_tensor_core_and_fp64_sweeps_agree_with_warm_start_and_windows():
+    ons, inst, owner, opol, pol = _dual_case(10, 80, 8000, 128, "product")
+    draft, _ = ORC.sequential(ons, NS(kind=1, hidden=64, gamma=2.0, horizon=None))
+    for ms in (0, 250):
+        a = P.picard_simulate(inst, pol, P.PartitionPlan(128, owner),
+                              P.PicardConfig(max_steps=ms, record_trace=True, engine="product"), draft)
+        b = P.picard_simulate(inst, pol, P.PartitionPlan(128, owner),
+                              P.PicardConfig(max_steps=ms, record_trace=True, engine="product_fp64"), draft)
+        assert a.timing["tc_used"] == 1 and b.timing["tc_used"] == 0
+        assert a.actions.tolist() == b.actions.tolist()
+        assert [x.astuple() for x in a.trace] == [x.astuple() for x in b.trace]
