@@ -247,16 +247,26 @@ def main():
     peaks, peak_src = load_peaks()
     F = flops_per_eval(w["J"])
     sweep_ms = tm["sweep_ms"]
-    achieved_tflops = tm["total_evals"] * F / (sweep_ms / 1000.0) / 1e12 if sweep_ms > 0 else 0.0
+    tc = bool(tm["tc_used"])
+    mlp_evals = tm["tc_rows"] if tc else tm["total_evals"]
+    achieved_tflops = mlp_evals * F / (sweep_ms / 1000.0) / 1e12 if sweep_ms > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     roofline = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved_tflops / peak, "traffic": None,
-                "kernel": "k_sweep_product<kDual> (FP64 SIMT, exact op order)",
+                "kernel": ("k_sweep_product_tc (tcgen05.mma kind::f16, fp16x3 split, TMEM accumulators; "
+                           "FP64 exact re-evaluation of rows with margin < guard)") if tc else
+                          "k_sweep_product<kDual> (FP64 SIMT, exact op order)",
                 "per_launch": {"launches": tm["sweep_launches"], "avg_ms": sweep_ms / max(1, tm["sweep_launches"]),
-                               "flops_per_eval": F, "evals": tm["total_evals"]},
-                "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
-                "note": "FP64 exact-order path; fraction is against the bf16 tensor peak the "
-                        "tcgen05 path targets (B200 FP64 nominal ~37 TF/s)"}
+                               "flops_per_eval": F, "mlp_evals": mlp_evals,
+                               "algorithmic_flops_per_launch": mlp_evals * F / max(1, tm["sweep_launches"]),
+                               "critical_steps": tm["steps_critical"],
+                               "us_per_critical_step": 1000.0 * sweep_ms / max(1, tm["steps_critical"])},
+                "tc_guard": {"rows": tm["tc_rows"], "flagged_exact_recheck": tm["tc_flagged"],
+                             "fp16x3_wrong_when_flagged": tm["tc_disagree"], "tiles": tm["tc_tiles"]},
+                "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json; fp16 dense = bf16)",
+                "note": "algorithmic FLOPs = MLP evaluations x (512J+8320); the fp16x3 split issues 3x "
+                        "these MACs. The sweep is a latency-bound lockstep of `critical_steps` dependent "
+                        "policy steps (128-row MMA tiles), not a throughput GEMM"}
 
     # ---- e2e through the public one-shot API from pinned host memory
     e2e = None

@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
         }
         __syncwarp();
         if (prof_on) { const long long n_ = clock64(); pacc[12] += n_ - fl; fl = n_; }
+        // -- (A) inventory features + D deltas, 4 independent rows
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = warp + kTcWarps * (i0 + i);
@@ -293,10 +294,9 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
             continue;
           }
           ++active_w;
-          const int p = inf[RI_P];
           const int ro = row_off(r);
-          // ---- inventory features (x/x0): full reload or single-entry update
-          if (xdirty[i] || !xpersist) {
+          if (xdirty[i] || !xpersist) {  // full reload (first step / product change)
+            const int p = inf[RI_P];
             const int* xr = S.xloc + (size_t)p * J;
             const float* ix0 = a.inv_x0 + (size_t)p * J;
 #pragma unroll
@@ -308,20 +308,16 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
               if (lane == 0) sXbit[r * 4 + c] = bal;
             }
             if (lane == 0) inf[RI_XDIRTY] = 0;
-          } else if (xupd[i] >= 0) {
+          } else if (xupd[i] >= 0 && lane == 4 + i) {  // single-entry update
             const int j = xupd[i];
-            if (lane == 0) {
-              put_feature_at(sA, ro + kcol_off(J + j), (float)xu[i] * xi[i]);
-              if (xu[i] <= 0) sXbit[r * 4 + (j >> 5)] &= ~(1u << (j & 31));
-            }
+            put_feature_at(sA, ro + kcol_off(J + j), (float)xu[i] * xi[i]);
+            if (xu[i] <= 0) sXbit[r * 4 + (j >> 5)] &= ~(1u << (j & 31));
           }
-          if (lane == 0) {
+          if (lane == 8 + i) {
             inf[RI_XUPD] = -1;
             inf[RI_EVT] = -1;
           }
-          if (prof_on) { const long long n_ = clock64(); pacc[13] += n_ - fl; fl = n_; }
-          // ---- D = Hown - F: apply last step's two deltas in registers and
-          //      write them back (the update phase only records them)
+          // D = Hown - F: apply last step's two deltas in registers, write back
           const int evt = evtp[i], dl = xupd[i];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
@@ -331,29 +327,37 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
             if (dl == j0) { dv[i][c][0] -= 1; Drow_st(r, j0, dv[i][c][0]); }
             if (dl == j0 + 1) { dv[i][c][1] -= 1; Drow_st(r, j0 + 1, dv[i][c][1]); }
           }
-          if (prof_on) { const long long n_ = clock64(); pacc[14] += n_ - fl; fl = n_; }
-          // ---- capacities: c = max(0, ckcap - H_t + Hown - F)
-          int* scr = sScr + warp * kScrJ;
+        }
+        if (prof_on) { const long long n_ = clock64(); pacc[13] += n_ - fl; fl = n_; }
+        // -- (B) partial block [lo + bK, t): per-row uint8 event counts
+        uint32_t* cnt = (uint32_t*)(sScr + warp * kScrJ);  // 4 rows x 26 words
+        if (lane < 26) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int j0 = 64 * c + 2 * lane;
-            if (j0 < J) {
-              *(int2*)(scr + j0) = make_int2(sCap[j0] - hv[i][c][0] + dv[i][c][0],
-                                             j0 + 1 < J ? sCap[j0 + 1] - hv[i][c][1] + dv[i][c][1] : 0);
-            }
-          }
-          __syncwarp();
-          if (evp[i] >= 0) atomicSub(&scr[evp[i]], 1);
-          __syncwarp();
+          for (int i = 0; i < 4; ++i) cnt[i * 26 + lane] = 0u;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (evp[i] >= 0) atomicAdd(&cnt[i * 26 + (evp[i] >> 2)], 1u << (8 * (evp[i] & 3)));
+        __syncwarp();
+        if (prof_on) { const long long n_ = clock64(); pacc[14] += n_ - fl; fl = n_; }
+        // -- (C) capacity features c = max(0, ckcap - H_t + Hown - F)
+        //        for 4 independent rows (no syncs between rows: ILP)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (!act[i]) continue;
+          const int r = warp + kTcWarps * (i0 + i);
+          const int ro = row_off(r);
+          const unsigned char* cb = (const unsigned char*)(cnt + i * 26);
           uint32_t any = 0;
-          if (prof_on) { const long long n_ = clock64(); pacc[15] += n_ - fl; fl = n_; }
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int j0 = 64 * c + 2 * lane;
             bool f0 = false, f1 = false;
             if (j0 < J) {
-              const int2 cc = *(const int2*)(scr + j0);
-              const int c0 = max(cc.x, 0), c1 = j0 + 1 < J ? max(cc.y, 0) : 0;
+              const uint16_t pc = *(const uint16_t*)(cb + j0);
+              const int c0 = max(sCap[j0] - hv[i][c][0] + dv[i][c][0] - (int)(pc & 0xff), 0);
+              const int c1 = j0 + 1 < J ? max(sCap[j0 + 1] - hv[i][c][1] + dv[i][c][1] - (int)(pc >> 8), 0) : 0;
               const uint32_t xb = sXbit[r * 4 + (j0 >> 5)];
               f0 = c0 > 0 && ((xb >> (j0 & 31)) & 1u);
               f1 = c1 > 0 && ((xb >> ((j0 + 1) & 31)) & 1u);
@@ -374,10 +378,11 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
             }
             any |= E | O;
           }
+          int* inf = sInfo + r * kInfo;
           if (lane == 2) put_feature_at(sA, ro + kcol_off(2 * J), (float)inf[RI_OT] * invT);
           if (lane == 3) inf[RI_ANY] = any ? 1 : 0;
-          if (prof_on) { const long long n_ = clock64(); pacc[16] += n_ - fl; fl = n_; }
         }
+        if (prof_on) { const long long n_ = clock64(); pacc[16] += n_ - fl; fl = n_; }
       }
       if (prof_on) pacc[11] += clock64() - plast;  // warp 0's own F work
       if (lane == 0 && active_w) atomicAdd(&sCtl[0], active_w);
