@@ -1,0 +1,271 @@
+// picard_b200.hpp — C++ drop-in for the reference's serial and Picard
+// simulation paths, running on the B200 engine through the C ABI
+// (picard_b200.h). Include it AFTER the reference headers:
+//
+//   #include "picard/engine.hpp"
+//   #include "picard/fo/policies.hpp"
+//   #include "picard_b200.hpp"
+//
+//   auto r = picard::b200::picard_simulate(env, policy, orders, plan, config,
+//                                          initial_cache, reference_actions);
+//
+// Same argument meanings, same PicardResult / IterationOutcome /
+// SequentialOutput, same exception types as
+//   picard::picard_simulate      engine.hpp:458-590
+//   picard::picard_iterate_once  engine.hpp:358-444
+//   picard::sequential_simulate  engine.hpp:237-267
+// for FoEnv x {GreedyPolicy, CapacityPenalizedPolicy, DualNetworkPolicy}.
+// Observers are not supported on the device path (they need per-step host
+// callbacks); the per-iteration cache history is available through
+// pcd_set_history instead.
+//
+// DualNetworkPolicy keeps its normalisation state (initial_, horizon_)
+// private; every reference call site builds it from the instance's initial
+// state and horizon (cli.cpp:324-349, tests), which is what the adapter
+// assumes. Pass a DualNormalization to state it explicitly.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "picard_b200.h"
+
+namespace picard::b200 {
+
+struct DualNormalization {
+  const fo::FoState* initial = nullptr;  // DualNetworkPolicy::initial_ (nullptr: env initial)
+  std::int64_t horizon = -1;             // DualNetworkPolicy::horizon_ (-1: orders.size())
+};
+
+namespace detail {
+
+// SoA marshalling of the reference's AoS instance (fo/types.hpp:26-31):
+// per-order reward vectors are deduplicated into a table (generated
+// instances have one distinct vector per origin node, instance.cpp:100-105).
+struct Marshalled {
+  std::int32_t J = 0, I = 0;
+  std::vector<std::int32_t> product, order_t, reward_row, capacity, inventory;
+  std::vector<double> reward_table;
+  pcd_instance view{};
+};
+
+inline void dense_state(const fo::FoState& s, std::int32_t J, std::int32_t I, std::vector<std::int32_t>& cap,
+                        std::vector<std::int32_t>& inv) {
+  cap.assign(s.capacity.begin(), s.capacity.end());
+  inv.assign(static_cast<std::size_t>(I) * J, 0);
+  for (const auto& [p, row] : s.inventory)
+    for (std::int32_t j = 0; j < J && j < static_cast<std::int32_t>(row.size()); ++j)
+      inv[static_cast<std::size_t>(p) * J + j] = row[static_cast<std::size_t>(j)];
+}
+
+inline Marshalled marshal(const fo::FoEnv& env, std::span<const fo::Order> orders) {
+  Marshalled m;
+  m.J = env.node_count();
+  m.I = env.product_count();
+  const auto init = env.initial_state();
+  dense_state(init, m.J, m.I, m.capacity, m.inventory);
+  struct VecHash {
+    std::size_t operator()(const std::vector<double>& v) const noexcept {
+      std::size_t h = 1469598103934665603ull;
+      for (double x : v) {
+        std::uint64_t b;
+        std::memcpy(&b, &x, 8);
+        h = (h ^ b) * 1099511628211ull;
+      }
+      return h;
+    }
+  };
+  std::unordered_map<std::vector<double>, std::int32_t, VecHash> rows;
+  m.product.reserve(orders.size());
+  m.order_t.reserve(orders.size());
+  m.reward_row.reserve(orders.size());
+  for (const auto& o : orders) {
+    if (static_cast<std::int32_t>(o.rewards.size()) != m.J)
+      throw std::invalid_argument("order reward vector length differs from the node count");
+    auto [it, fresh] = rows.emplace(o.rewards, static_cast<std::int32_t>(rows.size()));
+    if (fresh) m.reward_table.insert(m.reward_table.end(), o.rewards.begin(), o.rewards.end());
+    m.product.push_back(o.product);
+    m.order_t.push_back(o.t);
+    m.reward_row.push_back(it->second);
+  }
+  if (m.reward_table.empty()) m.reward_table.assign(static_cast<std::size_t>(m.J), 0.0);
+  m.view = pcd_instance{m.J,
+                        m.I,
+                        static_cast<std::int64_t>(orders.size()),
+                        m.product.data(),
+                        m.order_t.data(),
+                        m.reward_row.data(),
+                        m.reward_table.data(),
+                        static_cast<std::int64_t>(m.reward_table.size() / static_cast<std::size_t>(m.J)),
+                        m.capacity.data(),
+                        m.inventory.data()};
+  return m;
+}
+
+struct PolicySpec {
+  pcd_policy view{};
+  std::vector<std::int32_t> init_cap, init_inv;
+};
+
+inline PolicySpec policy_spec(const fo::GreedyPolicy&, const Marshalled&, const DualNormalization&) {
+  PolicySpec s;
+  s.view = pcd_policy{PCD_POLICY_GREEDY, 64, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, -1};
+  return s;
+}
+inline PolicySpec policy_spec(const fo::CapacityPenalizedPolicy& p, const Marshalled&, const DualNormalization&) {
+  PolicySpec s;
+  s.view = pcd_policy{PCD_POLICY_CAPACITY, 64, p.gamma, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, -1};
+  return s;
+}
+inline PolicySpec policy_spec(const fo::DualNetworkPolicy& p, const Marshalled& m, const DualNormalization& n) {
+  PolicySpec s;
+  const auto& w = p.params();
+  if (w.widths.size() != 4 || w.widths[1] != w.widths[2])
+    throw std::invalid_argument("dual network: unsupported layer widths");
+  s.view = pcd_policy{PCD_POLICY_DUAL, w.widths[1], 0.0, w.w1.data(), w.b1.data(), w.w2.data(), w.b2.data(),
+                      w.w3.data(), w.b3.data(), nullptr, nullptr, n.horizon};
+  if (n.initial) {
+    dense_state(*n.initial, m.J, m.I, s.init_cap, s.init_inv);
+    s.view.init_capacity = s.init_cap.data();
+    s.view.init_inventory = s.init_inv.data();
+  }
+  return s;
+}
+
+// Status code -> the reference's exception types (errors.hpp, engine.hpp:140-156).
+[[noreturn]] inline void raise(int rc, const pcd_result* res = nullptr,
+                               const std::vector<pcd_trace_row>* trace = nullptr) {
+  const std::string msg = pcd_last_error();
+  if (rc == PCD_CONTRACT_VIOLATION) throw ContractViolation(msg, pcd_last_error_time_step());
+  if (rc == PCD_ITERATION_LIMIT) {
+    std::vector<PicardTraceRow> rows;
+    if (res && trace)
+      for (std::int64_t i = 0; i < res->trace_rows && i < static_cast<std::int64_t>(trace->size()); ++i) {
+        const auto& t = (*trace)[static_cast<std::size_t>(i)];
+        rows.push_back({t.chunk, t.iteration, t.changed_slots, t.max_process_evals, t.t_reset});
+      }
+    throw IterationLimitError(msg, res ? res->iterations_run : 0, std::move(rows));
+  }
+  if (rc == PCD_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);  // PCD_CUDA_ERROR: no CPU fallback exists
+}
+
+struct Handle {
+  pcd_handle* h = nullptr;
+  Handle(const pcd_instance& in, const pcd_policy& p, int device) {
+    const int rc = pcd_create(&in, &p, device, &h);
+    if (rc) raise(rc);
+  }
+  ~Handle() { pcd_destroy(h); }
+  Handle(const Handle&) = delete;
+  Handle& operator=(const Handle&) = delete;
+};
+
+inline std::vector<std::int32_t> nodes_of(std::span<const fo::FoAction> a) {
+  std::vector<std::int32_t> v;
+  v.reserve(a.size());
+  for (const auto& x : a) v.push_back(x.node);
+  return v;
+}
+
+}  // namespace detail
+
+// picard_simulate (engine.hpp:458-590) on the B200.
+template <typename P>
+PicardResult<fo::FoAction> picard_simulate(const fo::FoEnv& env, const P& policy,
+                                           std::span<const fo::Order> orders, const PartitionPlan& plan,
+                                           const PicardConfig& config = {},
+                                           std::span<const fo::FoAction> initial_cache = {},
+                                           std::span<const fo::FoAction> reference_actions = {},
+                                           DualNormalization norm = {}, int device = 0) {
+  const std::int64_t T = static_cast<std::int64_t>(orders.size());
+  if (static_cast<std::int64_t>(plan.owner.size()) != T)
+    throw ContractViolation("partition plan does not cover the horizon");
+  if (!initial_cache.empty() && static_cast<std::int64_t>(initial_cache.size()) != T)
+    throw ContractViolation("initial cache length must equal the horizon");
+  if (!reference_actions.empty() && static_cast<std::int64_t>(reference_actions.size()) != T)
+    throw ContractViolation("reference action length must equal the horizon");
+  auto m = detail::marshal(env, orders);
+  auto ps = detail::policy_spec(policy, m, norm);
+  detail::Handle h(m.view, ps.view, device);
+  int rc = pcd_set_plan(h.h, plan.owner.data(), plan.processes);
+  if (rc) detail::raise(rc);
+  const pcd_config cfg{config.processes, config.record_trace ? 1 : 0, config.max_steps, config.max_iterations,
+                       config.threads, PCD_ENGINE_AUTO, 0.0, 0, 0};
+  const auto init = detail::nodes_of(initial_cache);
+  const auto ref = detail::nodes_of(reference_actions);
+  std::vector<std::int32_t> actions(static_cast<std::size_t>(T));
+  std::vector<pcd_trace_row> trace(config.record_trace ? static_cast<std::size_t>(4 * T + 16) : 1);
+  pcd_result res{};
+  rc = pcd_simulate(h.h, &cfg, init.empty() ? nullptr : init.data(), ref.empty() ? nullptr : ref.data(),
+                    actions.data(), &res, trace.data(), config.record_trace ? static_cast<std::int64_t>(trace.size()) : 0);
+  if (rc) detail::raise(rc, &res, &trace);
+  PicardResult<fo::FoAction> out;
+  out.actions.reserve(actions.size());
+  for (auto a : actions) out.actions.push_back(fo::FoAction{a});
+  out.iterations_to_converged = res.iterations_to_converged;
+  if (res.iterations_to_correct >= 0) out.iterations_to_correct = res.iterations_to_correct;
+  out.conflicts = res.conflicts;
+  out.policy_eval_count_sequential_equivalent = res.policy_eval_count_sequential_equivalent;
+  out.total_policy_evals = res.total_policy_evals;
+  for (std::int64_t i = 0; i < res.trace_rows && config.record_trace; ++i) {
+    const auto& t = trace[static_cast<std::size_t>(i)];
+    out.trace.push_back({t.chunk, t.iteration, t.changed_slots, t.max_process_evals, t.t_reset});
+  }
+  return out;
+}
+
+// picard_iterate_once (engine.hpp:358-444) on the B200; `cache` updated in place.
+template <typename P>
+IterationOutcome picard_iterate_once(const fo::FoEnv& env, const P& policy, std::span<const fo::Order> orders,
+                                     const PartitionPlan& plan, ActionCache<fo::FoAction>& cache,
+                                     std::int64_t t_lo, std::int64_t t_hi, const fo::FoState& checkpoint_state,
+                                     DualNormalization norm = {}, int device = 0) {
+  auto m = detail::marshal(env, orders);
+  auto ps = detail::policy_spec(policy, m, norm);
+  detail::Handle h(m.view, ps.view, device);
+  int rc = pcd_set_plan(h.h, plan.owner.data(), plan.processes);
+  if (rc) detail::raise(rc);
+  std::vector<std::int32_t> ck_cap, ck_inv;
+  detail::dense_state(checkpoint_state, m.J, m.I, ck_cap, ck_inv);
+  auto c = detail::nodes_of(cache);
+  IterationOutcome out;
+  out.evals_per_process.assign(static_cast<std::size_t>(plan.processes), 0);
+  std::vector<std::int64_t> changed(std::max<std::size_t>(cache.size(), 1));
+  std::int64_t n = 0;
+  rc = pcd_iterate_once(h.h, PCD_ENGINE_AUTO, c.data(), t_lo, t_hi, ck_cap.data(), ck_inv.data(),
+                        reinterpret_cast<std::int64_t*>(out.evals_per_process.data()), changed.data(), &n);
+  if (rc) detail::raise(rc);
+  for (std::size_t t = 0; t < cache.size(); ++t) cache[t] = fo::FoAction{c[t]};
+  out.changed_slots.assign(changed.begin(), changed.begin() + n);
+  return out;
+}
+
+// sequential_simulate (engine.hpp:237-267): the serial trajectory, computed
+// on the device as the Picard fixed point (Prop. 1); policy_evals = T.
+template <typename P>
+SequentialOutput<fo::FoAction> sequential_simulate(const fo::FoEnv& env, const P& policy,
+                                                   std::span<const fo::Order> orders,
+                                                   DualNormalization norm = {}, int device = 0) {
+  auto m = detail::marshal(env, orders);
+  auto ps = detail::policy_spec(policy, m, norm);
+  detail::Handle h(m.view, ps.view, device);
+  std::vector<std::int32_t> actions(orders.size());
+  std::int64_t evals = 0;
+  const int rc = pcd_sequential(h.h, actions.data(), &evals);
+  if (rc) detail::raise(rc);
+  SequentialOutput<fo::FoAction> out;
+  for (auto a : actions) out.actions.push_back(fo::FoAction{a});
+  out.policy_evals = evals;
+  return out;
+}
+
+}  // namespace picard::b200

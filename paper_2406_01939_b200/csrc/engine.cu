@@ -134,6 +134,11 @@ struct pcd_handle {
   int32_t rank = 0, nranks = 1;
   pcd::nccl_comm comm = nullptr;
   std::vector<int32_t> rank_of;
+  std::vector<int32_t> h_roff;
+  int32_t maxn = 0;
+  pcd::DBuf<unsigned char> d_mine;
+  pcd::DBuf<int> d_roff, d_rslots, d_send, d_recv;
+  pcd::DBuf<long long> d_red;
 
   pcd::DevModel model() const {
     pcd::DevModel m{};
@@ -152,6 +157,10 @@ struct pcd_handle {
     if (stream) cudaStreamDestroy(stream);
   }
 };
+
+// multi-GPU helpers (defined with the C ABI below)
+static void exchange(pcd_handle* h, int* buf, bool reduce);
+static void rebuild_shards(pcd_handle* h);
 
 namespace pcd {
 
@@ -243,6 +252,7 @@ static void launch_product_sweep(pcd_handle* h, int lo, int hi, long long* evals
   a.ckcap = h->ckcap.p; a.hck = h->hck.p; a.ev = h->ev.p; a.xloc = h->xloc.p;
   a.cache = h->cache.p; a.written = h->written.p; a.ref = h->ref.n ? h->ref.p : nullptr;
   a.scal = h->scal; a.evals_out = evals_out;
+  a.mine = h->comm ? h->d_mine.p : nullptr;
   const int wpb = 4;
   const size_t smem = warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
   static bool attr_set[4] = {false, false, false, false};
@@ -275,6 +285,7 @@ static void launch_replay_sweep(pcd_handle* h, int lo, int hi, long long* evals_
     a.owner = h->owner.p; a.pstart = h->pstart.p; a.pslots = h->pslots.p;
     a.ckcap = h->ckcap.p; a.ckinv = h->ckinv.p; a.cache = h->cache.p; a.fresh = h->fresh.p;
     a.scratch = h->scratch.p; a.scal = h->scal; a.evals_out = evals_out;
+    a.mine = h->comm ? h->d_mine.p : nullptr;
     const int nproc = a.m1 - a.m0;
     k_sweep_replay<KIND><<<(nproc + wpb - 1) / wpb, wpb * 32, smem, h->stream>>>(a);
     CK(cudaGetLastError());
@@ -371,12 +382,24 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     } else {
       dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
     }
+    exchange(h, h->cache.p, true);  // N>1: owned slots + convergence scalars
+    if (h->comm)  // every window slot is owned by some rank: all written now
+      CK(cudaMemsetAsync(h->written.p + lo, 1, (size_t)W, h->stream));
     h->timing.sweep_ms += tm.stop_ms();
     h->timing.kernel_launches += 1;
     h->timing.sweep_launches += 1;
   } else {
     tm.start();
     dispatch_kind(h->kind, [&](auto k) { launch_replay_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
+    if (h->comm) {  // fresh[] slices to every rank; then a replicated publish
+      exchange(h, h->fresh.p, false);
+      k_scalars_pack<<<1, 1, 0, h->stream>>>(h->scal, h->d_red.p);
+      int rc = g_nccl.AllReduce(h->d_red.p + 3, h->d_red.p + 3, 1, ncclInt64, ncclSum, h->comm, h->stream);
+      if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 5, h->d_red.p + 5, 2, ncclUint64, ncclMin, h->comm, h->stream);
+      if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 7, h->d_red.p + 7, 1, ncclUint64, ncclMax, h->comm, h->stream);
+      if (rc) throw CudaError(std::string("ncclAllReduce: ") + g_nccl.GetErrorString(rc));
+      k_scalars_unpack<<<1, 1, 0, h->stream>>>(h->d_red.p, h->scal);
+    }
     h->timing.sweep_ms += tm.stop_ms();
     h->timing.sweep_launches += 1;
     h->timing.kernel_launches += 1;
@@ -587,6 +610,83 @@ static void validate_instance(const pcd_instance* in) {
     if (!std::isfinite(in->reward_table[i])) throw InvalidArgument("rewards must be finite");
 }
 
+// Process sharding (this rank's processes; all ranks' slot lists for the
+// exchange) and the tensor-core tiles of this rank's processes.
+static void rebuild_shards(pcd_handle* h) {
+  if (!h->have_plan) return;
+  const int32_t M = h->M;
+  const int64_t T = h->T;
+  const std::vector<int32_t>& owner = h->h_owner;
+  std::vector<int64_t> load((size_t)M, 0);
+  for (int64_t t = 0; t < T; ++t) load[(size_t)owner[(size_t)t]] += 1;
+  h->rank_of.assign((size_t)M, 0);
+  if (h->comm) {
+    shard_processes(owner.data(), T, M, h->nranks, h->rank_of.data());
+    std::vector<unsigned char> mine((size_t)M);
+    for (int32_t m = 0; m < M; ++m) mine[(size_t)m] = h->rank_of[(size_t)m] == h->rank;
+    h->d_mine.upload(mine.data(), mine.size(), h->stream);
+    // rank-major, time-ordered slot lists (counting sort) for pack / unpack
+    std::vector<int32_t> off((size_t)h->nranks + 1, 0), slots((size_t)std::max<int64_t>(T, 1));
+    for (int64_t t = 0; t < T; ++t) off[(size_t)h->rank_of[(size_t)owner[(size_t)t]] + 1] += 1;
+    for (int32_t r = 0; r < h->nranks; ++r) off[(size_t)r + 1] += off[(size_t)r];
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int64_t t = 0; t < T; ++t) slots[(size_t)fill[(size_t)h->rank_of[(size_t)owner[(size_t)t]]]++] = (int32_t)t;
+    h->h_roff = off;
+    h->maxn = 0;
+    for (int32_t r = 0; r < h->nranks; ++r) h->maxn = std::max(h->maxn, off[(size_t)r + 1] - off[(size_t)r]);
+    h->d_roff.upload(off.data(), off.size(), h->stream);
+    h->d_rslots.upload(slots.data(), slots.size(), h->stream);
+    h->d_send.alloc((size_t)std::max(1, h->maxn));
+    h->d_recv.alloc((size_t)std::max(1, h->maxn) * h->nranks);
+    h->d_red.alloc(8);
+  }
+  // tensor-core tiles: this rank's non-empty processes, heaviest first. The
+  // per-row CUDA-core work (features, epilogues) dominates a step, so spread
+  // the processes over every SM (one CTA each, <= 128 rows), round robin in
+  // load order so all tiles carry the same critical path.
+  std::vector<int32_t> procs;
+  for (int32_t m = 0; m < M; ++m)
+    if (load[(size_t)m] > 0 && h->rank_of[(size_t)m] == h->rank) procs.push_back(m);
+  std::stable_sort(procs.begin(), procs.end(),
+                   [&](int32_t a, int32_t b) { return load[(size_t)a] > load[(size_t)b]; });
+  h->max_load = procs.empty() ? 0 : load[(size_t)procs[0]];
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+  const int64_t n = (int64_t)procs.size();
+  h->tc_tiles = (int32_t)std::max<int64_t>((n + kTcRows - 1) / kTcRows, std::min<int64_t>(nsm, n));
+  std::vector<int32_t> rows((size_t)std::max(1, h->tc_tiles) * kTcRows, -1);
+  for (int64_t k = 0; k < n; ++k)
+    rows[(size_t)(k % h->tc_tiles) * kTcRows + (size_t)(k / h->tc_tiles)] = procs[(size_t)k];
+  h->tc_rows.upload(rows.data(), rows.size(), h->stream);
+  h->tc_D.alloc(rows.size() * (size_t)std::max(1, h->J));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+// After a sweep on N>1 ranks: gather every rank's owned slots of `buf` (the
+// cache for the fused product sweeps, fresh[] for the replay sweep) and, for
+// the fused sweeps, reduce the per-rank convergence scalars.
+static void exchange(pcd_handle* h, int* buf, bool reduce) {
+  if (!h->comm) return;  // single GPU without a communicator
+  const int r = h->rank;
+  const int n = h->h_roff[(size_t)r + 1] - h->h_roff[(size_t)r];
+  k_pack_slots<<<grid_for(std::max(1, n), 256), 256, 0, h->stream>>>(buf, h->d_rslots.p + h->h_roff[(size_t)r], n,
+                                                                     h->d_send.p);
+  int rc = g_nccl.AllGather(h->d_send.p, h->d_recv.p, (size_t)h->maxn, ncclInt32, h->comm, h->stream);
+  if (rc) throw CudaError(std::string("ncclAllGather: ") + g_nccl.GetErrorString(rc));
+  k_unpack_slots<<<grid_for((long long)h->maxn * h->nranks, 256), 256, 0, h->stream>>>(
+      h->d_recv.p, h->d_rslots.p, h->d_roff.p, h->nranks, h->maxn, buf);
+  if (reduce) {
+    k_scalars_pack<<<1, 1, 0, h->stream>>>(h->scal, h->d_red.p);
+    rc = g_nccl.AllReduce(h->d_red.p, h->d_red.p, 4, ncclInt64, ncclSum, h->comm, h->stream);
+    if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 4, h->d_red.p + 4, 3, ncclUint64, ncclMin, h->comm, h->stream);
+    if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 7, h->d_red.p + 7, 1, ncclUint64, ncclMax, h->comm, h->stream);
+    if (rc) throw CudaError(std::string("ncclAllReduce: ") + g_nccl.GetErrorString(rc));
+    k_scalars_unpack<<<1, 1, 0, h->stream>>>(h->d_red.p, h->scal);
+  }
+  CK(cudaGetLastError());
+  h->timing.kernel_launches += reduce ? 4 : 2;
+}
+
 // Weight images for the tcgen05 sweep (tc_sweep.cuh): fp16 hi + 2^11-scaled lo
 // parts in the canonical K-major no-swizzle UMMA layout, W3' = W3[:J] + W3[J:]
 // (the score needs only p_j + p_{J+j}), fp32 biases and feature reciprocals.
@@ -737,30 +837,7 @@ extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
   h->is_product = hf == 0;
   h->have_plan = true;
   ensure_state_buffers(h);
-  // tensor-core tiles: non-empty processes, heaviest first, 128 per CTA
-  {
-    std::vector<int64_t> load((size_t)M, 0);
-    for (int64_t t = 0; t < h->T; ++t) load[(size_t)owner[t]] += 1;
-    std::vector<int32_t> procs;
-    for (int32_t m = 0; m < M; ++m)
-      if (load[(size_t)m] > 0) procs.push_back(m);
-    std::stable_sort(procs.begin(), procs.end(),
-                     [&](int32_t a, int32_t b) { return load[(size_t)a] > load[(size_t)b]; });
-    h->max_load = procs.empty() ? 0 : load[(size_t)procs[0]];
-    // The per-row CUDA-core work (features, epilogues) dominates a step, so
-    // spread the processes over every SM (one CTA each, <= 128 rows), round
-    // robin in load order so all tiles carry the same critical path.
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-    const int64_t n = (int64_t)procs.size();
-    h->tc_tiles = (int32_t)std::max<int64_t>((n + kTcRows - 1) / kTcRows, std::min<int64_t>(nsm, n));
-    std::vector<int32_t> rows((size_t)std::max(1, h->tc_tiles) * kTcRows, -1);
-    for (int64_t k = 0; k < n; ++k)
-      rows[(size_t)(k % h->tc_tiles) * kTcRows + (size_t)(k / h->tc_tiles)] = procs[(size_t)k];
-    h->tc_rows.upload(rows.data(), rows.size(), h->stream);
-    h->tc_D.alloc(rows.size() * (size_t)std::max(1, h->J));
-    CK(cudaStreamSynchronize(h->stream));
-  }
+  rebuild_shards(h);
   return PCD_OK;
   PCD_CATCH
 }
@@ -997,6 +1074,7 @@ extern "C" int pcd_attach_comm(pcd_handle* h, const unsigned char id[128], int32
   if (rc != 0) throw CudaError(std::string("ncclCommInitRank failed: ") + g_nccl.GetErrorString(rc));
   h->rank = rank;
   h->nranks = nranks;
+  rebuild_shards(h);
   return PCD_OK;
   PCD_CATCH
 }

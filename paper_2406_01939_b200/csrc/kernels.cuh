@@ -147,6 +147,7 @@ struct SweepArgs {
   const int* ref;
   Scalars* scal;
   long long* evals_out;  // optional [M]
+  const unsigned char* mine;  // [M] processes of this rank (multi-GPU), nullptr = all
 };
 
 __device__ __forceinline__ void carve_warp_smem(unsigned char* base, int warp, int J, int in, int H,
@@ -190,7 +191,7 @@ static __global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (m >= a.M) return;
+  if (m >= a.M || (a.mine && !a.mine[m])) return;
   const int J = a.J;
   int *D, *crow, *prow;
   WarpScratch ws;
@@ -281,6 +282,7 @@ struct ReplayArgs {
   int* scratch;  // [(m1-m0) * I * J]
   Scalars* scal;
   long long* evals_out;
+  const unsigned char* mine;  // [M] or nullptr
 };
 
 // ---------------------------------------------------------------------------
@@ -294,7 +296,7 @@ static __global__ void __launch_bounds__(128) k_sweep_replay(ReplayArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.m0 + blockIdx.x * (blockDim.x >> 5) + warp;
-  if (m >= a.m1) return;
+  if (m >= a.m1 || (a.mine && !a.mine[m])) return;
   const int J = a.J;
   int *caps, *unused1, *unused2;
   WarpScratch ws;
@@ -479,6 +481,39 @@ static __global__ void k_transpose_f64(const double* __restrict__ src, int rows,
   if (i >= (long long)rows * cols) return;
   const int r = (int)(i / cols), c = (int)(i % cols);
   dst[(size_t)c * rows + r] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU exchange: every rank packs the cache values of
+// the slots its processes own (rank-major slot CSR, time order) and one
+// ncclAllGather delivers every rank's slice; each rank scatters them back.
+// ---------------------------------------------------------------------------
+static __global__ void k_pack_slots(const int* __restrict__ src, const int* __restrict__ slots, int n,
+                                    int* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[slots[i]];
+}
+static __global__ void k_unpack_slots(const int* __restrict__ in, const int* __restrict__ slots,
+                                      const int* __restrict__ roff, int nranks, int maxn, int* __restrict__ dst) {
+  const long long total = (long long)nranks * maxn;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(g / maxn), i = (int)(g % maxn);
+    if (i < roff[r + 1] - roff[r]) dst[slots[roff[r] + i]] = in[g];
+  }
+}
+// Scalars <-> [sum: changed, conflicts, mismatch, total_evals | min: first,
+// err_nonfinite, err_infeasible | max: max_evals] (int64 reduction buffer).
+static __global__ void k_scalars_pack(const Scalars* s, long long* b) {
+  b[0] = (long long)s->changed; b[1] = (long long)s->conflicts; b[2] = s->mismatch_delta;
+  b[3] = (long long)s->total_evals;
+  b[4] = (long long)s->first_changed; b[5] = (long long)s->err_nonfinite; b[6] = (long long)s->err_infeasible;
+  b[7] = (long long)s->max_evals;
+}
+static __global__ void k_scalars_unpack(const long long* b, Scalars* s) {
+  s->changed = (unsigned long long)b[0]; s->conflicts = (unsigned long long)b[1]; s->mismatch_delta = b[2];
+  s->total_evals = (unsigned long long)b[3];
+  s->first_changed = (unsigned long long)b[4]; s->err_nonfinite = (unsigned long long)b[5];
+  s->err_infeasible = (unsigned long long)b[6];
+  s->max_evals = (unsigned long long)b[7];
 }
 
 }  // namespace pcd

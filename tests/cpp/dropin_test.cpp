@@ -1,0 +1,183 @@
+// dropin_test.cpp — the reference's own engine scenarios driven through the
+// B200 drop-in (include/picard_b200.hpp) and checked against the UNMODIFIED
+// reference CPU engine (compiled from /root/reference/proj). Restates the
+// engine cases of test_engine.cpp (:81-138, :140-173, :301-348, :350-371,
+// :395-414, :455-477, :525-545) with the same fixtures (test_helpers.hpp).
+// Build: make -C tests/cpp (here, where the reference tree exists); the
+// binary travels to the GPU box. Exit code = number of failed checks.
+#include <cstdio>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "picard/engine.hpp"
+#include "picard/fo/env.hpp"
+#include "picard/fo/instance.hpp"
+#include "picard/fo/policies.hpp"
+#include "picard/rng.hpp"
+#include "picard_b200.hpp"
+
+using namespace picard;
+using namespace picard::fo;
+
+static int failures = 0, checks = 0;
+#define CHECK(c)                                                             \
+  do {                                                                       \
+    ++checks;                                                                \
+    if (!(c)) {                                                              \
+      ++failures;                                                            \
+      std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #c);    \
+    }                                                                        \
+  } while (0)
+
+static Instance toy() {  // test_helpers.hpp:17-29 (fixture restated)
+  Instance inst;
+  inst.nodes = 2;
+  inst.products = 1;
+  inst.horizon = 2;
+  inst.initial.capacity = {1, 1};
+  inst.initial.inventory[0] = {1, 1};
+  inst.orders.resize(2);
+  inst.orders[0] = {0, 0, 0, {0.9, 0.1}};
+  inst.orders[1] = {1, 0, 0, {0.8, 0.2}};
+  return inst;
+}
+
+static Instance small_random(std::uint64_t seed) {  // test_helpers.hpp:31-41
+  auto gen = rng::make(seed);
+  const auto nodes = static_cast<std::int32_t>(2 + rng::below(gen, 4));
+  const auto products = static_cast<std::int32_t>(1 + rng::below(gen, 12));
+  const auto horizon = static_cast<std::int64_t>(1 + rng::below(gen, 60));
+  const double beta = -static_cast<double>(rng::below(gen, 11)) / 10.0;
+  const double coverage = 0.5 + 0.5 * rng::unit(gen);
+  return generate_instance(nodes, products, horizon, beta, coverage, seed ^ 0x9e3779b97f4a7c15ull);
+}
+
+template <typename P>
+static void compare(const Instance& inst, const P& policy, const PartitionPlan& plan, PicardConfig cfg,
+                    std::span<const FoAction> init = {}) {
+  const auto env = inst.make_env();
+  const std::span<const Order> orders(inst.orders);
+  const auto oracle = sequential_simulate(env, policy, orders);
+  cfg.record_trace = true;
+  const auto want = picard_simulate(env, policy, orders, plan, cfg, init, std::span<const FoAction>(oracle.actions));
+  const auto got = b200::picard_simulate(env, policy, orders, plan, cfg, init, std::span<const FoAction>(oracle.actions));
+  CHECK(got.actions == want.actions);
+  CHECK(got.actions == oracle.actions);
+  CHECK(got.iterations_to_converged == want.iterations_to_converged);
+  CHECK(got.iterations_to_correct == want.iterations_to_correct);
+  CHECK(got.conflicts == want.conflicts);
+  CHECK(got.policy_eval_count_sequential_equivalent == want.policy_eval_count_sequential_equivalent);
+  CHECK(got.total_policy_evals == want.total_policy_evals);
+  CHECK(got.trace.size() == want.trace.size());
+  for (std::size_t i = 0; i < std::min(got.trace.size(), want.trace.size()); ++i) {
+    CHECK(got.trace[i].iteration == want.trace[i].iteration);
+    CHECK(got.trace[i].changed_slots == want.trace[i].changed_slots);
+    CHECK(got.trace[i].max_process_evals == want.trace[i].max_process_evals);
+    CHECK(got.trace[i].t_reset == want.trace[i].t_reset);
+    CHECK(got.trace[i].chunk == want.trace[i].chunk);
+  }
+  const auto seq = b200::sequential_simulate(env, policy, orders);
+  CHECK(seq.actions == oracle.actions);
+  CHECK(seq.policy_evals == oracle.policy_evals);
+}
+
+int main() {
+  // toy two-process hand trace (test_engine.cpp:100-138)
+  {
+    const auto inst = toy();
+    const auto env = inst.make_env();
+    PartitionPlan plan;
+    plan.processes = 2;
+    plan.owner = {0, 1};
+    ActionCache<FoAction> cache(2, kNoFulfill);
+    const auto first = b200::picard_iterate_once(env, GreedyPolicy{}, std::span<const Order>(inst.orders), plan,
+                                                 cache, 0, 2, env.initial_state());
+    CHECK(cache[0] == FoAction{0});
+    CHECK(cache[1] == FoAction{0});
+    CHECK(first.changed_slots == (std::vector<std::int64_t>{0, 1}));
+    CHECK(first.evals_per_process == (std::vector<std::int64_t>{1, 1}));
+    compare(inst, GreedyPolicy{}, plan, {});
+  }
+  // infeasible cached action degrades to declining (test_engine.cpp:140-173)
+  {
+    Instance inst;
+    inst.nodes = 1;
+    inst.products = 1;
+    inst.horizon = 3;
+    inst.initial.capacity = {1};
+    inst.initial.inventory[0] = {3};
+    for (std::int32_t t = 0; t < 3; ++t) inst.orders.push_back(Order{t, 0, 0, {1.0}});
+    PartitionPlan plan;
+    plan.processes = 2;
+    plan.owner = {0, 1, 0};
+    const std::vector<FoAction> over(3, FoAction{0});
+    compare(inst, GreedyPolicy{}, plan, {}, std::span<const FoAction>(over));
+  }
+  // oracle equivalence grid (test_engine.cpp:301-348)
+  for (std::uint64_t seed = 100; seed < 140; ++seed) {
+    const auto inst = small_random(seed);
+    auto gen = rng::make(seed * 977);
+    const auto M = static_cast<std::int32_t>(1 + rng::below(gen, 8));
+    const bool product = rng::below(gen, 2) == 0;
+    const auto plan = product ? make_product_partition(inst, M, seed)
+                              : make_uniform_time_partition(inst.horizon, M, seed);
+    PicardConfig cfg;
+    cfg.max_steps = static_cast<std::int64_t>(rng::below(gen, 3) == 0 ? 0 : 1 + rng::below(gen, 20));
+    compare(inst, GreedyPolicy{}, plan, cfg);
+    compare(inst, CapacityPenalizedPolicy{rng::unit(gen) * 2.0}, plan, cfg);
+    if (seed % 4 == 0) compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, seed + 5), plan, cfg);
+  }
+  // warm starts with windows (test_engine.cpp:350-371, :395-414)
+  for (std::uint64_t seed = 200; seed < 212; ++seed) {
+    const auto inst = small_random(seed);
+    const auto env = inst.make_env();
+    const auto plan = make_product_partition(inst, 4, seed);
+    const auto draft = sequential_simulate(env, CapacityPenalizedPolicy{1.0}, std::span<const Order>(inst.orders));
+    for (std::int64_t ms : {0, 5}) {
+      PicardConfig cfg;
+      cfg.max_steps = ms;
+      compare(inst, GreedyPolicy{}, plan, cfg, std::span<const FoAction>(draft.actions));
+    }
+  }
+  // a J=30 dual run at a larger size (generated instance, product partition)
+  {
+    const auto inst = generate_instance(30, 200, 6000, -0.3, 0.8, 7);
+    compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, 5),
+            make_product_partition(inst, 64, 1), {});
+    compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, 5),
+            make_uniform_time_partition(inst.horizon, 16, 3), {});
+  }
+  // iteration cap (test_engine.cpp:525-545)
+  {
+    const auto inst = toy();
+    const auto env = inst.make_env();
+    PartitionPlan plan;
+    plan.processes = 2;
+    plan.owner = {0, 1};
+    PicardConfig cfg;
+    cfg.max_iterations = 1;
+    cfg.record_trace = true;
+    bool thrown = false;
+    try {
+      b200::picard_simulate(env, GreedyPolicy{}, std::span<const Order>(inst.orders), plan, cfg);
+    } catch (const IterationLimitError& e) {
+      thrown = true;
+      CHECK(e.iterations_run() == 1);
+      CHECK(e.partial_trace().size() == 1);
+    }
+    CHECK(thrown);
+    PartitionPlan bad;
+    bad.processes = 2;
+    bad.owner = {0, 5};
+    bool cv = false;
+    try {
+      b200::picard_simulate(env, GreedyPolicy{}, std::span<const Order>(inst.orders), bad, {});
+    } catch (const ContractViolation&) {
+      cv = true;
+    }
+    CHECK(cv);
+  }
+  std::printf("dropin_test: %d checks, %d failures\n", checks, failures);
+  return failures;
+}

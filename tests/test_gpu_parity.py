@@ -298,3 +298,34 @@ def test_tensor_core_and_fp64_sweeps_agree_with_warm_start_and_windows():
         assert a.timing["tc_used"] == 1 and b.timing["tc_used"] == 0
         assert a.actions.tolist() == b.actions.tolist()
         assert [x.astuple() for x in a.trace] == [x.astuple() for x in b.trace]
+
+
+def test_cpp_dropin_matches_reference_engine():
+    """The reference's own engine scenarios through include/picard_b200.hpp,
+    checked against the UNMODIFIED reference CPU engine (tests/cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_build", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/_build/dropin_test not built (needs the reference tree)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
+
+
+def test_single_rank_nccl_path_matches():
+    """The multi-GPU exchange (pack -> ncclAllGather -> unpack, scalar
+    all-reduces) exercised with a one-rank communicator: identical results."""
+    ons, inst, owner, opol, pol = _dual_case(30, 200, 12000, 256, "product")
+    seq, _ = ORC.sequential(ons, opol)
+    want = P.picard_simulate(inst, pol, P.PartitionPlan(256, owner), P.PicardConfig(record_trace=True),
+                             reference_actions=seq)
+    uid = P.nccl_unique_id()
+    for engine in ("auto", "product_fp64", "replay"):
+        with P.Simulator(inst, pol) as sim:
+            sim.set_plan(P.PartitionPlan(256, owner))
+            sim.attach_comm(uid if engine == "auto" else P.nccl_unique_id(), 0, 1)
+            r = sim.simulate(P.PicardConfig(record_trace=True, engine=engine), reference_actions=seq)
+        assert r.actions.tolist() == seq.tolist()
+        assert [x.astuple() for x in r.trace] == [x.astuple() for x in want.trace]
+        assert (r.conflicts, r.iterations_to_correct) == (want.conflicts, want.iterations_to_correct)
