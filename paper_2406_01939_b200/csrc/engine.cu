@@ -126,7 +126,7 @@ struct pcd_handle {
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   pcd::DBuf<unsigned char> tc_wimg;
   pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf;
-  pcd::DBuf<int> tc_rows, tc_D;
+  pcd::DBuf<int> tc_rows;
   pcd::DBuf<unsigned long long> tc_stats;
   int32_t tc_tiles = 0;
   int64_t max_load = 0;
@@ -323,12 +323,14 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   s.ckcap = h->ckcap.p; s.hck = h->hck.p; s.ev = h->ev.p; s.xloc = h->xloc.p;
   s.cache = h->cache.p; s.written = h->written.p; s.ref = h->ref.n ? h->ref.p : nullptr;
   s.scal = h->scal; s.evals_out = evals_out;
-  a.rows = h->tc_rows.p; a.D = h->tc_D.p; a.wimg = h->tc_wimg.p;
+  a.rows = h->tc_rows.p; a.wimg = h->tc_wimg.p;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p;
   a.guard = (float)(guard > 0 ? guard : 5e-5);
   a.verify = verify;
   a.stats = h->tc_stats.p;
+  static const int pf = getenv("PCD_TC_PF") ? atoi(getenv("PCD_TC_PF")) : 0;  // tuning knob
+  a.pf = pf;
   // PCD_TC_PROF=1: per-phase clock64 totals of CTA 0, printed to stderr (debug)
   static const bool prof = getenv("PCD_TC_PROF") != nullptr;
   static DBuf<long long> dprof;
@@ -337,7 +339,6 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     CK(cudaMemsetAsync(dprof.p, 0, 20 * sizeof(long long), h->stream));
     a.prof = dprof.p;
   }
-  a.fake = getenv("PCD_TC_FAKE") != nullptr;
   launch_tc_sweep(a, h->tc_tiles, h->stream);
   CK(cudaGetLastError());
   if (prof) {
@@ -346,7 +347,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     CK(cudaStreamSynchronize(h->stream));
     fprintf(stderr, "tcprof steps=%lld F=%lld(own %lld) L1=%lld E1=%lld L2=%lld E2=%lld L3=%lld S=%lld fin=%lld chk=%lld U=%lld\n",
             v[10], v[0], v[11], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
-    fprintf(stderr, "tcprof F: loads=%lld xpart=%lld dupd=%lld scr=%lld feat=%lld\n", v[12], v[13], v[14], v[15], v[16]);
+    fprintf(stderr, "tcprof F: loads=%lld feat=%lld x=%lld\n", v[12], v[13], v[14]);
   }
 }
 
@@ -363,16 +364,21 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     const int tpb = std::max(1, std::min(128, (int)((40 * 1024) / (4 * std::max(1, J)))));
     k_effective<<<(h->I + tpb - 1) / tpb, tpb, (size_t)tpb * J * 4, h->stream>>>(
         h->qstart.p, h->qslots.p, h->I, lo, hi, h->cache.p, h->ckinv.p, J, h->ev.p);
-    const int nb = (W + kK - 1) >> kLogK;
-    k_block_hist<<<nb, 128, (size_t)J * 4, h->stream>>>(h->ev.p, lo, W, J, h->hck.p);
+    const int nb = hck_rows(lo, hi);
     const int nseg = (nb + kSegRows - 1) / kSegRows;
-    k_seg_sums<<<nseg, 128, 0, h->stream>>>(h->hck.p, nb, J, h->seg.p);
-    k_seg_scan<<<1, 128, 0, h->stream>>>(h->seg.p, nseg, J);
-    k_seg_apply<<<nseg, 128, 0, h->stream>>>(h->hck.p, nb, J, h->seg.p);
+    const size_t hsm = (size_t)kSegRows * J * 4;
+    static size_t hsm_set = 0;
+    if (hsm > 48 * 1024 && hsm > hsm_set) {
+      CK(cudaFuncSetAttribute(k_hist_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+      hsm_set = hsm;
+    }
+    k_seg_count<<<nseg, 256, (size_t)J * 4, h->stream>>>(h->ev.p, lo, hi, J, h->seg.p);
+    k_seg_scan<<<J, 256, 0, h->stream>>>(h->seg.p, nseg, J);
+    k_hist_prefix<<<nseg, 256, hsm, h->stream>>>(h->ev.p, lo, hi, J, nb, h->seg.p, h->hck.p);
     CK(cudaMemcpyAsync(h->xloc.p, h->ckinv.p, sizeof(int) * (size_t)h->I * J, cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaGetLastError());
     h->timing.prep_ms += tm.stop_ms();
-    h->timing.kernel_launches += 6;
+    h->timing.kernel_launches += 4;
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {
@@ -470,15 +476,15 @@ static void ensure_state_buffers(pcd_handle* h) {
   const size_t IJ = std::max<size_t>(1, (size_t)h->I * h->J);
   h->cache.alloc(T);
   h->fresh.alloc(T);
-  h->ev.alloc(T);
+  h->ev.alloc(T + kK);  // + kK: the sweep reads whole K-slot blocks
   h->written.alloc(T);
   h->ckcap.alloc(std::max(1, h->J));
   h->ckinv.alloc(IJ);
   h->ckbak.alloc(IJ + h->J);
   h->xloc.alloc(IJ);
-  const size_t nb = (T + kK - 1) / kK;
-  h->hck.alloc(nb * std::max(1, h->J));
-  h->seg.alloc(((nb + kSegRows - 1) / kSegRows + 1) * std::max(1, h->J));
+  const size_t nb = (T + kK - 1) / kK + 1;  // + 1: blocks start at lo & ~(K-1)
+  h->hck.alloc(nb * hck_stride(std::max(1, h->J)));
+  h->seg.alloc(((nb + kSegRows - 1) / kSegRows + 1) * seg_stride(std::max(1, h->J)));
   h->evals.alloc(std::max(1, h->M));
 }
 
@@ -658,7 +664,6 @@ static void rebuild_shards(pcd_handle* h) {
   for (int64_t k = 0; k < n; ++k)
     rows[(size_t)(k % h->tc_tiles) * kTcRows + (size_t)(k / h->tc_tiles)] = procs[(size_t)k];
   h->tc_rows.upload(rows.data(), rows.size(), h->stream);
-  h->tc_D.alloc(rows.size() * (size_t)std::max(1, h->J));
   CK(cudaStreamSynchronize(h->stream));
 }
 
@@ -723,8 +728,10 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
   h->tc_b3.upload(b3.data(), b3.size(), h->stream);
   h->tc_ic0.upload(ic0.data(), ic0.size(), h->stream);
   h->tc_ix0.upload(ix0.data(), ix0.size(), h->stream);
-  std::vector<float> rtf((size_t)h->R * J);
-  for (size_t i = 0; i < rtf.size(); ++i) rtf[i] = (float)rtab[i];
+  const int RJ = (J + 7) & ~7;  // 32-byte rows for the 256-bit loads of the score phase
+  std::vector<float> rtf((size_t)h->R * RJ, 0.f);
+  for (int64_t rr = 0; rr < h->R; ++rr)
+    for (int j = 0; j < J; ++j) rtf[(size_t)rr * RJ + j] = (float)rtab[(size_t)rr * J + j];
   h->tc_rtf.upload(rtf.data(), rtf.size(), h->stream);
   h->tc_stats.alloc(4);
   CK(cudaStreamSynchronize(h->stream));

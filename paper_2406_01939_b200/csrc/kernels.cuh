@@ -12,7 +12,11 @@
 //   ckcap[J], ckinv[I*J]                  int32   checkpoint FoState (dense)
 //   xloc[I*J]                             int32   per-iteration own-product inventory
 //   ev[T]                                 int32   effective cached attempt (node or -1)
-//   hck[nb*J]                             int32   per-node prefix counts of ev every K=32 slots
+//   hck[nb*HJ]                            int32   hck[b][j] = H(b)[j] = effective attempts at
+//                                                 node j in [lo, base + 8b), base = lo & ~7
+//                                                 (K=8 blocks aligned on absolute slots; rows
+//                                                 padded to 8 nodes = 32 bytes)
+//   seg[nseg*SJ]                          int32   scratch: per-segment totals / offsets
 #pragma once
 
 #include <cstdint>
@@ -22,9 +26,18 @@
 
 namespace pcd {
 
-constexpr int kLogK = 5;  // checkpoint stride K = 32 slots (one warp-wide partial scan)
+constexpr int kLogK = 3;  // checkpoint stride K = 8 slots (partial block <= 7 events)
 constexpr int kK = 1 << kLogK;
-constexpr int kSegRows = 256;  // checkpoint rows per scan segment
+constexpr int kLogSeg = 6;
+constexpr int kSegRows = 1 << kLogSeg;  // checkpoint rows per scan segment
+
+__host__ __device__ __forceinline__ int hck_stride(int J) { return (J + 7) & ~7; }  // 32-byte rows
+__host__ __device__ __forceinline__ int seg_stride(int J) { return (J + 7) & ~7; }
+__host__ __device__ __forceinline__ int hck_base(int lo) { return lo & ~(kK - 1); }
+// checkpoint rows covering the window [lo, hi)
+__host__ __device__ __forceinline__ int hck_rows(int lo, int hi) {
+  return (hi - hck_base(lo) + kK - 1) >> kLogK;
+}
 
 struct Scalars {
   unsigned long long changed;
@@ -80,56 +93,79 @@ static __global__ void k_effective(const int* __restrict__ qstart, const int* __
   }
 }
 
-// Per K-slot block histogram of effective attempts: hck[b][j].
-static __global__ void k_block_hist(const int* __restrict__ ev, int lo, int W, int J, int* __restrict__ hck) {
-  extern __shared__ int hist[];
-  const int b = blockIdx.x;
-  for (int j = threadIdx.x; j < J; j += blockDim.x) hist[j] = 0;
+// Prefix counts of effective attempts, reduce-then-scan over segments of
+// kSegRows K-slot blocks: (1) per-segment totals, (2) exclusive scan of the
+// totals per node (seg[] then holds H at every segment start), (3) per-block
+// histograms in smem scanned from the segment offset and written once as the
+// final prefix (ev is read twice, hck written once).
+static __global__ void k_seg_count(const int* __restrict__ ev, int lo, int hi, int J, int* __restrict__ seg) {
+  extern __shared__ int cs[];  // [J]
+  const int sg = blockIdx.x, SJ = seg_stride(J);
+  for (int j = threadIdx.x; j < J; j += blockDim.x) cs[j] = 0;
   __syncthreads();
-  const int s0 = b << kLogK;
-  for (int s = s0 + threadIdx.x; s < min(W, s0 + kK); s += blockDim.x) {
-    const int e = ev[lo + s];
-    if (e >= 0) atomicAdd(&hist[e], 1);
+  const int base = hck_base(lo);
+  const int s0 = max(lo, base + (sg << (kLogSeg + kLogK))), s1 = min(hi, base + ((sg + 1) << (kLogSeg + kLogK)));
+  for (int s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    const int e = ev[s];
+    if (e >= 0) atomicAdd(&cs[e], 1);
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < J; j += blockDim.x) hck[(size_t)b * J + j] = hist[j];
+  for (int j = threadIdx.x; j < SJ; j += blockDim.x) seg[(size_t)sg * SJ + j] = j < J ? cs[j] : 0;
 }
 
-// Column sums of each segment of kSegRows checkpoint rows.
-static __global__ void k_seg_sums(const int* __restrict__ hck, int nb, int J, int* __restrict__ seg) {
-  const int s = blockIdx.x;
-  const int r0 = s * kSegRows, r1 = min(nb, r0 + kSegRows);
-  for (int j = threadIdx.x; j < J; j += blockDim.x) {
-    int acc = 0;
-    for (int r = r0; r < r1; ++r) acc += hck[(size_t)r * J + j];
-    seg[(size_t)s * J + j] = acc;
-  }
-}
-
-// Exclusive scan of the segment sums over segments, per column (one CTA).
+// Exclusive scan of the segment totals over segments: one CTA per node j.
 static __global__ void k_seg_scan(int* __restrict__ seg, int nseg, int J) {
-  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+  __shared__ int part[256];
+  const int j = blockIdx.x, SJ = seg_stride(J);
+  const int per = (nseg + blockDim.x - 1) / blockDim.x;
+  const int s0 = threadIdx.x * per, s1 = min(nseg, s0 + per);
+  int sum = 0;
+  for (int s = s0; s < s1; ++s) sum += seg[(size_t)s * SJ + j];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int acc = 0;
-    for (int s = 0; s < nseg; ++s) {
-      const int v = seg[(size_t)s * J + j];
-      seg[(size_t)s * J + j] = acc;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int v = part[i];
+      part[i] = acc;
       acc += v;
     }
   }
+  __syncthreads();
+  int acc = part[threadIdx.x];
+  for (int s = s0; s < s1; ++s) {
+    const int v = seg[(size_t)s * SJ + j];
+    seg[(size_t)s * SJ + j] = acc;
+    acc += v;
+  }
 }
 
-// In-segment exclusive scan plus the segment offset: hck[b][j] becomes the
-// number of effective attempts at node j in [lo, lo + b*K).
-static __global__ void k_seg_apply(int* __restrict__ hck, int nb, int J, const int* __restrict__ seg) {
-  const int s = blockIdx.x;
-  const int r0 = s * kSegRows, r1 = min(nb, r0 + kSegRows);
+static __global__ void k_hist_prefix(const int* __restrict__ ev, int lo, int hi, int J, int nb,
+                                     const int* __restrict__ seg, int* __restrict__ hck) {
+  extern __shared__ int hs[];  // [kSegRows][J]
+  const int sg = blockIdx.x, HJ = hck_stride(J), SJ = seg_stride(J);
+  const int b0 = sg << kLogSeg, nrows = min(kSegRows, nb - b0);
+  for (int i = threadIdx.x; i < kSegRows * J; i += blockDim.x) hs[i] = 0;
+  __syncthreads();
+  const int base = hck_base(lo), sb = base + (b0 << kLogK);
+  const int s0 = max(lo, sb), s1 = min(hi, sb + (nrows << kLogK));
+  for (int s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    const int e = ev[s];
+    if (e >= 0) atomicAdd(&hs[((s - sb) >> kLogK) * J + e], 1);
+  }
+  __syncthreads();
   for (int j = threadIdx.x; j < J; j += blockDim.x) {
-    int acc = seg[(size_t)s * J + j];
-    for (int r = r0; r < r1; ++r) {
-      const int v = hck[(size_t)r * J + j];
-      hck[(size_t)r * J + j] = acc;
+    int acc = seg[(size_t)sg * SJ + j];
+    for (int r = 0; r < nrows; ++r) {
+      const int v = hs[r * J + j];
+      hs[r * J + j] = acc;
       acc += v;
     }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrows * HJ; i += blockDim.x) {
+    const int r = i / HJ, j = i - r * HJ;
+    hck[(size_t)b0 * HJ + i] = j < J ? hs[r * J + j] : 0;
   }
 }
 
@@ -210,15 +246,15 @@ static __global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
     const int p = a.model.product[t];
     const int aold = a.cache[t];
     const int evt = a.ev[t];
-    const int b = (t - a.lo) >> kLogK;
-    const int* hb = a.hck + (size_t)b * J;
+    const int b = (t - hck_base(a.lo)) >> kLogK;
+    const int* hrow = a.hck + (size_t)b * hck_stride(J);
     int* xrow = a.xloc + (size_t)p * J;
     for (int j = lane; j < J; j += 32) {
-      crow[j] = a.ckcap[j] - hb[j] + D[j];
+      crow[j] = a.ckcap[j] - hrow[j] + D[j];
       prow[j] = xrow[j];
     }
     __syncwarp();
-    for (int s = a.lo + (b << kLogK) + lane; s < t; s += 32) {
+    for (int s = max(a.lo, hck_base(a.lo) + (b << kLogK)) + lane; s < t; s += 32) {
       const int e = a.ev[s];
       if (e >= 0) atomicSub(&crow[e], 1);
     }
