@@ -104,12 +104,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_workload(name: str):
+PARTITIONS = {
+    "product": "make_product_partition(M, seed 1) (the reference's partitioner)",
+    "chunk": "make_product_chunk_partition(M): each product's orders cut into contiguous chunks, one process each",
+}
+
+
+def make_workload(name: str, partition: str = "product"):
     import paper_2406_01939_b200 as P
     J, I, T, M, theta = WORKLOADS[name]
     inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
     pol = P.DualNetworkPolicy.seeded(inst, theta)
-    plan = P.make_product_partition(inst, M, 1)
+    if partition == "chunk":
+        plan = P.make_product_chunk_partition(inst, M, 1)
+    else:
+        plan = P.make_product_partition(inst, M, 1)
     return inst, pol, plan, dict(J=J, I=I, T=T, M=M, theta=theta)
 
 
@@ -150,7 +159,7 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    inst, pol, plan, w = make_workload(args.workload)
+    inst, pol, plan, w = make_workload(args.workload, args.partition)
     from oracle.oracle import REF
     steps = []
     for _ in range(args.warmup + args.steps):
@@ -162,7 +171,7 @@ def run_reference_arm(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * w["T"] / value, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, **w, "policy": "dual MLP seeded", "partition": "product"},
+            "config": {"workload": args.workload, **w, "policy": "dual MLP seeded", "partition": args.partition},
             "cpu_baseline": {**timed[-1], "value": value},
             "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "reference has no GPU path; the serial CPU path is the reference's fastest way to the "
@@ -180,6 +189,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--partition", default="product", choices=sorted(PARTITIONS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -196,7 +206,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2406_01939_b200 as P
-    inst, pol, plan, w = make_workload(args.workload)
+    inst, pol, plan, w = make_workload(args.workload, args.partition)
     T = w["T"]
     cfg = P.PicardConfig(max_steps=300 * w["M"])
     sim = P.Simulator(inst, pol, device=local)
@@ -301,7 +311,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": args.workload, **w, "policy": "dual MLP {2J+1,64,64,2J} seeded",
-                           "partition": "product", "max_steps": 300 * w["M"],
+                           "partition": PARTITIONS[args.partition], "max_steps": 300 * w["M"],
                            "l2": "512 MiB flush before every step; working set > L2",
                            "parallelism": f"processes sharded over {world} GPU(s)"},
                 "iterations": res.iterations_to_converged,

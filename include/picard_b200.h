@@ -68,10 +68,12 @@ enum {
 
 /* Sweep engine selection for pcd_simulate / pcd_iterate_once. */
 enum {
-  PCD_ENGINE_AUTO = 0,          /* closed form when the plan is a product partition;
+  PCD_ENGINE_AUTO = 0,          /* closed form when the plan is a run partition;
                                    tensor-core policy when eligible               */
   PCD_ENGINE_REPLAY = 1,        /* exact per-process window replay (any plan)     */
-  PCD_ENGINE_PRODUCT = 2,       /* closed-form product-partition sweep (checked)  */
+  PCD_ENGINE_PRODUCT = 2,       /* closed-form run-partition sweep (checked): each
+                                   process owns one contiguous stretch of a
+                                   product's orders, or only whole products      */
   PCD_ENGINE_PRODUCT_FP64 = 3   /* ... with the FP64 SIMT policy only             */
 };
 
@@ -197,6 +199,14 @@ int pcd_generate_instance(int32_t nodes, int32_t products, int64_t horizon,
 /* make_product_partition (instance.cpp:142-186): owner[T]. */
 int pcd_product_partition(const pcd_instance* inst, int32_t processes,
                           uint64_t seed, int32_t* owner);
+/* Product-chunk partition (no reference counterpart; any PartitionPlan is
+ * valid input to picard_simulate, engine.hpp:74-96): each product's orders
+ * in time order are cut into contiguous chunks of near-equal length L, one
+ * process per chunk, L the smallest length with at most `processes` chunks.
+ * Falls back to pcd_product_partition(seed) when processes < ordered
+ * products. A run partition, so PCD_ENGINE_PRODUCT applies. owner[T]. */
+int pcd_product_chunk_partition(const pcd_instance* inst, int32_t processes,
+                                uint64_t seed, int32_t* owner);
 /* make_uniform_time_partition (engine.hpp:99-114): owner[T]. */
 int pcd_uniform_partition(int64_t horizon, int32_t processes, uint64_t seed,
                           int32_t* owner);

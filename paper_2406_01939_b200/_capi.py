@@ -72,6 +72,7 @@ SIGNATURES = {
     "pcd_generate_instance": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_double,
                                         C.c_uint64, C.c_int32, I32P, I32P, F64P, I32P, I32P]),
     "pcd_product_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),
+    "pcd_product_chunk_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),
     "pcd_uniform_partition": (C.c_int, [C.c_int64, C.c_int32, C.c_uint64, I32P]),
     "pcd_seeded_mlp": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_int32,
                                  F64P, F64P, F64P, F64P, F64P, F64P]),

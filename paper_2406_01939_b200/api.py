@@ -8,6 +8,7 @@ reference (file:line)                  here
 fo::Instance (instance.hpp:25-37)      :class:`Instance`
 fo::generate_instance (instance.cpp:80) :func:`generate_instance`
 fo::make_product_partition (:142-186)  :func:`make_product_partition`
+(ours, no reference counterpart)       :func:`make_product_chunk_partition`
 make_uniform_time_partition (engine.hpp:99-114) :func:`make_uniform_time_partition`
 PartitionPlan (engine.hpp:74-96)       :class:`PartitionPlan`
 PicardConfig (engine.hpp:120-126)      :class:`PicardConfig`
@@ -207,6 +208,18 @@ def make_product_partition(instance: Instance, processes: int, seed: int) -> Par
     owner = np.zeros(max(int(instance.horizon), 1), np.int32)
     c = instance.to_c()
     _check(LIB.pcd_product_partition(C.byref(c), int(processes), int(seed) & (2**64 - 1), _ptr(owner)))
+    return PartitionPlan(int(processes), owner[:int(instance.horizon)])
+
+
+def make_product_chunk_partition(instance: Instance, processes: int, seed: int = 1) -> PartitionPlan:
+    """Product chunks (ours, ``pcd_product_chunk_partition``): each product's
+    orders cut into contiguous near-equal chunks, one process per chunk, so
+    up to ``processes`` processes carry work (a product partition activates
+    at most I). Falls back to :func:`make_product_partition` when
+    ``processes`` is below the number of ordered products."""
+    owner = np.zeros(max(int(instance.horizon), 1), np.int32)
+    c = instance.to_c()
+    _check(LIB.pcd_product_chunk_partition(C.byref(c), int(processes), int(seed) & (2**64 - 1), _ptr(owner)))
     return PartitionPlan(int(processes), owner[:int(instance.horizon)])
 
 

@@ -84,6 +84,17 @@ int pcd_product_partition(const pcd_instance* inst, int32_t processes, uint64_t 
   PCD_CATCH
 }
 
+int pcd_product_chunk_partition(const pcd_instance* inst, int32_t processes, uint64_t seed, int32_t* owner) {
+  PCD_TRY
+  if (!inst || !owner) throw pcd::InvalidArgument("null argument");
+  for (int64_t t = 0; t < inst->horizon; ++t)
+    if (inst->product[t] < 0 || inst->product[t] >= inst->products)
+      throw pcd::InvalidArgument("order product out of range");
+  pcd::product_chunk_partition(inst->product, inst->horizon, inst->products, processes, seed, owner);
+  return PCD_OK;
+  PCD_CATCH
+}
+
 int pcd_uniform_partition(int64_t horizon, int32_t processes, uint64_t seed, int32_t* owner) {
   PCD_TRY
   if (horizon > 0 && !owner) throw pcd::InvalidArgument("null argument");

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <cuda_fp16.h>
 
@@ -111,8 +112,13 @@ struct pcd_handle {
   bool have_plan = false, is_product = false;
   std::vector<int32_t> h_owner;
   pcd::DBuf<int> owner, pstart, pslots, qstart, qslots;
+  pcd::DBuf<int> rid;     // run of every slot (run partitions)
+  int64_t runs = 0;       // R
+  // per-iteration work list of the tensor-core sweep (window load desc)
+  pcd::DBuf<int> wload, wids, wload_s, wq, wctl;  // wctl = {nq, head}
+  pcd::DBuf<unsigned char> wtmp;
   // dynamic state
-  pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, scratch;
+  pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, scratch, tau;
   pcd::DBuf<unsigned char> written;
   pcd::DBuf<long long> evals;
   pcd::Scalars* scal = nullptr;  // device
@@ -126,7 +132,6 @@ struct pcd_handle {
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   pcd::DBuf<unsigned char> tc_wimg;
   pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf;
-  pcd::DBuf<int> tc_rows;
   pcd::DBuf<unsigned long long> tc_stats;
   int32_t tc_tiles = 0;
   int64_t max_load = 0;
@@ -249,7 +254,7 @@ static void launch_product_sweep(pcd_handle* h, int lo, int hi, long long* evals
   a.model = h->model();
   a.M = h->M; a.J = h->J; a.lo = lo; a.hi = hi;
   a.pstart = h->pstart.p; a.pslots = h->pslots.p;
-  a.ckcap = h->ckcap.p; a.hck = h->hck.p; a.ev = h->ev.p; a.xloc = h->xloc.p;
+  a.ckcap = h->ckcap.p; a.hck = h->hck.p; a.ev = h->ev.p; a.xloc = h->xloc.p; a.rid = h->rid.p;
   a.cache = h->cache.p; a.written = h->written.p; a.ref = h->ref.n ? h->ref.p : nullptr;
   a.scal = h->scal; a.evals_out = evals_out;
   a.mine = h->comm ? h->d_mine.p : nullptr;
@@ -320,10 +325,30 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   s.model = h->model();
   s.M = h->M; s.J = h->J; s.lo = lo; s.hi = hi;
   s.pstart = h->pstart.p; s.pslots = h->pslots.p;
-  s.ckcap = h->ckcap.p; s.hck = h->hck.p; s.ev = h->ev.p; s.xloc = h->xloc.p;
+  s.ckcap = h->ckcap.p; s.hck = h->hck.p; s.ev = h->ev.p; s.xloc = h->xloc.p; s.rid = h->rid.p;
   s.cache = h->cache.p; s.written = h->written.p; s.ref = h->ref.n ? h->ref.p : nullptr;
   s.scal = h->scal; s.evals_out = evals_out;
-  a.rows = h->tc_rows.p; a.wimg = h->tc_wimg.p;
+  // work list: this rank's processes with window slots, heaviest first; the
+  // first tiles*128 entries are dealt round robin over the tiles, the rest
+  // are pulled by rows as they finish (wctl[1] = next entry)
+  {
+    const int M = h->M;
+    h->wload.alloc(M); h->wids.alloc(M); h->wload_s.alloc(M); h->wq.alloc(M); h->wctl.alloc(2);
+    CK(cudaMemsetAsync(h->wctl.p, 0, 2 * sizeof(int), h->stream));
+    k_window_load<<<(M + 255) / 256, 256, 0, h->stream>>>(h->pstart.p, h->pslots.p, M, lo, hi,
+                                                          h->comm ? h->d_mine.p : nullptr, h->wload.p, h->wids.p,
+                                                          h->wctl.p);
+    int bits = 1;
+    while ((1LL << bits) <= (long long)h->max_load) ++bits;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
+                                                 bits, h->stream));
+    h->wtmp.alloc(tb);
+    CK(cub::DeviceRadixSort::SortPairsDescending(h->wtmp.p, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
+                                                 bits, h->stream));
+    h->timing.kernel_launches += 2;
+  }
+  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p;
   a.guard = (float)(guard > 0 ? guard : 5e-5);
@@ -339,7 +364,10 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     CK(cudaMemsetAsync(dprof.p, 0, 20 * sizeof(long long), h->stream));
     a.prof = dprof.p;
   }
-  launch_tc_sweep(a, h->tc_tiles, h->stream);
+  // PCD_TC_TILES=n (tests): fewer CTAs than SMs, so rows pull from the work list
+  int tiles = h->tc_tiles;
+  if (const char* e = getenv("PCD_TC_TILES")) tiles = std::max(1, std::min(tiles, atoi(e)));
+  launch_tc_sweep(a, tiles, h->stream);
   CK(cudaGetLastError());
   if (prof) {
     long long v[20];
@@ -361,9 +389,10 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   if (engine == PCD_ENGINE_PRODUCT || engine == PCD_ENGINE_PRODUCT_FP64) {
     tm.start();
     const int J = h->J;
-    const int tpb = std::max(1, std::min(128, (int)((40 * 1024) / (4 * std::max(1, J)))));
-    k_effective<<<(h->I + tpb - 1) / tpb, tpb, (size_t)tpb * J * 4, h->stream>>>(
-        h->qstart.p, h->qslots.p, h->I, lo, hi, h->cache.p, h->ckinv.p, J, h->ev.p);
+    const int wpb = 8;  // warps (products) per block
+    const int pgrid = (h->I + wpb - 1) / wpb;
+    k_effective<<<pgrid, wpb * 32, (size_t)wpb * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi,
+                                                                     h->cache.p, h->ckinv.p, J, h->ev.p);
     const int nb = hck_rows(lo, hi);
     const int nseg = (nb + kSegRows - 1) / kSegRows;
     const size_t hsm = (size_t)kSegRows * J * 4;
@@ -375,10 +404,12 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     k_seg_count<<<nseg, 256, (size_t)J * 4, h->stream>>>(h->ev.p, lo, hi, J, h->seg.p);
     k_seg_scan<<<J, 256, 0, h->stream>>>(h->seg.p, nseg, J);
     k_hist_prefix<<<nseg, 256, hsm, h->stream>>>(h->ev.p, lo, hi, J, nb, h->seg.p, h->hck.p);
-    CK(cudaMemcpyAsync(h->xloc.p, h->ckinv.p, sizeof(int) * (size_t)h->I * J, cudaMemcpyDeviceToDevice, h->stream));
+    k_tau<<<(J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
+    k_xinit<<<pgrid, wpb * 32, (size_t)wpb * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
+                                                                 h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
     CK(cudaGetLastError());
     h->timing.prep_ms += tm.stop_ms();
-    h->timing.kernel_launches += 4;
+    h->timing.kernel_launches += 6;
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {
@@ -465,7 +496,7 @@ static int choose_engine(pcd_handle* h, int requested) {
   if (requested == PCD_ENGINE_REPLAY) return PCD_ENGINE_REPLAY;
   if (requested == PCD_ENGINE_PRODUCT || requested == PCD_ENGINE_PRODUCT_FP64) {
     if (!h->is_product)
-      throw InvalidArgument("engine=PRODUCT requires a product partition (each product on one process)");
+      throw InvalidArgument("engine=PRODUCT requires a run partition (each process owns one contiguous stretch of a product's orders, or whole products)");
     return requested;
   }
   return h->is_product ? PCD_ENGINE_PRODUCT : PCD_ENGINE_REPLAY;
@@ -481,7 +512,8 @@ static void ensure_state_buffers(pcd_handle* h) {
   h->ckcap.alloc(std::max(1, h->J));
   h->ckinv.alloc(IJ);
   h->ckbak.alloc(IJ + h->J);
-  h->xloc.alloc(IJ);
+  h->xloc.alloc(std::max<size_t>(1, (size_t)h->runs * std::max(1, h->J)));
+  h->tau.alloc(std::max(1, h->J));
   const size_t nb = (T + kK - 1) / kK + 1;  // + 1: blocks start at lo & ~(K-1)
   h->hck.alloc(nb * hck_stride(std::max(1, h->J)));
   h->seg.alloc(((nb + kSegRows - 1) / kSegRows + 1) * seg_stride(std::max(1, h->J)));
@@ -646,24 +678,15 @@ static void rebuild_shards(pcd_handle* h) {
     h->d_recv.alloc((size_t)std::max(1, h->maxn) * h->nranks);
     h->d_red.alloc(8);
   }
-  // tensor-core tiles: this rank's non-empty processes, heaviest first. The
-  // per-row CUDA-core work (features, epilogues) dominates a step, so spread
-  // the processes over every SM (one CTA each, <= 128 rows), round robin in
-  // load order so all tiles carry the same critical path.
-  std::vector<int32_t> procs;
+  // tensor-core sweep: one CTA per SM; rows pull this rank's processes from
+  // the per-iteration work list (launch_tc), so only the largest load (for
+  // the sort key width) is kept here
+  h->max_load = 0;
   for (int32_t m = 0; m < M; ++m)
-    if (load[(size_t)m] > 0 && h->rank_of[(size_t)m] == h->rank) procs.push_back(m);
-  std::stable_sort(procs.begin(), procs.end(),
-                   [&](int32_t a, int32_t b) { return load[(size_t)a] > load[(size_t)b]; });
-  h->max_load = procs.empty() ? 0 : load[(size_t)procs[0]];
+    if (h->rank_of[(size_t)m] == h->rank) h->max_load = std::max(h->max_load, load[(size_t)m]);
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-  const int64_t n = (int64_t)procs.size();
-  h->tc_tiles = (int32_t)std::max<int64_t>((n + kTcRows - 1) / kTcRows, std::min<int64_t>(nsm, n));
-  std::vector<int32_t> rows((size_t)std::max(1, h->tc_tiles) * kTcRows, -1);
-  for (int64_t k = 0; k < n; ++k)
-    rows[(size_t)(k % h->tc_tiles) * kTcRows + (size_t)(k / h->tc_tiles)] = procs[(size_t)k];
-  h->tc_rows.upload(rows.data(), rows.size(), h->stream);
+  h->tc_tiles = nsm;
   CK(cudaStreamSynchronize(h->stream));
 }
 
@@ -831,16 +854,35 @@ extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
   h->owner.upload(owner, (size_t)h->T, h->stream);
   build_csr(h, h->owner.p, M, h->pstart, h->pslots);
   build_csr(h, h->product.p, h->I, h->qstart, h->qslots);
-  int* flag;
-  CK(cudaMalloc(&flag, sizeof(int)));
-  CK(cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
-  if (h->T > 0)
-    k_check_product_partition<<<grid_for(h->T, 256), 256, 0, h->stream>>>(h->owner.p, h->product.p, h->qstart.p,
-                                                                        h->qslots.p, h->T, flag);
+  // runs along the product slot lists (kernels.cuh: k_run_starts / k_run_ids /
+  // k_check_runs): the closed-form engines need a run partition
+  h->rid.alloc((size_t)std::max<int64_t>(h->T, 1));
   int hf = 0;
-  CK(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  cudaFree(flag);
+  h->runs = 0;
+  if (h->T > 0) {
+    DBuf<int> flagk, incl, nruns, nonlead, flag;
+    flagk.alloc(h->T); incl.alloc(h->T); nruns.alloc(M); nonlead.alloc(M); flag.alloc(1);
+    CK(cudaMemsetAsync(nruns.p, 0, sizeof(int) * (size_t)M, h->stream));
+    CK(cudaMemsetAsync(nonlead.p, 0, sizeof(int) * (size_t)M, h->stream));
+    CK(cudaMemsetAsync(flag.p, 0, sizeof(int), h->stream));
+    k_run_starts<<<grid_for(h->T, 256), 256, 0, h->stream>>>(h->qslots.p, h->product.p, h->owner.p, h->T, flagk.p);
+    size_t tb = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flagk.p, incl.p, (int)h->T, h->stream));
+    DBuf<unsigned char> tmp;
+    tmp.alloc(tb);
+    CK(cub::DeviceScan::InclusiveSum(tmp.p, tb, flagk.p, incl.p, (int)h->T, h->stream));
+    k_run_ids<<<grid_for(h->T, 256), 256, 0, h->stream>>>(h->qslots.p, h->qstart.p, h->product.p, h->owner.p,
+                                                          flagk.p, incl.p, h->T, h->rid.p, nruns.p, nonlead.p);
+    k_check_runs<<<(M + 255) / 256, 256, 0, h->stream>>>(nruns.p, nonlead.p, M, flag.p);
+    CK(cudaGetLastError());
+    int nr = 0;
+    CK(cudaMemcpyAsync(&nr, incl.p + h->T - 1, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->runs = nr;
+    // xloc is R x J int32: refuse the closed form for pathological plans
+    if ((double)nr * h->J * 4 > 8e9) hf = 1;
+  }
   h->is_product = hf == 0;
   h->have_plan = true;
   ensure_state_buffers(h);

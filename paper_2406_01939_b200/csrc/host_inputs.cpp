@@ -200,6 +200,50 @@ void product_partition(const int32_t* product, int64_t T, int32_t I, int32_t M, 
   for (int64_t t = 0; t < T; ++t) owner[t] = group_of[(size_t)product[t]];
 }
 
+// Product-chunk partition (ours; no reference counterpart): every product's
+// orders, in time order, are cut into k_i = ceil(Q_i / L) contiguous chunks of
+// near-equal size, one process per chunk, with L the smallest chunk length for
+// which sum_i k_i <= M. A run partition (engine.cu: k_check_runs), so the
+// closed-form engines apply; with M >= I it spreads the window over up to M
+// processes instead of I. Falls back to make_product_partition when M is
+// below the number of ordered products.
+void product_chunk_partition(const int32_t* product, int64_t T, int32_t I, int32_t M, uint64_t seed,
+                             int32_t* owner) {
+  if (M < 1) throw InvalidArgument("process count must be >= 1");
+  std::vector<int64_t> counts((size_t)I, 0);
+  for (int64_t t = 0; t < T; ++t) counts[(size_t)product[t]] += 1;
+  int64_t used = 0, qmax = 0;
+  for (int64_t q : counts) {
+    used += q > 0;
+    qmax = std::max(qmax, q);
+  }
+  if (used > M || T == 0) return product_partition(product, T, I, M, seed, owner);
+  auto chunks = [&](int64_t L) {
+    int64_t k = 0;
+    for (int64_t q : counts) k += (q + L - 1) / L;
+    return k;
+  };
+  int64_t lo = 1, hi = qmax;  // chunks(qmax) = used <= M
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (chunks(mid) <= M) hi = mid; else lo = mid + 1;
+  }
+  const int64_t L = lo;
+  std::vector<int32_t> first((size_t)I, 0);  // first process of each product
+  std::vector<int64_t> seen((size_t)I, 0);
+  int32_t next = 0;
+  for (int32_t i = 0; i < I; ++i) {
+    first[(size_t)i] = next;
+    next += (int32_t)((counts[(size_t)i] + L - 1) / L);
+  }
+  for (int64_t t = 0; t < T; ++t) {
+    const int32_t i = product[t];
+    const int64_t q = counts[(size_t)i], k = (q + L - 1) / L, c = seen[(size_t)i]++;
+    // chunk c' holds ranks [floor(c' q / k), floor((c'+1) q / k))
+    owner[t] = first[(size_t)i] + (int32_t)(((c + 1) * k - 1) / q);
+  }
+}
+
 void uniform_partition(int64_t T, int32_t M, uint64_t seed, int32_t* owner) {
   if (M < 1) throw ContractViolation("uniform partition: process count must be >= 1");
   Engine gen(seed);

@@ -10,7 +10,9 @@
 //   cache[T], fresh[T], ref[T]            int32   ActionCache / fresh / oracle
 //   written[T]                            uint8   "slot written before" (conflicts)
 //   ckcap[J], ckinv[I*J]                  int32   checkpoint FoState (dense)
-//   xloc[I*J]                             int32   per-iteration own-product inventory
+//   rid[T]                                int32   run of each slot (run = one process's stretch
+//                                                 of one product's slot list)
+//   xloc[R*J]                             int32   per-iteration inventory of every run
 //   ev[T]                                 int32   effective cached attempt (node or -1)
 //   hck[nb*HJ]                            int32   hck[b][j] = H(b)[j] = effective attempts at
 //                                                 node j in [lo, base + 8b), base = lo & ~7
@@ -63,34 +65,190 @@ __device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
 }
 
 // ---------------------------------------------------------------------------
-// Effective-attempt pass (product-partition closed form).
+// Effective-attempt pass (run-partition closed form).
 // For every product, walk its slots of the window in time order; the cached
 // attempt at slot t (node a) is *effective* iff fewer than ckinv[p][a]
 // earlier cached attempts of the same (product, node) exist in the window —
 // i.e. it would succeed inventory-wise with unlimited capacity.
+// One warp per product, 32 slots per round: the rank of an attempt among the
+// equal (product, node) attempts of the round comes from __match_any_sync,
+// the running per-node counts live in the warp's smem row.
 // ---------------------------------------------------------------------------
-static __global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
-                            int lo, int hi, const int* __restrict__ cache,
-                            const int* __restrict__ ckinv, int J, int* __restrict__ ev) {
-  extern __shared__ int cnt_smem[];
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= I) return;
-  int* cnt = cnt_smem + threadIdx.x * J;
-  for (int j = 0; j < J; ++j) cnt[j] = 0;
+__device__ __forceinline__ void product_window(const int* __restrict__ qstart, const int* __restrict__ qslots, int p,
+                                               int lo, int hi, const int*& sl, int& k0, int& k1) {
   const int beg = qstart[p], n = qstart[p + 1] - beg;
-  const int* sl = qslots + beg;
+  sl = qslots + beg;
+  k0 = lower_bound_i32(sl, n, lo);
+  k1 = k0 + lower_bound_i32(sl + k0, n - k0, hi);
+}
+
+static __global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
+                                   int lo, int hi, const int* __restrict__ cache,
+                                   const int* __restrict__ ckinv, int J, int* __restrict__ ev) {
+  extern __shared__ int cnt_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (p >= I) return;  // warp-uniform
+  int* cnt = cnt_smem + warp * J;
+  for (int j = lane; j < J; j += 32) cnt[j] = 0;
+  const int* sl;
+  int k0, k1;
+  product_window(qstart, qslots, p, lo, hi, sl, k0, k1);
   const int* x0 = ckinv + (size_t)p * J;
-  for (int k = lower_bound_i32(sl, n, lo); k < n; ++k) {
-    const int t = sl[k];
-    if (t >= hi) break;
-    const int a = cache[t];
-    int e = -1;
-    if (a >= 0 && a < J) {
-      e = cnt[a] < x0[a] ? a : -1;
-      cnt[a] += 1;
-    }
-    ev[t] = e;
+  const unsigned lt = (1u << lane) - 1u;
+  __syncwarp();
+  for (int b = k0; b < k1; b += 32) {
+    const int k = b + lane;
+    const bool valid = k < k1;
+    const int t = valid ? sl[k] : 0;
+    const int a = valid ? cache[t] : -1;
+    const bool att = valid && a >= 0 && a < J;
+    const unsigned peers = __match_any_sync(0xffffffffu, att ? a : -1);
+    const int rank = __popc(peers & lt);
+    const int c = att ? cnt[a] : 0;
+    const int e = att && c + rank < x0[a] ? a : -1;
+    if (valid) ev[t] = e;
+    __syncwarp();
+    if (att && rank == 0) cnt[a] = c + __popc(peers);
+    __syncwarp();
   }
+}
+
+// Death slot of every node under the frozen cache: tau[j] = the slot of the
+// effective attempt at node j whose index (in window order) is ckcap[j] —
+// the first one that finds the node empty when the cache is replayed from
+// the checkpoint; INT_MAX when the node never empties in the window.
+static __global__ void k_tau(const int* __restrict__ hck, const int* __restrict__ ev, const int* __restrict__ ckcap,
+                             int lo, int hi, int J, int nb, int* __restrict__ tau) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  const int HJ = hck_stride(J), c = ckcap[j], base = hck_base(lo);
+  // last checkpoint row with H <= c (row 0 holds 0)
+  int l = 0, r = nb - 1;
+  while (l < r) {
+    const int mid = (l + r + 1) >> 1;
+    if (hck[(size_t)mid * HJ + j] <= c) l = mid; else r = mid - 1;
+  }
+  int h = hck[(size_t)l * HJ + j], out = 0x7fffffff;
+  const int s1 = min(hi, base + ((l + 1) << kLogK));
+  for (int s = max(lo, base + (l << kLogK)); s < s1; ++s) {
+    if (ev[s] != j) continue;
+    if (h == c) { out = s; break; }
+    ++h;
+  }
+  tau[j] = out;
+}
+
+// Inventory of every run at its first slot in the window (run partitions:
+// each (process, product) pair owns one contiguous stretch of the product's
+// slot list). Before its first own slot a process holds the replay state of
+// the frozen cache, so
+//   xloc[run][j] = ckinv[p][j] - #{effective cached attempts (p, j) in
+//                                  [lo, first slot) that precede tau[j]}.
+// One warp per product walks the window slots in time order with per-node
+// counts in smem and writes a row at every run start.
+static __global__ void k_xinit(const int* __restrict__ qstart, const int* __restrict__ qslots, int I, int lo,
+                               int hi, const int* __restrict__ ev, const int* __restrict__ rid,
+                               const int* __restrict__ tau, const int* __restrict__ ckinv, int J,
+                               int* __restrict__ xloc) {
+  extern __shared__ int cnt_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (p >= I) return;  // warp-uniform
+  int* cnt = cnt_smem + warp * J;
+  for (int j = lane; j < J; j += 32) cnt[j] = 0;
+  const int* sl;
+  int k0, k1;
+  product_window(qstart, qslots, p, lo, hi, sl, k0, k1);
+  const int* x0 = ckinv + (size_t)p * J;
+  int prev_run = -1;
+  __syncwarp();
+  for (int b = k0; b < k1; b += 32) {
+    const int k = b + lane;
+    const bool valid = k < k1;
+    const int t = valid ? sl[k] : 0;
+    const int e = valid ? ev[t] : -1;
+    const int r = valid ? rid[t] : -1;
+    const bool contrib = e >= 0 && t < tau[e];
+    int pr = __shfl_up_sync(0xffffffffu, r, 1);
+    if (lane == 0) pr = prev_run;
+    unsigned starts = __ballot_sync(0xffffffffu, valid && r != pr);
+    int done = 0;
+    while (starts) {
+      const int L = __ffs(starts) - 1;
+      starts &= starts - 1;
+      if (contrib && lane >= done && lane < L) atomicAdd(&cnt[e], 1);
+      __syncwarp();
+      const int rr = __shfl_sync(0xffffffffu, r, L);
+      int* xr = xloc + (size_t)rr * J;
+      for (int j = lane; j < J; j += 32) xr[j] = x0[j] - cnt[j];
+      __syncwarp();
+      done = L;
+    }
+    if (contrib && lane >= done) atomicAdd(&cnt[e], 1);
+    prev_run = __shfl_sync(0xffffffffu, r, 31);
+    __syncwarp();
+  }
+}
+
+// Run structure of a plan along the product slot lists (qslots, time order
+// per product): run_start[k] = 1 where a product's list starts or the owner
+// changes.
+static __global__ void k_run_starts(const int* __restrict__ qslots, const int* __restrict__ product,
+                                    const int* __restrict__ owner, long long T, int* __restrict__ flag) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < T; k += (long long)gridDim.x * blockDim.x) {
+    const int t = qslots[k];
+    int st = 1;
+    if (k > 0) {
+      const int tp = qslots[k - 1];
+      st = product[tp] != product[t] || owner[tp] != owner[t];
+    }
+    flag[k] = st;
+  }
+}
+// rid[t] = run of slot t; per process the number of runs and whether any of
+// them is non-leading (does not start at its product's first slot).
+static __global__ void k_run_ids(const int* __restrict__ qslots, const int* __restrict__ qstart,
+                                 const int* __restrict__ product, const int* __restrict__ owner,
+                                 const int* __restrict__ flag, const int* __restrict__ incl, long long T,
+                                 int* __restrict__ rid, int* __restrict__ nruns, int* __restrict__ nonlead) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < T; k += (long long)gridDim.x * blockDim.x) {
+    const int t = qslots[k];
+    rid[t] = incl[k] - 1;
+    if (flag[k]) {
+      const int m = owner[t];
+      atomicAdd(&nruns[m], 1);
+      if (k != qstart[product[t]]) atomicOr(&nonlead[m], 1);
+    }
+  }
+}
+// The closed form needs every process to hold the replay state of the frozen
+// cache before each of its runs: true when the process owns a single run, or
+// only leading runs (no other process touches those products earlier).
+static __global__ void k_check_runs(const int* __restrict__ nruns, const int* __restrict__ nonlead, int M,
+                                    int* flag) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int bad = m < M && nruns[m] > 1 && nonlead[m];
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// Work list of one iteration: window load of every process of this rank
+// (owned slots in [lo, hi)); the engine sorts (load desc) so the rows of the
+// tensor-core sweep pull the longest processes first.
+static __global__ void k_window_load(const int* __restrict__ pstart, const int* __restrict__ pslots, int M, int lo,
+                                     int hi, const unsigned char* __restrict__ mine, int* __restrict__ load,
+                                     int* __restrict__ ids, int* __restrict__ nq) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  int n = 0;
+  if (!mine || mine[m]) {
+    const int beg = pstart[m], c = pstart[m + 1] - beg;
+    const int k0 = lower_bound_i32(pslots + beg, c, lo);
+    n = k0 < c && pslots[beg + k0] < hi ? lower_bound_i32(pslots + beg, c, hi) - k0 : 0;
+  }
+  load[m] = n;
+  ids[m] = m;
+  if (n) atomicAdd(nq, 1);
 }
 
 // Prefix counts of effective attempts, reduce-then-scan over segments of
@@ -178,6 +336,7 @@ struct SweepArgs {
   const int* hck;
   const int* ev;
   int* xloc;
+  const int* rid;
   int* cache;
   unsigned char* written;
   const int* ref;
@@ -209,11 +368,12 @@ __host__ __device__ inline size_t warp_smem_bytes(int J, int in, int H, int out)
 }
 
 // ---------------------------------------------------------------------------
-// Closed-form sweep for product partitions (every product's slots belong to a
-// single process). One warp per process walks ONLY its own slots of the
-// window; the local state at own slot t is
+// Closed-form sweep for run partitions (product partitions, and product
+// chunks: every process's slots of a product form one contiguous stretch of
+// the product's slot list, k_check_runs). One warp per process walks ONLY its
+// own slots of the window; the local state at own slot t (run r, product p) is
 //   c[j] = max(0, ckcap[j] - H_t[j] + Hown_t[j] - F_t[j])
-//   x[p][j] = ckinv[p][j] - F_t[p][j]          (own product p)
+//   x[p][j] = xloc[r][j] - F_t[p][j]           (xloc from k_xinit)
 // where H_t = effective cached attempts in [lo,t) (hck + partial block scan),
 // Hown_t the effective attempts at own slots before t and F_t the process's
 // own fresh fulfilments before t. This equals the state the reference's
@@ -243,12 +403,11 @@ static __global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
   for (; k < n; ++k) {
     const int t = sl[k];
     if (t >= a.hi) break;
-    const int p = a.model.product[t];
     const int aold = a.cache[t];
     const int evt = a.ev[t];
     const int b = (t - hck_base(a.lo)) >> kLogK;
     const int* hrow = a.hck + (size_t)b * hck_stride(J);
-    int* xrow = a.xloc + (size_t)p * J;
+    int* xrow = a.xloc + (size_t)a.rid[t] * J;
     for (int j = lane; j < J; j += 32) {
       crow[j] = a.ckcap[j] - hrow[j] + D[j];
       prow[j] = xrow[j];
@@ -485,18 +644,6 @@ static __global__ void k_window_evals(const int* __restrict__ pstart, const int*
   if (m >= M) return;
   const int beg = pstart[m], n = pstart[m + 1] - beg;
   out[m] = lower_bound_i32(pslots + beg, n, hi) - lower_bound_i32(pslots + beg, n, lo);
-}
-
-// Product-partition test: every slot's owner equals its product's first owner.
-static __global__ void k_check_product_partition(const int* __restrict__ owner, const int* __restrict__ product,
-                                          const int* __restrict__ qstart, const int* __restrict__ qslots,
-                                          long long T, int* flag) {
-  int bad = 0;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
-    const int p = product[t];
-    bad |= owner[t] != owner[qslots[qstart[p]]];
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
 static __global__ void k_iota(int* p, long long n) {

@@ -1,5 +1,11 @@
 // tc_sweep.cu — the tcgen05 product-partition sweep (see tc_sweep.cuh).
 //
+// Work distribution: one CTA per SM, 128 rows (processes in flight). The
+// engine sorts the processes with window slots by load (desc) into wq; entry
+// k < tiles*128 starts on row k / tiles of tile k % tiles, and a row whose
+// process is done pulls the next entry (atomic counter), so every row works
+// until the list is drained (list scheduling, longest first).
+//
 // Thread mapping: thread (warp w, lane l) owns row r = 32*(w%4) + l — the
 // TMEM lane it may access — and column group g = w/4 (nodes [32g, 32g+32)).
 // Warps 12..15 (group 3, at most one 8-node chunk) are also the row agents:
@@ -44,7 +50,7 @@ constexpr int kGroups = kTcWarps / 4;      // column groups (warps w, w+4, ... s
 constexpr int kTcBlock = kTcWarps * 32;
 constexpr int kGC = 32;                    // nodes per column group
 constexpr int kGChunks = kGC / 8;          // 8-node chunks per group
-constexpr int kInfo = 24;                  // ints of per-row state
+constexpr int kInfo = 28;                  // ints of per-row state
 constexpr int kMaxJ = 103;                 // 2J+1 <= 208
 constexpr int kScrJ = 112;
 constexpr uint32_t kTmemCols = 512;
@@ -67,9 +73,13 @@ enum {
   RI_XUPD,    // node whose own inventory dropped in the last step (-1): F += 1
   RI_OT,      // Order::t of the current step
   RI_EVT,     // effective cached attempt at the last step's slot (-1): Hown += 1
+  RI_X,       // run of the current step (row of xloc)
+  RI_M,       // process of the row (-1 idle)
+  RI_DRESET,  // a new process started: D = 0
   // operands of this step's update, loaded by the row agent at the step start
-  RI_UEV, RI_UOLD, RI_UWR, RI_UREF, RI_UPN, RI_URRN, RI_UOTN, RI_UTNN
+  RI_UEV, RI_UOLD, RI_UWR, RI_UREF, RI_UPN, RI_URRN, RI_UOTN, RI_UTNN, RI_UXN
 };
+static_assert(RI_UXN < kInfo, "per-row state fits");
 // per-row counters of the launch (sCnt[k * 128 + r], row agents)
 enum { CN_CHANGED = 0, CN_CONFLICTS, CN_FIRST, CN_MISM, CN_NEV, CN_TC, CN_COUNT };
 // sCtl: [0] active rows, [1] flagged rows, [2..130) flagged list, recheck statistics
@@ -293,29 +303,41 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
     sB2[i] = a.b2f[i];
   }
   for (int i = tid; i < kTcN3; i += kTcBlock) sB3[i] = a.b3f[i];
-  if (agent) {
-    const int m = a.rows[tile * kTcRows + r];
+  const int nq = a.wctl[0], dealt = (int)gridDim.x * kTcRows;
+  // row agent: bind process m (>= 0) or go idle (m < 0)
+  auto begin_proc = [&](int* inf, int m) {
     int pos = 0, end = 0;
     if (m >= 0) {
       const int beg = S.pstart[m], n = S.pstart[m + 1] - beg;
       pos = beg + lower_bound_i32(S.pslots + beg, n, lo);
       end = beg + lower_bound_i32(S.pslots + beg, n, hi);
     }
-    int* inf = sInfo + r * kInfo;
+    inf[RI_M] = m;
     inf[RI_POS] = pos;
     inf[RI_END] = end;
     inf[RI_XDIRTY] = 1;
     inf[RI_XUPD] = -1;
     inf[RI_EVT] = -1;
+    inf[RI_DRESET] = 1;
     inf[RI_P] = -1;
+    inf[RI_X] = -1;
     if (pos < end) {
       const int t = S.pslots[pos];
       inf[RI_T] = t;
       inf[RI_P] = S.model.product[t];
+      inf[RI_X] = S.rid[t];
       inf[RI_RR] = S.model.rrow[t];
       inf[RI_OT] = S.model.order_t ? S.model.order_t[t] : t;
       inf[RI_TN] = pos + 1 < end ? S.pslots[pos + 1] : -1;
     }
+  };
+  auto next_entry = [&]() -> int {
+    const int k = dealt + atomicAdd(&a.wctl[1], 1);
+    return k < nq ? a.wq[k] : -1;
+  };
+  if (agent) {
+    const int k = r * (int)gridDim.x + tile;
+    begin_proc(sInfo + r * kInfo, k < nq ? a.wq[k] : -1);
     for (int k = 0; k < CN_COUNT; ++k) sCnt[k * kTcRows + r] = k == CN_FIRST ? INT_MAX : 0;
   }
   if (tid == 0) {
@@ -374,7 +396,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
       if (PROF && prof_on) fl = clock64();
       const int* inf = sInfo + r * kInfo;
       const bool act = inf[RI_POS] < inf[RI_END];
-      int t = 0, b = 0, p = 0, xd = 0, xu = -1, evt = -1, xuv = 0;
+      int t = 0, b = 0, p = 0, x = 0, xd = 0, xu = -1, evt = -1, xuv = 0, dres = 0;
       float xui = 0.f;
       uint32_t hv[NCH][8];  // checkpoint counts of the group's nodes, 8 per chunk
       uint32_t e8[8];       // the 8-slot event block
@@ -387,6 +409,8 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
       if (act) {
         t = inf[RI_T];
         p = inf[RI_P];
+        x = inf[RI_X];
+        dres = inf[RI_DRESET];
         xd = inf[RI_XDIRTY] | (xpersist ? 0 : 1);
         xu = inf[RI_XUPD];
         evt = inf[RI_EVT];
@@ -398,7 +422,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
         for (int c = 0; c < NCH; ++c)
           if (8 * c < gcn) ldg256(hr + 8 * c, hv[c]);
         if (!xd && xu >= gc0 && xu < gc0 + gcn) {
-          xuv = S.xloc[(size_t)p * J + xu];
+          xuv = S.xloc[(size_t)x * J + xu];
           xui = __ldg(a.inv_x0 + (size_t)p * J + xu);
         }
       }
@@ -437,7 +461,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
         float fv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int d = (int)dv[i] + (i == eE ? 1 : 0) - (i == eX ? 1 : 0);
+          const int d = (dres ? 0 : (int)dv[i]) + (i == eE ? 1 : 0) - (i == eX ? 1 : 0);
           dv[i] = (uint32_t)d;
           const int cc = max(capv[i] - (int)hv[c][i] + d - (int)((pk[c] >> (4 * i)) & 15u), 0);
           cv[i] = (uint32_t)cc;
@@ -472,7 +496,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
       if (PROF && prof_on) { const long long n_ = clock64(); pacc[13] += n_ - fl; fl = n_; }
       // inventory features x/x0 (columns J + node) and the x > 0 bits
       if (act && xd) {
-        const int* xr = S.xloc + (size_t)p * J + gc0;
+        const int* xr = S.xloc + (size_t)x * J + gc0;
         const float* ix = a.inv_x0 + (size_t)p * J + gc0;
         uint32_t nb = 0;
         for (int i = 0; i < gcn; ++i) {
@@ -499,7 +523,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
     };
     if (agent) {
       // P: the loads this row's update (U) needs; their latency hides behind F
-      int u_ev = -1, u_old = 0, u_wr = 0, u_ref = 0, u_pn = -1, u_rrn = 0, u_otn = 0, u_tnn = -1;
+      int u_ev = -1, u_old = 0, u_wr = 0, u_ref = 0, u_pn = -1, u_rrn = 0, u_otn = 0, u_tnn = -1, u_xn = -1;
       int* inf = sInfo + r * kInfo;
       const int pos = inf[RI_POS], end = inf[RI_END];
       if (pos < end) {
@@ -517,6 +541,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
             asm volatile("prefetch.global.L2 [%0];" ::"l"(S.ev + base + (bn << kLogK)));
           }
           u_pn = S.model.product[tn];
+          u_xn = S.rid[tn];
           u_rrn = S.model.rrow[tn];
           u_otn = S.model.order_t ? S.model.order_t[tn] : tn;
         }
@@ -531,6 +556,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
       inf[RI_URRN] = u_rrn;
       inf[RI_UOTN] = u_otn;
       inf[RI_UTNN] = u_tnn;
+      inf[RI_UXN] = u_xn;
     } else {
       f_phase(std::integral_constant<int, kGChunks>{});
     }
@@ -752,7 +778,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
       for (int i = tid; i < nb * J; i += kTcBlock) {
         const int k = i / J, j = i - k * J;
         const int* inf = sInfo + sCtl[2 + f0 + k] * kInfo;
-        xrow[k * kScrJ + j] = S.xloc[(size_t)inf[RI_P] * J + j];
+        xrow[k * kScrJ + j] = S.xloc[(size_t)inf[RI_X] * J + j];
       }
       __syncthreads();
       cta_recheck(S.model, sA, caps, xrow, sCtl + 2 + f0, nb, sInfo, tid);
@@ -762,7 +788,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
         const int* res = (const int*)(sA + kRcInts) + 2 * kRecheckRows * kScrJ;
         const int exact = res[warp], nonfinite = res[kRecheckRows + warp];
         if (nonfinite) {
-          const int m = a.rows[tile * kTcRows + rr];
+          const int m = inf[RI_M];
           atomicMin(&S.scal->err_nonfinite, ((unsigned long long)m << 32) | (unsigned)inf[RI_OT]);
         }
         if (inf[RI_FLAG] == 1) {
@@ -789,13 +815,14 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
     // ============================ U: update + publish (row agents)
     if (agent) {
       int* inf = sInfo + r * kInfo;
+      inf[RI_DRESET] = 0;
       if (inf[RI_ANY] >= 0) {
-        const int t = inf[RI_T], p = inf[RI_P], dec = inf[RI_DEC];
-        const int u_old = inf[RI_UOLD], u_pn = inf[RI_UPN];
+        const int t = inf[RI_T], x = inf[RI_X], dec = inf[RI_DEC];
+        const int u_old = inf[RI_UOLD], u_xn = inf[RI_UXN];
         // D deltas are applied by the row's F threads next step
         inf[RI_EVT] = inf[RI_UEV];
         inf[RI_XUPD] = dec;
-        if (dec >= 0) atomicSub(&S.xloc[(size_t)p * J + dec], 1);  // fire-and-forget RED
+        if (dec >= 0) atomicSub(&S.xloc[(size_t)x * J + dec], 1);  // fire-and-forget RED
         int* cn = sCnt + r;
         if (dec != u_old) {
           cn[CN_CHANGED * kTcRows] += 1;
@@ -819,11 +846,22 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
             asm volatile("prefetch.global.L2 [%0];" ::"l"(S.ev + base + (bn << kLogK)));
           }
           inf[RI_T] = inf[RI_TN];
-          inf[RI_XDIRTY] = u_pn != p ? 1 : 0;
-          inf[RI_P] = u_pn;
+          inf[RI_XDIRTY] = u_xn != x ? 1 : 0;
+          inf[RI_X] = u_xn;
+          inf[RI_P] = inf[RI_UPN];
           inf[RI_RR] = inf[RI_URRN];
           inf[RI_OT] = inf[RI_UOTN];
           inf[RI_TN] = inf[RI_UTNN];
+        } else {
+          // process done: its evaluation count (evals_per_process, max and
+          // total), then the next entry of the work list
+          const int m = inf[RI_M];
+          const unsigned long long nev = (unsigned)cn[CN_NEV * kTcRows];
+          atomicMax(&S.scal->max_evals, nev);
+          atomicAdd(&S.scal->total_evals, nev);
+          if (S.evals_out) S.evals_out[m] = (long long)nev;
+          cn[CN_NEV * kTcRows] = 0;
+          begin_proc(inf, next_entry());
         }
       }
       if (tid == kTcBlock - 1) {
@@ -840,14 +878,7 @@ __global__ void __launch_bounds__(kTcBlock, 1) k_sweep_product_tc(TcArgs a) {
     for (int k = 0; k < 17; ++k) a.prof[k] = pacc[k];
 #undef PMARK
   if (agent) {
-    const int m = a.rows[tile * kTcRows + r];
     const int* cn = sCnt + r;
-    if (m >= 0) {
-      const unsigned long long nev = (unsigned)cn[CN_NEV * kTcRows];
-      atomicMax(&S.scal->max_evals, nev);
-      atomicAdd(&S.scal->total_evals, nev);
-      if (S.evals_out) S.evals_out[m] = (long long)nev;
-    }
     if (cn[CN_CHANGED * kTcRows]) {
       atomicAdd(&S.scal->changed, (unsigned long long)(unsigned)cn[CN_CHANGED * kTcRows]);
       atomicAdd(&S.scal->conflicts, (unsigned long long)(unsigned)cn[CN_CONFLICTS * kTcRows]);

@@ -48,7 +48,8 @@ __host__ __device__ constexpr int canon_off(int R, int r, int k) {
 
 struct TcArgs {
   SweepArgs s;          // state, publish and counter pointers (as k_sweep_product)
-  const int* rows;      // [ntiles*128] process of each row, -1 = idle
+  const int* wq;        // work list: processes with window slots, heaviest first
+  int* wctl;            // {entries of wq, next entry beyond the dealt ones}
   const unsigned char* wimg;  // kWImgBytes: W1hi W1lo W2hi W2lo W3hi W3lo
   const float* b1f;     // [64]
   const float* b2f;     // [64]

@@ -69,3 +69,18 @@ def all_cases(golden, groups=("toy_two_order", "toy_single_process", "infeasible
         for i, c in enumerate(v if isinstance(v, list) else [v]):
             out.append((f"{g}[{i}]", c))
     return out
+
+
+def is_run_partition(owner, product):
+    """The closed-form engines' plan condition (engine.cu: k_check_runs): every
+    (process, product) stretch is contiguous in the product's slot list, and a
+    process with several stretches owns only whole products."""
+    owner = np.asarray(owner)
+    product = np.asarray(product)
+    runs = {}
+    for p in np.unique(product):
+        own = owner[product == p]
+        cut = np.flatnonzero(np.diff(own)) + 1
+        for k, o in enumerate(np.split(own, cut)):
+            runs.setdefault(int(o[0]), []).append(k == 0)
+    return all(len(v) == 1 or all(v) for v in runs.values())

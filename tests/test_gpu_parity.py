@@ -10,7 +10,7 @@ import pytest
 
 import paper_2406_01939_b200 as P
 from oracle.oracle import ORC, OracleError
-from tests.helpers import (all_cases, load_golden, oracle_instance, oracle_policy, product_instance,
+from tests.helpers import (all_cases, is_run_partition, load_golden, oracle_instance, oracle_policy, product_instance,
                            product_policy)
 
 pytestmark = pytest.mark.gpu
@@ -57,12 +57,14 @@ def test_replay_engine_matches_reference_golden(name, case):
 
 
 def test_product_engine_is_used_for_product_partitions(golden):
+    """engine=PRODUCT on every golden case: run partitions (product partitions
+    and any plan whose per-product stretches qualify) give the golden result,
+    the others are refused with InvalidArgument."""
     used = 0
     for name, case in CASES:
         owner = np.array(case["owner"])
         prod = oracle_instance(case["instance"], ORC).product
-        is_pp = all(len(set(owner[prod == p])) <= 1 for p in set(prod.tolist()))
-        if not is_pp:
+        if not is_run_partition(owner, prod):
             with pytest.raises(P.InvalidArgument):
                 run_gpu(case, "product", history=False)
             continue
@@ -146,6 +148,114 @@ def test_dual_policy_matches_oracle_counters(J, I, T, M, part):
     assert r.policy_eval_count_sequential_equivalent == want.policy_eval_count_sequential_equivalent
     assert r.total_policy_evals == want.total_policy_evals
     assert [x.astuple() for x in r.trace] == [tuple(x) for x in want.trace]
+
+
+def _chunk_case(J, I, T, M, kind, seed=7):
+    ons = NS(**ORC.generate_instance_arrays(J, I, T, 0.0, 0.8, seed, geometry=0 if J <= 30 else 1))
+    inst = product_instance(ons)
+    owner = P.make_product_chunk_partition(inst, M).owner
+    spec = dict(kind=kind, gamma=1.7, seed=5)
+    return ons, inst, owner, oracle_policy(spec, ons, ORC), product_policy(spec, inst)
+
+
+def _same_run(r, want, seq):
+    assert r.actions.tolist() == seq.tolist()
+    assert r.iterations_to_converged == want.iterations_to_converged
+    assert r.iterations_to_correct == want.iterations_to_correct
+    assert r.conflicts == want.conflicts
+    assert r.policy_eval_count_sequential_equivalent == want.policy_eval_count_sequential_equivalent
+    assert r.total_policy_evals == want.total_policy_evals
+    assert [x.astuple() for x in r.trace] == [tuple(x) for x in want.trace]
+
+
+@pytest.mark.parametrize("J,I,T,M,kind", [(10, 300, 20000, 1500, 2), (30, 50, 6000, 400, 2), (100, 20, 3000, 120, 2),
+                                          (10, 100, 8000, 500, 0), (10, 100, 8000, 500, 1), (1, 10, 10000, 64, 2),
+                                          (100, 40, 4000, 300, 2)])
+def test_chunk_partition_matches_oracle(J, I, T, M, kind):
+    """Product chunks (several processes per product, contiguous stretches):
+    the closed form starts every stretch from the frozen-cache replay state
+    (k_xinit); trajectory and every per-iteration counter as the oracle."""
+    ons, inst, owner, opol, pol = _chunk_case(J, I, T, M, kind)
+    assert len(np.unique(owner)) > I  # products really are split
+    seq, _ = ORC.sequential(ons, opol)
+    want = ORC.picard(ons, opol, owner, M, record_trace=True, reference=seq)
+    for engine in (("product", "product_fp64") if kind == 2 else ("product",)):
+        r = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(record_trace=True, engine=engine),
+                              reference_actions=seq)
+        assert r.timing["tc_used"] == (1 if engine == "product" and kind == 2 else 0)
+        _same_run(r, want, seq)
+
+
+def test_chunk_partition_windows_and_warm_starts_match_oracle():
+    ons, inst, owner, opol, pol = _chunk_case(10, 50, 3000, 160, 2)
+    seq, _ = ORC.sequential(ons, opol)
+    draft, _ = ORC.sequential(ons, NS(kind=1, hidden=64, gamma=2.0, horizon=None))
+    for ms in (1, 7, 300, 0):
+        for init in (None, draft):
+            want = ORC.picard(ons, opol, owner, 160, max_steps=ms, record_trace=True, reference=seq,
+                              initial_cache=init)
+            for engine in ("product", "product_fp64"):
+                r = P.picard_simulate(inst, pol, P.PartitionPlan(160, owner),
+                                      P.PicardConfig(max_steps=ms, record_trace=True, engine=engine), init, seq)
+                _same_run(r, want, seq)
+
+
+@pytest.mark.parametrize("engine", ["product", "product_fp64"])
+def test_chunk_partition_iterate_once_random_caches_match_oracle(engine):
+    """Arbitrary caches, windows and checkpoints under product chunks and mixed
+    run plans (whole products + chunks): one iteration equals
+    picard_iterate_once exactly — the closed form holds for any cache."""
+    rng = np.random.default_rng(23)
+    for seed in range(30):
+        J, I, T, beta, cov, s = ORC.small_random_params(900 + seed)
+        ons = NS(**ORC.generate_instance_arrays(J, I, T, beta, cov, s))
+        inst = product_instance(ons)
+        M = int(rng.integers(I, 4 * I + 8))
+        owner = P.make_product_chunk_partition(inst, M).owner.copy()
+        if seed % 2:  # mixed: merge some whole products onto one process
+            q = np.bincount(ons.product, minlength=I)
+            whole = [p for p in range(I) if q[p] and len(np.unique(owner[ons.product == p])) == 1]
+            for p in whole[1::2]:
+                owner[ons.product == p] = owner[ons.product == whole[0]][0]
+        kind = 2 if engine == "product" else seed % 3
+        spec = dict(kind=kind, gamma=1.3, seed=seed)
+        opol = oracle_policy(spec, ons, ORC)
+        pol = product_policy(spec, inst)
+        cache = rng.integers(-3, J + 2, T).astype(np.int32)
+        lo = int(rng.integers(0, T))
+        hi = int(rng.integers(lo, T + 1))
+        ck_cap = ons.capacity.copy()
+        ck_inv = ons.inventory.copy().reshape(I, J)
+        for t in range(lo):
+            a = int(rng.integers(-1, J))
+            p = ons.product[t]
+            if a >= 0 and ck_cap[a] > 0 and ck_inv[p, a] > 0:
+                ck_cap[a] -= 1
+                ck_inv[p, a] -= 1
+        want, want_evals, want_changed = ORC.iterate_once(ons, opol, owner, M, cache, lo, hi, ck_cap, ck_inv.ravel())
+        got = cache.copy()
+        out = P.picard_iterate_once(inst, pol, P.PartitionPlan(M, owner), got, lo, hi, ck_cap, ck_inv, engine)
+        assert got.tolist() == want.tolist(), seed
+        assert out.evals_per_process.tolist() == want_evals.tolist()
+        assert out.changed_slots.tolist() == want_changed.tolist()
+
+
+@pytest.mark.parametrize("tiles", ["1", "3"])
+def test_tensor_core_work_list_pulls_match(tiles, monkeypatch):
+    """Fewer CTAs than processes / 128: rows pull processes from the work list
+    mid-iteration (per-process counters flushed at each switch)."""
+    ons, inst, owner, opol, pol = _chunk_case(30, 100, 20000, 900, 2)
+    seq, _ = ORC.sequential(ons, opol)
+    ref = P.picard_simulate(inst, pol, P.PartitionPlan(900, owner),
+                            P.PicardConfig(record_trace=True, engine="product_fp64"), reference_actions=seq)
+    monkeypatch.setenv("PCD_TC_TILES", tiles)
+    r = P.picard_simulate(inst, pol, P.PartitionPlan(900, owner), P.PicardConfig(record_trace=True, engine="product"),
+                          reference_actions=seq)
+    assert r.timing["tc_used"] == 1
+    assert r.actions.tolist() == seq.tolist()
+    assert [x.astuple() for x in r.trace] == [x.astuple() for x in ref.trace]
+    assert (r.conflicts, r.iterations_to_correct, r.total_policy_evals) == \
+        (ref.conflicts, ref.iterations_to_correct, ref.total_policy_evals)
 
 
 def test_sequential_drop_in_matches_oracle():

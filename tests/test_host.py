@@ -11,7 +11,7 @@ import pytest
 import paper_2406_01939_b200 as P
 from paper_2406_01939_b200 import _capi
 from oracle.oracle import ORC
-from tests.helpers import oracle_instance
+from tests.helpers import is_run_partition, oracle_instance
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -89,6 +89,34 @@ def test_product_partition_matches_oracle(M, seed):
     # each product on one process (test_instance.cpp:243-255)
     for p in range(60):
         assert len(set(plan.owner[inst.product == p].tolist())) <= 1
+
+
+@pytest.mark.parametrize("J,I,T,M", [(4, 60, 700, 64), (4, 60, 700, 200), (10, 300, 20000, 4096), (3, 5, 40, 1000),
+                                     (4, 60, 700, 7)])
+def test_product_chunk_partition_is_a_balanced_run_partition(J, I, T, M):
+    inst = P.generate_instance(J, I, T, -0.5, 0.8, 13)
+    plan = P.make_product_chunk_partition(inst, M)
+    assert plan.owner.min() >= 0 and plan.owner.max() < M
+    assert is_run_partition(plan.owner, inst.product)
+    q = np.bincount(inst.product, minlength=I)
+    used = int((q > 0).sum())
+    if M < used:  # falls back to the reference's product partition
+        assert np.array_equal(plan.owner, P.make_product_partition(inst, M, 1).owner)
+        return
+    loads = np.bincount(plan.owner, minlength=M)
+    L = int(loads.max())
+    # L is the smallest chunk length that fits in M processes
+    assert int(np.ceil(q / L).sum()) <= M
+    if L > 1:
+        assert int(np.ceil(q / (L - 1)).sum()) > M
+    # chunks of a product differ by at most one order and follow time order
+    for p in range(I):
+        own = plan.owner[inst.product == p]
+        if own.size:
+            assert (np.diff(own) >= 0).all()
+            c = np.bincount(own - own.min())
+            c = c[c > 0]
+            assert c.max() - c.min() <= 1
 
 
 def test_product_partition_hand_trace(golden):
