@@ -26,7 +26,8 @@
 
 namespace pcd {
 
-void launch_tc_sweep(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_sweep.cu
+void launch_tc_sweep(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_sweep.cu (128-row lockstep)
+void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream);     // tc_pp.cu (two 64-row halves)
 size_t tc_smem_bytes();
 
 #define CK(x)                                                                              \
@@ -367,7 +368,9 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   // PCD_TC_TILES=n (tests): fewer CTAs than SMs, so rows pull from the work list
   int tiles = h->tc_tiles;
   if (const char* e = getenv("PCD_TC_TILES")) tiles = std::max(1, std::min(tiles, atoi(e)));
-  launch_tc_sweep(a, tiles, h->stream);
+  static const bool lockstep = getenv("PCD_TC_LOCKSTEP") != nullptr;  // A/B knob
+  if (lockstep) launch_tc_sweep(a, tiles, h->stream);
+  else launch_tc_pp(a, tiles, h->stream);
   CK(cudaGetLastError());
   if (prof) {
     long long v[20];

@@ -1,0 +1,827 @@
+// tc_pp.cu — the tcgen05 run-partition sweep, ping-pong form (see
+// tc_sweep.cuh for the MLP / precision / exactness scheme).
+//
+// A CTA (one per SM, 16 warps) runs TWO independent 64-row pipelines
+// ("halves"). Half h owns warps 8h..8h+7, the TMEM lanes {32q + 16h + i :
+// q < 4, i < 16} (an M=64 tcgen05.mma accumulator at lane offset 16h), its
+// own 64-row A operand in smem, its own mbarrier and named barrier (1 + h).
+// The weights and the tensor core are shared. While one half waits on its
+// MMAs or on the checkpoint-row loads of its next step, the other half's
+// CUDA-core phases (features, tanh epilogues, scores) run, so latency that a
+// single 128-row lockstep exposes is overlapped.
+//
+// Thread mapping inside a half: warp w = 8h + 4p + q, lane l: row
+// r = 16q + (l & 15) (TMEM lane 32q + 16h + (l & 15)), node group
+// g = 2p + (l >> 4). TMEM is accessed with the .16x32bx2 shapes (split 8
+// columns), so group g of a row owns the 8-node chunks g, g+4, g+8, g+12 of
+// every per-node TMEM region and the 8-unit chunks g, g+4 of the hidden
+// layers. Group 3 threads are the row agents (per-row bookkeeping, update
+// operand loads, publish, work-list pulls).
+//
+// Per step and half: F (capacities c = max(0, ckcap - H + D - partial),
+// features, feasibility) -> L1 / E1 / L2 / E2 / L3 (fp16x3 MMAs, tanh
+// epilogues) -> S (scores, per-group argmax + margin) -> agents combine ->
+// exact FP64 re-evaluation of rows with margin < guard (half-local) -> U.
+// The state algebra is the run-partition closed form of k_sweep_product.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdio>
+
+#include "tc_sweep.cuh"
+
+namespace pcd {
+namespace pp {
+
+constexpr int kBlock = 512;
+constexpr int kHalfRows = 64;
+constexpr int kHalfThreads = 256;
+constexpr int kInfo = 28;
+constexpr int kMaxJ = 103;  // 2J+1 <= 208
+constexpr int kScrJ = 112;
+constexpr int kMaxCI = 4;   // node chunks per thread (13 chunks for J <= 103)
+constexpr uint32_t kTmemCols = 512, kColD = 256, kColCap = 384;
+constexpr int kAH = kHalfRows * kTcK1 * 2;  // bytes of one of hi / lo for a half
+constexpr int kChunkB = kHalfRows * 8 * 2;  // bytes per k-chunk of a half's operand
+
+enum {
+  RI_T = 0, RI_P, RI_POS, RI_END, RI_ANY, RI_DEC, RI_FLAG, RI_RR, RI_TN, RI_XDIRTY, RI_XUPD, RI_OT, RI_EVT,
+  RI_X, RI_M, RI_DRESET,
+  RI_UEV, RI_UOLD, RI_UWR, RI_UREF, RI_UPN, RI_URRN, RI_UOTN, RI_UTNN, RI_UXN
+};
+static_assert(RI_UXN < kInfo, "per-row state fits");
+enum { CN_CHANGED = 0, CN_CONFLICTS, CN_FIRST, CN_MISM, CN_NEV, CN_TC, CN_COUNT };
+// per-half control block: [0] active rows, [1] flagged rows, [2..66) flagged rows
+enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, kCtl = 80 };
+
+struct Layout {
+  static constexpr int w = 0;
+  static constexpr int a = kWImgBytes;                       // half h: hi at a + 2h kAH, lo + kAH
+  static constexpr int info = a + 4 * kAH;                   // 128 x kInfo ints
+  static constexpr int best = info + kTcRows * kInfo * 4;    // 128 x 4 groups x 3
+  static constexpr int cap = best + kTcRows * 4 * 3 * 4;     // checkpoint capacities [112]
+  static constexpr int ctl = cap + kScrJ * 4;                // 2 x kCtl
+  static constexpr int cst = ctl + 2 * kCtl * 4;             // invc0[112] b1[64] b2[64] b3[112]
+  static constexpr int cnt = cst + 352 * 4;                  // per-row counters
+  static constexpr int prof = cnt + CN_COUNT * kTcRows * 4;  // debug phase clocks [20]
+  static constexpr int bar = prof + 20 * 8;                  // one mbarrier per half
+  static constexpr int tmem = bar + 16;
+  static constexpr int total = tmem + 16;
+};
+static_assert(Layout::total <= 232448, "ping-pong sweep shared memory budget");
+static_assert(Layout::cap % 16 == 0 && Layout::cst % 16 == 0 && Layout::prof % 8 == 0, "aligned smem rows");
+
+// canonical K-major no-swizzle offsets of a 64-row operand
+__device__ __forceinline__ int kc64(int k) { return (k >> 3) * kChunkB + (k & 7) * 2; }
+__device__ __forceinline__ int ro64(int r) { return (r >> 3) * 128 + (r & 7) * 16; }
+
+__device__ __forceinline__ void bar_half(int h) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(kHalfThreads) : "memory");
+}
+// .16x32bx2 TMEM access: threads 0-15 -> lanes base..base+15 at columns
+// col..col+7, threads 16-31 -> the same lanes at col+8..col+15
+__device__ __forceinline__ void ld8s(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], 8;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void st8s(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], 8, {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 hh = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(hh);
+  const __half2 l = __floats2half2_rn((x0 - hf.x) * kLoScale, (x1 - hf.y) * kLoScale);
+  hi = *(const uint32_t*)&hh;
+  lo = *(const uint32_t*)&l;
+}
+__device__ __forceinline__ void put_feature(unsigned char* sAh, int off, float v) {
+  __half hh, l;
+  split_f16(v, hh, l);
+  *(__half*)(sAh + off) = hh;
+  *(__half*)(sAh + kAH + off) = l;
+}
+
+// ---------------------------------------------------------------------------
+// Exact FP64 re-evaluation of one flagged row by its half (256 threads):
+// DualNetworkPolicy::evaluate (policies.hpp:121-168) in exactly the operation
+// order of warp_policy_eval<kDual> — one thread per output neuron runs the
+// acc = b; acc += w * x chain on weights read from L2. Scratch lives in the
+// first k-chunks of the half's operand (free between layer 3 and the next F).
+//   hi [0, ...)  caps / x row / results (ints)
+//   lo [0, ...)  f / h1 / h2 / pr (doubles)
+constexpr int kRcInts = 0;
+constexpr int kRcVec = 2 * kMaxJ + 2 + 2 * kTcH + 2 * kMaxJ;
+constexpr int kRcScratchHi = (kRcInts + (2 * kScrJ + 2) * 4 + 15) & ~15;
+constexpr int kRcScratchLo = (kRcVec * 8 + 15) & ~15;
+static_assert(kRcScratchHi <= 12 * kChunkB && kRcScratchLo <= 12 * kChunkB, "recheck scratch in k-chunks 0..11");
+// operand columns the recheck scratch may overwrite (the x/x0 features persist
+// across steps only when they lie above these and above the hidden operands)
+constexpr int kScratchCols = ((kRcScratchHi > kRcScratchLo ? kRcScratchHi : kRcScratchLo) + kChunkB - 1) / kChunkB * 8;
+
+// outv[r] = (tanh?)(bias[r] + sum_c W[c][r] * xin[c]) for r < width: one
+// thread per output neuron, the weights read straight from L2 (W is [K][width],
+// so a warp reads contiguous rows), 16 loads in flight ahead of the chain
+__device__ void rc_layer(const double* __restrict__ W, const double* __restrict__ bias, int K, int width,
+                         const double* xin, double* outv, bool act_tanh, int tanh_fma, int ht, int h) {
+  if (ht < width) {
+    double acc = __ldg(bias + ht);
+    const double* w = W + ht;
+    int c = 0;
+    for (; c + 16 <= K; c += 16) {
+      double wv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) wv[u] = __ldg(w + (size_t)(c + u) * width);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, __dmul_rn(wv[u], xin[c + u]));
+    }
+    for (; c < K; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(w + (size_t)c * width), xin[c]));
+    outv[ht] = act_tanh ? gt_tanh(acc, tanh_fma) : acc;
+  }
+  bar_half(h);
+}
+
+// res[0] = exact decision, res[1] = non-finite score flag
+__device__ void half_recheck(const DevModel& P, unsigned char* sAh, const int* caps, const int* xrow, int t,
+                             int* res, int ht, int h) {
+  const int J = P.J, H = P.H, in = P.in, out = P.out;
+  double* vec = (double*)(sAh + kAH);
+  for (int j = ht; j < in; j += kHalfThreads) {
+    double f;
+    if (j < J) {
+      const int c0 = __ldg(P.pcap0 + j);
+      f = c0 > 0 ? __ddiv_rn((double)caps[j], (double)c0) : 0.0;
+    } else if (j < 2 * J) {
+      const int x0 = __ldg(P.pinv0 + (size_t)P.product[t] * J + (j - J));
+      f = x0 > 0 ? __ddiv_rn((double)xrow[j - J], (double)x0) : 0.0;
+    } else {
+      const int ot = P.order_t ? P.order_t[t] : t;
+      f = P.horizon > 0 ? __ddiv_rn((double)ot, (double)P.horizon) : 0.0;
+    }
+    vec[j] = f;
+  }
+  bar_half(h);
+  const int oh1 = 2 * kMaxJ + 2, oh2 = oh1 + kTcH, opr = oh2 + kTcH;
+  rc_layer(P.w1t, P.b1, in, H, vec, vec + oh1, true, P.tanh_fma, ht, h);
+  rc_layer(P.w2t, P.b2, H, H, vec + oh1, vec + oh2, true, P.tanh_fma, ht, h);
+  rc_layer(P.w3t, P.b3, H, out, vec + oh2, vec + opr, false, P.tanh_fma, ht, h);
+  if (ht < 32) {  // scores and argmax as warp_policy_eval<kDual>
+    const int lane = ht;
+    const double* rw = P.rtab + (size_t)P.rrow[t] * J;
+    const double* pr = vec + opr;
+    bool feas = false;
+    for (int j = lane; j < J; j += 32) feas |= caps[j] > 0 && xrow[j] > 0;
+    int exact = -1, nonfinite = 0;
+    if (__any_sync(0xffffffffu, feas)) {
+      double bv = 0.0;
+      int bi = -1;
+      bool bad = false;
+      for (int j = lane; j < J; j += 32) {
+        if (caps[j] <= 0 || xrow[j] <= 0) continue;
+        const double sc = __dsub_rn(__dsub_rn(__ldg(rw + j), pr[j]), pr[J + j]);
+        if (!isfinite(sc)) { bad = true; continue; }
+        argmax_combine(bv, bi, sc, j);
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+        nonfinite = 1;
+      } else {
+        warp_argmax(bv, bi);
+        exact = (bi >= 0 && bv >= 0.0) ? bi : -1;
+      }
+    }
+    if (lane == 0) {
+      res[0] = exact;
+      res[1] = nonfinite;
+    }
+  }
+  bar_half(h);
+}
+
+template <bool PROF>
+__global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const SweepArgs& S = a.s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int J = S.J, lo = S.lo, hi = S.hi;
+  const int base = hck_base(lo), HJ = hck_stride(J), RJ = (J + 7) & ~7;
+  unsigned char* sW = smem + Layout::w;
+  int* sInfo = (int*)(smem + Layout::info);
+  float* sBest = (float*)(smem + Layout::best);
+  int* sCap = (int*)(smem + Layout::cap);
+  int* sCtlAll = (int*)(smem + Layout::ctl);
+  int* sCnt = (int*)(smem + Layout::cnt);
+  uint64_t* sBar = (uint64_t*)(smem + Layout::bar);
+  uint32_t* sTmem = (uint32_t*)(smem + Layout::tmem);
+  float* sInvC0 = (float*)(smem + Layout::cst);
+  float* sB1 = sInvC0 + kScrJ;
+  float* sB2 = sB1 + 64;
+  float* sB3 = sB2 + 64;
+  const int tile = blockIdx.x;
+  // half / row / node-group of this thread
+  const int h = warp >> 3, wq = warp & 7, q = wq & 3, p2 = wq >> 2, th = lane >> 4;
+  const int g = 2 * p2 + th;
+  const int rr = 16 * q + (lane & 15);
+  const int R = kHalfRows * h + rr;
+  const bool agent = g == 3;
+  const int ht = tid & (kHalfThreads - 1);
+  const uint32_t tl = (uint32_t)(32 * q + 16 * h) << 16;
+  unsigned char* sAh = smem + Layout::a + 2 * h * kAH;
+  int* ctl = sCtlAll + h * kCtl;
+  uint64_t* bar = sBar + h;
+  const int rowo = ro64(rr);
+  const int nchunk = (J + 7) >> 3;
+  const int ni = (nchunk - 2 * p2 + 3) >> 2;  // node chunks of this warp pair (warp-uniform)
+  const bool xpersist = J >= kTcH && J >= kScratchCols;  // x/x0 columns never overwritten
+
+  // ---------------------------------------------------------------- setup
+  {
+    const uint4* src = (const uint4*)a.wimg;
+    uint4* dst = (uint4*)sW;
+    for (int i = tid; i < kWImgBytes / 16; i += kBlock) dst[i] = src[i];
+    uint4* da = (uint4*)(smem + Layout::a);
+    for (int i = tid; i < 4 * kAH / 16; i += kBlock) da[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int j = tid; j < kScrJ; j += kBlock) {
+    sCap[j] = j < J ? S.ckcap[j] : 0;
+    sInvC0[j] = j < J ? a.inv_c0[j] : 0.f;
+  }
+  for (int i = tid; i < kTcH; i += kBlock) {
+    sB1[i] = a.b1f[i];
+    sB2[i] = a.b2f[i];
+  }
+  for (int i = tid; i < kTcN3; i += kBlock) sB3[i] = a.b3f[i];
+  const int nq = a.wctl[0], dealt = (int)gridDim.x * kTcRows;
+  auto begin_proc = [&](int* inf, int m) {
+    int pos = 0, end = 0;
+    if (m >= 0) {
+      const int beg = S.pstart[m], n = S.pstart[m + 1] - beg;
+      pos = beg + lower_bound_i32(S.pslots + beg, n, lo);
+      end = beg + lower_bound_i32(S.pslots + beg, n, hi);
+    }
+    inf[RI_M] = m;
+    inf[RI_POS] = pos;
+    inf[RI_END] = end;
+    inf[RI_XDIRTY] = 1;
+    inf[RI_XUPD] = -1;
+    inf[RI_EVT] = -1;
+    inf[RI_DRESET] = 1;
+    inf[RI_P] = -1;
+    inf[RI_X] = -1;
+    if (pos < end) {
+      const int t = S.pslots[pos];
+      inf[RI_T] = t;
+      inf[RI_P] = S.model.product[t];
+      inf[RI_X] = S.rid[t];
+      inf[RI_RR] = S.model.rrow[t];
+      inf[RI_OT] = S.model.order_t ? S.model.order_t[t] : t;
+      inf[RI_TN] = pos + 1 < end ? S.pslots[pos + 1] : -1;
+    }
+  };
+  auto next_entry = [&]() -> int {
+    const int k = dealt + atomicAdd(&a.wctl[1], 1);
+    return k < nq ? a.wq[k] : -1;
+  };
+  if (agent) {
+    const int k = R * (int)gridDim.x + tile;
+    begin_proc(sInfo + R * kInfo, k < nq ? a.wq[k] : -1);
+    for (int k2 = 0; k2 < CN_COUNT; ++k2) sCnt[k2 * kTcRows + R] = k2 == CN_FIRST ? INT_MAX : 0;
+  }
+  for (int i = tid; i < 2 * kCtl; i += kBlock) sCtlAll[i] = 0;
+  if (tid == 0) {
+    mbar_init(sBar, 1);
+    mbar_init(sBar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *sTmem;
+  const uint32_t tD = tmem + ((uint32_t)(16 * h) << 16);  // MMA accumulator base of the half
+  {  // D = 0
+    const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < ni; ++i) st8s(tmem + tl + kColD + 16 * p2 + 32 * i, z);
+    tmem_wait_st();
+  }
+
+  const uint32_t aBase = smem_u32(sAh);
+  const uint32_t w1h = smem_u32(sW), w1l = w1h + kW1Bytes;
+  const uint32_t w2h = w1l + kW1Bytes, w2l = w2h + kW2Bytes;
+  const uint32_t w3h = w2l + kW2Bytes, w3l = w3h + kW3Bytes;
+  const uint32_t id64 = idesc_f16(64, 64), id112 = idesc_f16(64, kTcN3);
+  uint32_t phase = 0;
+  const float invT = S.model.horizon > 0 ? (float)(1.0 / (double)S.model.horizon) : 0.f;
+  uint32_t xb = 0;  // x > 0 bits of the thread's nodes (bit 8i + k: node 8(g + 4i) + k), persistent
+
+  long long* pacc = (long long*)(smem + Layout::prof);
+  if (PROF && tid == 0)
+    for (int k = 0; k < 20; ++k) pacc[k] = 0;
+  long long plast = PROF ? clock64() : 0;
+  const bool prof_on = PROF && blockIdx.x == 0 && tid == 0;
+#define PMARK(k) do { if (PROF && prof_on) { const long long now_ = clock64(); pacc[k] += now_ - plast; plast = now_; } } while (0)
+
+  // the half's MMAs of one layer: K16 k-steps, three products into (acc, acc+off)
+  auto issue_layer = [&](uint32_t acc, uint32_t off, uint32_t wh, uint32_t wl, uint32_t wlbo, int ksteps,
+                         uint32_t id) {
+    tc_fence_after();
+    const uint64_t dA = umma_desc(aBase, kHalfRows * 16, 128), dAl = umma_desc(aBase + kAH, kHalfRows * 16, 128);
+    const uint64_t dW = umma_desc(wh, wlbo, 128), dWl = umma_desc(wl, wlbo, 128);
+    for (int s = 0; s < ksteps; ++s) {
+      const uint64_t ah = dA + s * ((2 * kChunkB) >> 4), al = dAl + s * ((2 * kChunkB) >> 4);
+      const uint64_t bh = dW + s * ((2 * wlbo) >> 4), bl = dWl + s * ((2 * wlbo) >> 4);
+      mma_f16(tD + acc, ah, bh, id, s > 0);
+      mma_f16(tD + acc + off, ah, bl, id, s > 0);
+      mma_f16(tD + acc + off, al, bh, id, 1);
+    }
+    mma_commit(bar);
+  };
+
+  for (;;) {
+    // ============================ F: capacities, features, feasibility
+    uint32_t fmask = 0;  // feasible nodes of the thread (bit 8i + k)
+    int* inf = sInfo + R * kInfo;
+    int u_ev = -1, u_old = 0, u_wr = 0, u_ref = 0, u_pn = -1, u_rrn = 0, u_otn = 0, u_tnn = -1, u_xn = -1;
+    if (agent) {  // P: the operands of this row's update (U); latency hidden behind F
+      const int pos = inf[RI_POS], end = inf[RI_END];
+      if (pos < end) {
+        const int t = inf[RI_T];
+        u_ev = S.ev[t];
+        u_old = S.cache[t];
+        u_wr = S.written[t];
+        if (S.ref) u_ref = S.ref[t];
+        const int tn = inf[RI_TN];
+        if (tn >= 0) {
+          u_pn = S.model.product[tn];
+          u_xn = S.rid[tn];
+          u_rrn = S.model.rrow[tn];
+          u_otn = S.model.order_t ? S.model.order_t[tn] : tn;
+        }
+        if (pos + 2 < end) u_tnn = S.pslots[pos + 2];
+      }
+    }
+    {
+      const bool act = inf[RI_POS] < inf[RI_END];
+      int t = 0, b = 0, p = 0, x = 0, xd = 0, xu = -1, evt = -1, xuv = 0, dres = 0;
+      float xui = 0.f;
+      uint32_t hv[kMaxCI][8];
+      uint32_t e8[8];
+#pragma unroll
+      for (int i = 0; i < kMaxCI; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hv[i][k] = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e8[k] = 0xffffffffu;
+      // the thread's chunk of a node (>= 0) or -1
+      auto my_ci = [&](int j) { return (j >= 0 && ((j >> 3) & 3) == g) ? (j >> 5) : -1; };
+      if (act) {
+        t = inf[RI_T];
+        p = inf[RI_P];
+        x = inf[RI_X];
+        dres = inf[RI_DRESET];
+        xd = inf[RI_XDIRTY] | (xpersist ? 0 : 1);
+        xu = inf[RI_XUPD];
+        evt = inf[RI_EVT];
+        b = (t - base) >> kLogK;
+        ldg256(S.ev + base + (b << kLogK), e8);
+        const int* hr = S.hck + (size_t)b * HJ;
+#pragma unroll
+        for (int i = 0; i < kMaxCI; ++i)
+          if (i < ni && 8 * (g + 4 * i) < J) ldg256(hr + 8 * (g + 4 * i), hv[i]);
+        if (!xd && my_ci(xu) >= 0) {
+          xuv = S.xloc[(size_t)x * J + xu];
+          xui = __ldg(a.inv_x0 + (size_t)p * J + xu);
+        }
+      }
+      // partial block [max(lo, base + 8b), t): per-chunk packed nibble counts
+      uint32_t pk[kMaxCI];
+#pragma unroll
+      for (int i = 0; i < kMaxCI; ++i) pk[i] = 0;
+      {
+        const int sb = base + (b << kLogK);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int s = sb + k;
+          const int ek = (int)e8[k];
+          const int ci = (act && s >= lo && s < t) ? my_ci(ek) : -1;
+          const uint32_t nib = 1u << (4 * (ek & 7));
+#pragma unroll
+          for (int i = 0; i < kMaxCI; ++i) pk[i] += ci == i ? nib : 0u;
+        }
+      }
+      PMARK(12);
+      const int ciE = my_ci(evt), ciX = my_ci(xu);
+#pragma unroll
+      for (int i = 0; i < kMaxCI; ++i) {
+        if (i >= ni) break;  // warp-uniform; constant trip count keeps the arrays in registers
+        const int j0 = 8 * (g + 4 * i);
+        const bool live = j0 < J;
+        const int jc = live ? j0 : 0;
+        uint32_t dv[8];
+        ld8s(tmem + tl + kColD + 16 * p2 + 32 * i, dv);
+        tmem_wait_ld();
+        const int eE = ciE == i ? (evt & 7) : -1, eX = ciX == i ? (xu & 7) : -1;
+        const int4 cp0 = *(const int4*)(sCap + jc), cp1 = *(const int4*)(sCap + jc + 4);
+        const float4 iv0 = *(const float4*)(sInvC0 + jc), iv1 = *(const float4*)(sInvC0 + jc + 4);
+        const int capv[8] = {cp0.x, cp0.y, cp0.z, cp0.w, cp1.x, cp1.y, cp1.z, cp1.w};
+        const float inv[8] = {iv0.x, iv0.y, iv0.z, iv0.w, iv1.x, iv1.y, iv1.z, iv1.w};
+        uint32_t cv[8], bits = 0;
+        float fv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int d = (dres ? 0 : (int)dv[k]) + (k == eE ? 1 : 0) - (k == eX ? 1 : 0);
+          dv[k] = (uint32_t)d;
+          const int cc = max(capv[k] - (int)hv[i][k] + d - (int)((pk[i] >> (4 * k)) & 15u), 0);
+          cv[k] = (uint32_t)cc;
+          bits |= (cc > 0 ? 1u : 0u) << k;
+          fv[k] = (float)cc * inv[k];
+        }
+        st8s(tmem + tl + kColD + 16 * p2 + 32 * i, dv);
+        st8s(tmem + tl + kColCap + 16 * p2 + 32 * i, cv);
+        if (live) {
+          fmask |= bits << (8 * i);
+          uint32_t h4[4], l4[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) split2(fv[2 * k], fv[2 * k + 1], h4[k], l4[k]);
+          if (act) {
+            const int off = rowo + kc64(j0);
+            if (j0 + 8 <= J) {
+              *(uint4*)(sAh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+              *(uint4*)(sAh + kAH + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+            } else {  // last partial chunk: the columns from J on are inventory features
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (j0 + 2 * k + 1 < J) {
+                  *(uint32_t*)(sAh + off + 4 * k) = h4[k];
+                  *(uint32_t*)(sAh + kAH + off + 4 * k) = l4[k];
+                } else if (j0 + 2 * k < J) {
+                  *(uint16_t*)(sAh + off + 4 * k) = (uint16_t)h4[k];
+                  *(uint16_t*)(sAh + kAH + off + 4 * k) = (uint16_t)l4[k];
+                }
+              }
+            }
+          }
+        }
+      }
+      PMARK(13);
+      // inventory features x/x0 (columns J + node) and the x > 0 bits
+      if (act && xd) {
+        const int* xr = S.xloc + (size_t)x * J;
+        const float* ix = a.inv_x0 + (size_t)p * J;
+        uint32_t nb = 0;
+#pragma unroll
+        for (int i = 0; i < kMaxCI; ++i) {
+          if (i >= ni) break;
+          const int j0 = 8 * (g + 4 * i);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (j0 + k >= J) break;
+            const int xj = xr[j0 + k];
+            put_feature(sAh, rowo + kc64(J + j0 + k), (float)xj * __ldg(ix + j0 + k));
+            nb |= (xj > 0 ? 1u : 0u) << (8 * i + k);
+          }
+        }
+        xb = nb;
+      } else if (act && ciX >= 0) {
+        put_feature(sAh, rowo + kc64(J + xu), (float)xuv * xui);
+        if (xuv <= 0) xb &= ~(1u << (8 * ciX + (xu & 7)));
+      }
+      if (act && agent) put_feature(sAh, rowo + kc64(2 * J), (float)inf[RI_OT] * invT);
+      fmask = act ? (fmask & xb) : 0u;
+      if (p2 == 0) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, act) & 0xffffu;
+        if (lane == 0) {
+          ctl[CT_QACT + q] = bal != 0;
+          if (bal) atomicAdd(&ctl[0], __popc(bal));
+        }
+      }
+      tmem_wait_st();
+      PMARK(14);
+    }
+    if (agent) {
+      inf[RI_UEV] = u_ev;
+      inf[RI_UOLD] = u_old;
+      inf[RI_UWR] = u_wr;
+      inf[RI_UREF] = u_ref;
+      inf[RI_UPN] = u_pn;
+      inf[RI_URRN] = u_rrn;
+      inf[RI_UOTN] = u_otn;
+      inf[RI_UTNN] = u_tnn;
+      inf[RI_UXN] = u_xn;
+    }
+    tc_fence_before();
+    fence_async_smem();
+    bar_half(h);
+    PMARK(0);
+    if (ctl[0] == 0) break;
+    if (PROF && prof_on) pacc[10] += 1;
+
+    // ============================ layer 1: z1 = F . W1^T (three products)
+    if (ht == 0) issue_layer(0, 64, w1h, w1l, kTcH * 16, kTcK1 / 16, id64);
+    mbar_wait(bar, phase);
+    PMARK(1);
+    phase ^= 1;
+    tc_fence_after();
+
+    // ============================ hidden epilogues (z -> tanh -> fp16 hi/lo)
+    const bool qact = ctl[CT_QACT + q] != 0;  // warp-uniform: skip idle row quarters
+    auto hidden_epilogue = [&](uint32_t col_hh, uint32_t col_x, const float* bias) {
+      if (!qact) return;
+      uint32_t vh[2][8], vx[2][8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        ld8s(tmem + tl + col_hh + 16 * p2 + 32 * i, vh[i]);
+        ld8s(tmem + tl + col_x + 16 * p2 + 32 * i, vx[i]);
+      }
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int u0 = 8 * (g + 4 * i);
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const float z0 = fmaf(__uint_as_float(vx[i][k]), kLoInv, __uint_as_float(vh[i][k])) + bias[u0 + k];
+          const float z1 =
+              fmaf(__uint_as_float(vx[i][k + 1]), kLoInv, __uint_as_float(vh[i][k + 1])) + bias[u0 + k + 1];
+          split2(tanh_f32(z0), tanh_f32(z1), ph[k / 2], pl[k / 2]);
+        }
+        const int off = rowo + kc64(u0);
+        *(uint4*)(sAh + off) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+        *(uint4*)(sAh + kAH + off) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+      }
+    };
+    hidden_epilogue(0, 64, sB1);
+    tc_fence_before();
+    fence_async_smem();
+    bar_half(h);
+    PMARK(2);
+
+    // ============================ layer 2
+    if (ht == 0) issue_layer(128, 64, w2h, w2l, kTcH * 16, kTcH / 16, id64);
+    mbar_wait(bar, phase);
+    PMARK(3);
+    phase ^= 1;
+    tc_fence_after();
+    hidden_epilogue(128, 192, sB2);  // h2 overwrites h1 (layer 2 has completed)
+    tc_fence_before();
+    fence_async_smem();
+    bar_half(h);
+    PMARK(4);
+
+    // ============================ layer 3: q = h2 . W3'^T (N = 112)
+    if (ht == 0) issue_layer(0, kTcN3, w3h, w3l, kTcN3 * 16, kTcH / 16, id112);
+    // this thread's reward loads while layer 3 runs
+    uint32_t rwv[kMaxCI][8];
+    {
+      const float* rw = a.rtabf + (size_t)(fmask ? inf[RI_RR] : 0) * RJ;
+#pragma unroll
+      for (int i = 0; i < kMaxCI; ++i) {
+        if ((fmask >> (8 * i)) & 0xffu) {
+          ldg256(rw + 8 * (g + 4 * i), rwv[i]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) rwv[i][k] = 0u;
+        }
+      }
+    }
+    mbar_wait(bar, phase);
+    PMARK(5);
+    phase ^= 1;
+    tc_fence_after();
+
+    // ============================ S: scores, argmax, margin (row, group)
+    {
+      float v1 = -INFINITY, v2 = -INFINITY;
+      int i1 = -1;
+      bool bad = false;
+      if (qact) {
+#pragma unroll
+        for (int i0 = 0; i0 < kMaxCI; i0 += 2) {
+          if (i0 >= ni) break;  // warp-uniform
+          uint32_t vh[2][8], vx[2][8];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (i0 + u < ni) {
+              ld8s(tmem + tl + 16 * p2 + 32 * (i0 + u), vh[u]);
+              ld8s(tmem + tl + kTcN3 + 16 * p2 + 32 * (i0 + u), vx[u]);
+            }
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int i = i0 + u;
+            if (i >= ni) break;
+            const int j0 = 8 * (g + 4 * i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (!((fmask >> (8 * i + k)) & 1u)) continue;  // feasible implies node < J
+              const float qv = fmaf(__uint_as_float(vx[u][k]), kLoInv, __uint_as_float(vh[u][k])) + sB3[j0 + k];
+              const float sc = __uint_as_float(rwv[i][k]) - qv;
+              if (!isfinite(sc)) bad = true;
+              if (sc > v1) { v2 = v1; v1 = sc; i1 = j0 + k; }
+              else if (sc > v2) v2 = sc;
+            }
+          }
+        }
+      }
+      float* bs = sBest + R * 12 + g * 3;
+      bs[0] = v1;
+      bs[1] = __int_as_float(bad ? -2 : i1);
+      bs[2] = v2;
+    }
+    tc_fence_before();
+    bar_half(h);
+    PMARK(6);
+    if (agent) {  // combine the groups
+      inf[RI_FLAG] = 0;
+      if (inf[RI_POS] >= inf[RI_END]) {
+        inf[RI_ANY] = -1;
+      } else {
+        const float* bs = sBest + R * 12;
+        float v1 = bs[0], v2 = bs[2];
+        int i1 = __float_as_int(bs[1]);
+        bool bad = i1 == -2;
+#pragma unroll
+        for (int gg = 1; gg < 4; ++gg) {
+          const float w1 = bs[3 * gg], w2 = bs[3 * gg + 2];
+          const int j1 = __float_as_int(bs[3 * gg + 1]);
+          bad |= j1 == -2;
+          if (w1 > v1 || (w1 == v1 && j1 >= 0 && (i1 < 0 || j1 < i1))) { v2 = fmaxf(v1, w2); v1 = w1; i1 = j1; }
+          else v2 = fmaxf(v2, w1);
+        }
+        if (i1 == -1 && !bad) {  // nothing feasible
+          inf[RI_ANY] = 0;
+          inf[RI_DEC] = -1;
+        } else {
+          inf[RI_ANY] = 1;
+          inf[RI_DEC] = v1 >= 0.f ? i1 : -1;
+          const bool flag = bad || i1 < 0 || !(v1 - v2 >= a.guard) || !(fabsf(v1) >= a.guard);
+          sCnt[CN_TC * kTcRows + R] += 1;
+          if (flag || a.verify) {
+            inf[RI_FLAG] = flag ? 1 : 2;
+            const int k = atomicAdd(&ctl[1], 1);
+            ctl[2 + k] = R;
+          }
+        }
+      }
+    }
+    bar_half(h);
+    PMARK(7);
+
+    // ============================ exact FP64 re-evaluation of flagged rows
+    const int nflag = ctl[1];
+    for (int f = 0; f < nflag; ++f) {
+      const int Rf = ctl[2 + f], rf = Rf - kHalfRows * h;
+      int* caps = (int*)(sAh + kRcInts);
+      int* xrow = caps + kScrJ;
+      int* res = xrow + kScrJ;
+      // the step's capacities (TMEM cap columns) from the row's four threads
+      if ((rf >> 4) == q) {  // warp-uniform
+        for (int i = 0; i < ni; ++i) {
+          uint32_t v[8];
+          ld8s(tmem + tl + kColCap + 16 * p2 + 32 * i, v);
+          tmem_wait_ld();
+          const int j0 = 8 * (g + 4 * i);
+          if (rr == rf && j0 < kScrJ)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) caps[j0 + k] = (int)v[k];
+        }
+      }
+      const int* infF = sInfo + Rf * kInfo;
+      for (int j = ht; j < J; j += kHalfThreads) xrow[j] = S.xloc[(size_t)infF[RI_X] * J + j];
+      bar_half(h);
+      half_recheck(S.model, sAh, caps, xrow, infF[RI_T], res, ht, h);
+      if (ht == 0) {
+        int* infw = sInfo + Rf * kInfo;
+        const int exact = res[0], nonfinite = res[1];
+        if (nonfinite)
+          atomicMin(&S.scal->err_nonfinite, ((unsigned long long)infw[RI_M] << 32) | (unsigned)infw[RI_OT]);
+        if (infw[RI_FLAG] == 1) {
+          ctl[CT_FLAG] += 1;
+          ctl[CT_DIS] += exact != infw[RI_DEC] ? 1 : 0;
+        } else {
+          ctl[CT_BAD] += exact != infw[RI_DEC] ? 1 : 0;
+        }
+        infw[RI_DEC] = exact;
+      }
+      bar_half(h);
+      if (f + 1 == nflag) {
+        // the scratch overlaps K-padding columns of the layer-1 operand when
+        // 2J+1 < kScratchCols: leave zeros behind, as the setup did
+        uint4* zh = (uint4*)sAh;
+        uint4* zl = (uint4*)(sAh + kAH);
+        for (int i = ht; i < kRcScratchHi / 16; i += kHalfThreads) zh[i] = make_uint4(0, 0, 0, 0);
+        for (int i = ht; i < kRcScratchLo / 16; i += kHalfThreads) zl[i] = make_uint4(0, 0, 0, 0);
+        bar_half(h);
+      }
+    }
+    PMARK(8);
+
+    // ============================ U: update + publish (row agents)
+    if (agent) {
+      inf[RI_DRESET] = 0;
+      if (inf[RI_ANY] >= 0) {
+        const int t = inf[RI_T], x = inf[RI_X], dec = inf[RI_DEC];
+        const int uo = inf[RI_UOLD], uxn = inf[RI_UXN];
+        // D deltas are applied by the row's F threads next step
+        inf[RI_EVT] = inf[RI_UEV];
+        inf[RI_XUPD] = dec;
+        if (dec >= 0) atomicSub(&S.xloc[(size_t)x * J + dec], 1);  // fire-and-forget RED
+        int* cn = sCnt + R;
+        if (dec != uo) {
+          cn[CN_CHANGED * kTcRows] += 1;
+          cn[CN_FIRST * kTcRows] = min(cn[CN_FIRST * kTcRows], t);
+          cn[CN_CONFLICTS * kTcRows] += inf[RI_UWR] ? 1 : 0;
+        }
+        if (S.ref) {
+          const int ur = inf[RI_UREF];
+          cn[CN_MISM * kTcRows] += (dec != ur ? 1 : 0) - (uo != ur ? 1 : 0);
+        }
+        S.cache[t] = dec;
+        S.written[t] = 1;
+        cn[CN_NEV * kTcRows] += 1;
+        const int pos = inf[RI_POS] + 1;
+        inf[RI_POS] = pos;
+        if (pos < inf[RI_END]) {
+          inf[RI_T] = inf[RI_TN];
+          inf[RI_XDIRTY] = uxn != x ? 1 : 0;
+          inf[RI_X] = uxn;
+          inf[RI_P] = inf[RI_UPN];
+          inf[RI_RR] = inf[RI_URRN];
+          inf[RI_OT] = inf[RI_UOTN];
+          inf[RI_TN] = inf[RI_UTNN];
+        } else {
+          // process done: its evaluation count, then the next work-list entry
+          const int m = inf[RI_M];
+          const unsigned long long nev = (unsigned)cn[CN_NEV * kTcRows];
+          atomicMax(&S.scal->max_evals, nev);
+          atomicAdd(&S.scal->total_evals, nev);
+          if (S.evals_out) S.evals_out[m] = (long long)nev;
+          cn[CN_NEV * kTcRows] = 0;
+          begin_proc(inf, next_entry());
+        }
+      }
+    }
+    if (ht == kHalfThreads - 1) {
+      ctl[0] = 0;
+      ctl[1] = 0;
+    }
+    bar_half(h);
+    PMARK(9);
+  }
+
+  // ---------------------------------------------------------------- teardown
+  __syncthreads();
+  if (PROF && prof_on)
+    for (int k = 0; k < 17; ++k) a.prof[k] = pacc[k];
+#undef PMARK
+  if (agent) {
+    const int* cn = sCnt + R;
+    if (cn[CN_CHANGED * kTcRows]) {
+      atomicAdd(&S.scal->changed, (unsigned long long)(unsigned)cn[CN_CHANGED * kTcRows]);
+      atomicAdd(&S.scal->conflicts, (unsigned long long)(unsigned)cn[CN_CONFLICTS * kTcRows]);
+      atomicMin(&S.scal->first_changed, (unsigned long long)(unsigned)cn[CN_FIRST * kTcRows]);
+    }
+    const long long mism = cn[CN_MISM * kTcRows];
+    if (mism) atomicAdd((unsigned long long*)&S.scal->mismatch_delta, (unsigned long long)mism);
+    if (cn[CN_TC * kTcRows]) atomicAdd(&a.stats[0], (unsigned long long)(unsigned)cn[CN_TC * kTcRows]);
+  }
+  if (tid == 0) {
+    for (int hh = 0; hh < 2; ++hh) {
+      const int* c = sCtlAll + hh * kCtl;
+      if (c[CT_FLAG]) atomicAdd(&a.stats[1], (unsigned long long)(unsigned)c[CT_FLAG]);
+      if (c[CT_DIS]) atomicAdd(&a.stats[2], (unsigned long long)(unsigned)c[CT_DIS]);
+      if (c[CT_BAD]) atomicAdd(&a.stats[3], (unsigned long long)(unsigned)c[CT_BAD]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+}  // namespace pp
+
+void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+  static bool attr = false;
+  const size_t smem = pp::Layout::total;
+  if (!attr) {
+    cudaFuncSetAttribute(pp::k_sweep_pp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pp::k_sweep_pp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (a.prof)
+    pp::k_sweep_pp<true><<<ntiles, pp::kBlock, smem, stream>>>(a);
+  else
+    pp::k_sweep_pp<false><<<ntiles, pp::kBlock, smem, stream>>>(a);
+}
+
+}  // namespace pcd
