@@ -317,7 +317,10 @@ def main():
                 "iterations": res.iterations_to_converged,
                 "steps_critical": tm["steps_critical"], "total_evals": tm["total_evals"],
                 "us_per_critical_step": 1000.0 * ms_per_step / max(1, tm["steps_critical"]),
-                "phase_ms": {k: tm[k] for k in ("sweep_ms", "prep_ms", "publish_ms", "advance_ms")},
+                "phase_ms": {**{k: tm[k] for k in ("sweep_ms", "prep_ms", "publish_ms", "advance_ms")},
+                             "engine_total_ms": tm["total_ms"],
+                             "host_gap_ms": tm["total_ms"] - sum(tm[k] for k in ("sweep_ms", "prep_ms", "publish_ms",
+                                                                                    "advance_ms"))},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(sum(t["kernel_launches"] for t in timings)),
                 "clocks": clocks.summary()}

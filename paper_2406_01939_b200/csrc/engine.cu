@@ -119,7 +119,7 @@ struct pcd_handle {
   pcd::DBuf<int> wload, wids, wload_s, wq, wctl;  // wctl = {nq, head}
   pcd::DBuf<unsigned char> wtmp;
   // dynamic state
-  pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, scratch, tau;
+  pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, segtot, scratch, tau;
   pcd::DBuf<unsigned char> written;
   pcd::DBuf<long long> evals;
   pcd::Scalars* scal = nullptr;  // device
@@ -405,14 +405,20 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
       hsm_set = hsm;
     }
     k_seg_count<<<nseg, 256, (size_t)J * 4, h->stream>>>(h->ev.p, lo, hi, J, h->seg.p);
-    k_seg_scan<<<J, 256, 0, h->stream>>>(h->seg.p, nseg, J);
+    {
+      const int nblk = std::max(1, std::min(256, nseg));
+      h->segtot.alloc((size_t)nblk * seg_stride(J));
+      k_seg_scan_a<<<nblk, 128, 0, h->stream>>>(h->seg.p, nseg, J, h->segtot.p);
+      k_seg_scan_b<<<seg_stride(J), 256, 0, h->stream>>>(h->segtot.p, nblk, J);
+      k_seg_scan_c<<<nblk, 128, 0, h->stream>>>(h->seg.p, nseg, J, h->segtot.p);
+    }
     k_hist_prefix<<<nseg, 256, hsm, h->stream>>>(h->ev.p, lo, hi, J, nb, h->seg.p, h->hck.p);
     k_tau<<<(J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
     k_xinit<<<pgrid, wpb * 32, (size_t)wpb * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
                                                                  h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
     CK(cudaGetLastError());
     h->timing.prep_ms += tm.stop_ms();
-    h->timing.kernel_launches += 6;
+    h->timing.kernel_launches += 8;
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {

@@ -271,30 +271,45 @@ static __global__ void k_seg_count(const int* __restrict__ ev, int lo, int hi, i
   for (int j = threadIdx.x; j < SJ; j += blockDim.x) seg[(size_t)sg * SJ + j] = j < J ? cs[j] : 0;
 }
 
-// Exclusive scan of the segment totals over segments: one CTA per node j.
-static __global__ void k_seg_scan(int* __restrict__ seg, int nseg, int J) {
-  __shared__ int part[256];
-  const int j = blockIdx.x, SJ = seg_stride(J);
-  const int per = (nseg + blockDim.x - 1) / blockDim.x;
-  const int s0 = threadIdx.x * per, s1 = min(nseg, s0 + per);
-  int sum = 0;
-  for (int s = s0; s < s1; ++s) sum += seg[(size_t)s * SJ + j];
-  part[threadIdx.x] = sum;
+// Exclusive scan of the segment totals over segments, per node: the segments
+// are cut into gridDim.x ranges; thread j of a block walks node j down its
+// range (a row of seg is read coalesced by the block). (a) range totals,
+// (b) one block scans the range totals, (c) ranges apply their offsets.
+static __global__ void k_seg_scan_a(const int* __restrict__ seg, int nseg, int J, int* __restrict__ tot) {
+  const int SJ = seg_stride(J), per = (nseg + gridDim.x - 1) / gridDim.x;
+  const int s0 = blockIdx.x * per, s1 = min(nseg, s0 + per);
+  for (int j = threadIdx.x; j < SJ; j += blockDim.x) {
+    int sum = 0;
+#pragma unroll 8
+    for (int s = s0; s < s1; ++s) sum += seg[(size_t)s * SJ + j];
+    tot[(size_t)blockIdx.x * SJ + j] = sum;
+  }
+}
+// one block per node column, a block-wide scan over the (<= 256) range totals
+static __global__ void k_seg_scan_b(int* __restrict__ tot, int nblk, int J) {
+  __shared__ int sh[256];
+  const int SJ = seg_stride(J), j = blockIdx.x, b = threadIdx.x;
+  const int v = b < nblk ? tot[(size_t)b * SJ + j] : 0;
+  sh[b] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      const int v = part[i];
-      part[i] = acc;
+  for (int off = 1; off < 256; off <<= 1) {
+    const int add = b >= off ? sh[b - off] : 0;
+    __syncthreads();
+    sh[b] += add;
+    __syncthreads();
+  }
+  if (b < nblk) tot[(size_t)b * SJ + j] = sh[b] - v;  // exclusive
+}
+static __global__ void k_seg_scan_c(int* __restrict__ seg, int nseg, int J, const int* __restrict__ tot) {
+  const int SJ = seg_stride(J), per = (nseg + gridDim.x - 1) / gridDim.x;
+  const int s0 = blockIdx.x * per, s1 = min(nseg, s0 + per);
+  for (int j = threadIdx.x; j < SJ; j += blockDim.x) {
+    int acc = tot[(size_t)blockIdx.x * SJ + j];
+    for (int s = s0; s < s1; ++s) {
+      const int v = seg[(size_t)s * SJ + j];
+      seg[(size_t)s * SJ + j] = acc;
       acc += v;
     }
-  }
-  __syncthreads();
-  int acc = part[threadIdx.x];
-  for (int s = s0; s < s1; ++s) {
-    const int v = seg[(size_t)s * SJ + j];
-    seg[(size_t)s * SJ + j] = acc;
-    acc += v;
   }
 }
 

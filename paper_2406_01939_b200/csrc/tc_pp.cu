@@ -389,11 +389,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         xu = inf[RI_XUPD];
         evt = inf[RI_EVT];
         b = (t - base) >> kLogK;
-        ldg256(S.ev + base + (b << kLogK), e8);
+        // streamed rows bypass L1, so the reward table (read every step) stays there
         const int* hr = S.hck + (size_t)b * HJ;
+        ldg256_na(S.ev + base + (b << kLogK), e8);
 #pragma unroll
         for (int i = 0; i < kMaxCI; ++i)
-          if (i < ni && 8 * (g + 4 * i) < J) ldg256(hr + 8 * (g + 4 * i), hv[i]);
+          if (i < ni && 8 * (g + 4 * i) < J) ldg256_na(hr + 8 * (g + 4 * i), hv[i]);
         if (!xd && my_ci(xu) >= 0) {
           xuv = S.xloc[(size_t)x * J + xu];
           xui = __ldg(a.inv_x0 + (size_t)p * J + xu);
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 #pragma unroll
       for (int i = 0; i < kMaxCI; ++i) {
         if ((fmask >> (8 * i)) & 0xffu) {
-          ldg256(rw + 8 * (g + 4 * i), rwv[i]);
+          ldg256_el(rw + 8 * (g + 4 * i), rwv[i]);
         } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k) rwv[i][k] = 0u;
@@ -749,6 +750,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         const int pos = inf[RI_POS] + 1;
         inf[RI_POS] = pos;
         if (pos < inf[RI_END]) {
+          {  // warm L2 with the next step's checkpoint row and event block
+            const int bn = (inf[RI_TN] - base) >> kLogK;
+            const int* hbn = S.hck + (size_t)bn * HJ;
+            for (int k = 0; k < HJ; k += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(hbn + k));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(S.ev + base + (bn << kLogK)));
+          }
           inf[RI_T] = inf[RI_TN];
           inf[RI_XDIRTY] = uxn != x ? 1 : 0;
           inf[RI_X] = uxn;

@@ -144,6 +144,19 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t* r) {
                : "l"(p));
 }
 
+// ... without allocating in L1 (streamed checkpoint rows / event blocks)
+__device__ __forceinline__ void ldg256_na(const void* p, uint32_t* r) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+// ... kept in L1 (the reward table, re-read by every step)
+__device__ __forceinline__ void ldg256_el(const void* p, uint32_t* r) {
+  asm volatile("ld.global.nc.L1::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+
 __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
   hi = __float2half_rn(x);
   lo = __float2half_rn((x - __half2float(hi)) * kLoScale);
