@@ -6,8 +6,12 @@ Workload (default "c3", BASELINE.json configs[2], the north-star target and the
 largest config; it fits one B200): SCO with J=100 nodes, I=10^4 products,
 T=10^7 orders (generate_instance recipe, seed 7, beta 0, coverage 0.8, the
 seeded synthetic 100-node geometry), dual-price MLP policy {201,64,64,200}
-with theta seed 5, M=65536 processes under make_product_partition (seed 1),
-max_steps = 300*M (whole horizon, cli.cpp:225-227). One "step" = one full
+with theta seed 5, M=65536 processes, max_steps = 300*M (whole horizon,
+cli.cpp:225-227). Partition (--partition): "chunk" (default) =
+make_product_chunk_partition(M): every product's orders cut into contiguous
+chunks, one process each, so all 65536 processes carry work; "product" = the
+reference's make_product_partition(M, seed 1), which activates only I=10^4 of
+them. Both reach the same (serial) trajectory. One "step" = one full
 picard_simulate to convergence. Synthetic data, random-init weights.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -189,7 +193,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
-    ap.add_argument("--partition", default="product", choices=sorted(PARTITIONS))
+    ap.add_argument("--partition", default="chunk", choices=sorted(PARTITIONS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -9,6 +9,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -37,21 +39,81 @@ size_t tc_smem_bytes();
       throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x);   \
   } while (0)
 
+// Process-wide caching allocator (per device): one-shot API calls create and
+// destroy a handle each time; recycling the device blocks (~1.5 GB at C3)
+// keeps cudaMalloc / cudaFree (and their implicit device syncs) out of the
+// end-to-end path. Blocks are only returned here when no work of their
+// stream is pending (handles sync before destroy; growth syncs the device).
+struct DevicePool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free;
+  void* get(size_t bytes, size_t* got) {
+    bytes = (bytes + 511) & ~(size_t)511;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free.lower_bound({dev, bytes});
+      if (it != free.end() && it->first.first == dev && it->first.second <= 2 * bytes + (1 << 20)) {
+        void* p = it->second;
+        *got = it->first.second;
+        free.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {  // release the cache and retry once
+      cudaGetLastError();
+      trim(dev);
+      CK(cudaMalloc(&p, bytes));
+    }
+    *got = bytes;
+    return p;
+  }
+  void put(void* p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    free.insert({{dev, bytes}, p});
+  }
+  void trim(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = free.begin(); it != free.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        it = free.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+};
+static DevicePool g_pool;
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
-  size_t n = 0;
+  size_t n = 0;       // elements requested
+  size_t bytes = 0;   // block size
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() { if (p) cudaFree(p); }
-  void alloc(size_t count) {
-    if (count <= n && p) return;
-    if (p) cudaFree(p);
+  ~DBuf() { release(); }
+  void release() {
+    if (p) g_pool.put(p, bytes);
     p = nullptr;
     n = 0;
+    bytes = 0;
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    if (p) {  // growth: the old block may still be read by queued work
+      cudaDeviceSynchronize();
+      release();
+    }
     if (count == 0) return;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    p = (T*)g_pool.get(count * sizeof(T), &bytes);
     n = count;
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
@@ -111,7 +173,6 @@ struct pcd_handle {
   // plan
   int32_t M = 0;
   bool have_plan = false, is_product = false;
-  std::vector<int32_t> h_owner;
   pcd::DBuf<int> owner, pstart, pslots, qstart, qslots;
   pcd::DBuf<int> rid;     // run of every slot (run partitions)
   int64_t runs = 0;       // R
@@ -185,6 +246,19 @@ static int grid_for(long long n, int block, int cap = 148 * 16) {
 }
 
 // Builds a time-ordered CSR of slot indices keyed by `keys` (owner or product).
+// first index t with a[t] outside [lo, hi) (device-side input validation), -1 if none
+static long long first_out_of_range(pcd_handle* h, const int* a, int64_t n, int lo, int hi) {
+  if (n <= 0) return -1;
+  DBuf<unsigned long long> first;
+  first.alloc(1);
+  CK(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), h->stream));
+  k_first_out_of_range<<<grid_for(n, 256), 256, 0, h->stream>>>(a, n, lo, hi, first.p);
+  unsigned long long r = ~0ull;
+  CK(cudaMemcpyAsync(&r, first.p, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return r == ~0ull ? -1 : (long long)r;
+}
+
 static void build_csr(pcd_handle* h, const int* d_keys, int nkeys, DBuf<int>& start, DBuf<int>& slots) {
   const int64_t T = h->T;
   start.alloc((size_t)nkeys + 1);
@@ -647,12 +721,7 @@ static void validate_instance(const pcd_instance* in) {
   if (in->horizon > 0 && (!in->product || !in->reward_row || !in->reward_table))
     throw InvalidArgument("instance arrays missing");
   if (!in->capacity || !in->inventory) throw InvalidArgument("instance state missing");
-  for (int64_t t = 0; t < in->horizon; ++t) {
-    if (in->product[t] < 0 || in->product[t] >= in->products)
-      throw InvalidArgument("order product out of range at t=" + std::to_string(t));
-    if (in->reward_row[t] < 0 || in->reward_row[t] >= in->reward_rows)
-      throw InvalidArgument("reward row out of range at t=" + std::to_string(t));
-  }
+  // per-order range checks run on the device after the upload (pcd_create)
   for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i)
     if (!std::isfinite(in->reward_table[i])) throw InvalidArgument("rewards must be finite");
 }
@@ -663,11 +732,17 @@ static void rebuild_shards(pcd_handle* h) {
   if (!h->have_plan) return;
   const int32_t M = h->M;
   const int64_t T = h->T;
-  const std::vector<int32_t>& owner = h->h_owner;
+  // per-process loads from the owned-slot CSR (device)
+  std::vector<int32_t> pst((size_t)M + 1);
+  CK(cudaMemcpyAsync(pst.data(), h->pstart.p, sizeof(int32_t) * ((size_t)M + 1), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   std::vector<int64_t> load((size_t)M, 0);
-  for (int64_t t = 0; t < T; ++t) load[(size_t)owner[(size_t)t]] += 1;
+  for (int32_t m = 0; m < M; ++m) load[(size_t)m] = pst[(size_t)m + 1] - pst[(size_t)m];
   h->rank_of.assign((size_t)M, 0);
   if (h->comm) {
+    std::vector<int32_t> owner((size_t)std::max<int64_t>(T, 1));
+    if (T) CK(cudaMemcpy(owner.data(), h->owner.p, sizeof(int32_t) * (size_t)T, cudaMemcpyDeviceToHost));
     shard_processes(owner.data(), T, M, h->nranks, h->rank_of.data());
     std::vector<unsigned char> mine((size_t)M);
     for (int32_t m = 0; m < M; ++m) mine[(size_t)m] = h->rank_of[(size_t)m] == h->rank;
@@ -795,6 +870,14 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
   h->product.upload(in->product, T, s);
   if (in->order_t) h->order_t.upload(in->order_t, T, s);
   h->rrow.upload(in->reward_row, T, s);
+  if (in->reward_rows > 0x7fffffffLL) throw InvalidArgument("too many reward rows");
+  {  // per-order range checks (first offending t, product before reward row)
+    const long long bp = first_out_of_range(h.get(), h->product.p, h->T, 0, h->I);
+    const long long br = first_out_of_range(h.get(), h->rrow.p, h->T, 0, (int)h->R);
+    if (bp >= 0 && (br < 0 || bp <= br))
+      throw InvalidArgument("order product out of range at t=" + std::to_string(bp));
+    if (br >= 0) throw InvalidArgument("reward row out of range at t=" + std::to_string(br));
+  }
   h->rtab.upload(in->reward_table, (size_t)h->R * J, s);
   h->cap0.upload(in->capacity, J, s);
   h->inv0.upload(in->inventory, IJ, s);
@@ -846,6 +929,7 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
 extern "C" void pcd_destroy(pcd_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);  // buffers go back to the pool idle
   delete h;
 }
 
@@ -856,11 +940,12 @@ extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
   // PartitionPlan::validate (engine.hpp:82-95)
   if (M < 1) throw ContractViolation("partition plan: process count must be >= 1");
   if (h->T > 0 && !owner) throw ContractViolation("partition plan does not cover the horizon");
-  for (int64_t t = 0; t < h->T; ++t)
-    if (owner[t] < 0 || owner[t] >= M) throw ContractViolation("partition plan: owner out of range", t);
-  h->M = M;
-  h->h_owner.assign(owner, owner + h->T);
   h->owner.upload(owner, (size_t)h->T, h->stream);
+  {
+    const long long bad = first_out_of_range(h, h->owner.p, h->T, 0, M);
+    if (bad >= 0) throw ContractViolation("partition plan: owner out of range", bad);
+  }
+  h->M = M;
   build_csr(h, h->owner.p, M, h->pstart, h->pslots);
   build_csr(h, h->product.p, h->I, h->qstart, h->qslots);
   // runs along the product slot lists (kernels.cuh: k_run_starts / k_run_ids /
@@ -909,9 +994,7 @@ static void upload_cache_ref(pcd_handle* h, const int32_t* initial_cache, const 
     h->ref.alloc(std::max<size_t>(T, 1));
     CK(cudaMemcpyAsync(h->ref.p, reference, T * 4, cudaMemcpyHostToDevice, h->stream));
   } else if (h->ref.p) {
-    cudaFree(h->ref.p);
-    h->ref.p = nullptr;
-    h->ref.n = 0;
+    h->ref.release();
   }
   CK(cudaGetLastError());
 }
@@ -1063,7 +1146,11 @@ extern "C" int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* poli
   product_partition(prod.data(), h->T, h->I, M, 1, owner.data());
   // save / restore any user plan
   const bool had = h->have_plan;
-  std::vector<int32_t> saved = h->h_owner;
+  std::vector<int32_t> saved;
+  if (had) {
+    saved.resize((size_t)h->T);
+    if (h->T) CK(cudaMemcpy(saved.data(), h->owner.p, sizeof(int32_t) * (size_t)h->T, cudaMemcpyDeviceToHost));
+  }
   const int32_t savedM = h->M;
   int rc = pcd_set_plan(h, owner.data(), M);
   if (rc) return rc;

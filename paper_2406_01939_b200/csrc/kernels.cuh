@@ -661,6 +661,12 @@ static __global__ void k_window_evals(const int* __restrict__ pstart, const int*
   out[m] = lower_bound_i32(pslots + beg, n, hi) - lower_bound_i32(pslots + beg, n, lo);
 }
 
+static __global__ void k_first_out_of_range(const int* __restrict__ a, long long n, int lo, int hi,
+                                            unsigned long long* first) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    if (a[t] < lo || a[t] >= hi) atomicMin(first, (unsigned long long)t);
+}
+
 static __global__ void k_iota(int* p, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = (int)i;
 }
