@@ -98,6 +98,16 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   hi = *(const uint32_t*)&hh;
   lo = *(const uint32_t*)&l;
 }
+// tanh(z) = 1 - 2/(1 + e^{2z}): MUFU ex2 and rcp, one Newton step on the
+// reciprocal (~1e-7 absolute; the verify-mode tests bound the end-to-end margin)
+__device__ __forceinline__ float tanh_mufu(float z) {
+  z = fminf(fmaxf(z, -9.f), 9.f);  // NaN propagates (a non-finite score is flagged)
+  const float d = 1.f + exp2f_approx(2.8853900817779268f * z);
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
+  y = y * fmaf(-d, y, 2.f);
+  return fmaf(-2.f, y, 1.f);
+}
 __device__ __forceinline__ void put_feature(unsigned char* sAh, int off, float v) {
   __half hh, l;
   split_f16(v, hh, l);
@@ -525,7 +535,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
     // ============================ layer 1: z1 = F . W1^T (three products)
     if (ht == 0) issue_layer(0, 64, w1h, w1l, kTcH * 16, kTcK1 / 16, id64);
-    mbar_wait(bar, phase);
+    if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
+    bar_half(h);
     PMARK(1);
     phase ^= 1;
     tc_fence_after();
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
           const float z0 = fmaf(__uint_as_float(vx[i][k]), kLoInv, __uint_as_float(vh[i][k])) + bias[u0 + k];
           const float z1 =
               fmaf(__uint_as_float(vx[i][k + 1]), kLoInv, __uint_as_float(vh[i][k + 1])) + bias[u0 + k + 1];
-          split2(tanh_f32(z0), tanh_f32(z1), ph[k / 2], pl[k / 2]);
+          split2(tanh_mufu(z0), tanh_mufu(z1), ph[k / 2], pl[k / 2]);
         }
         const int off = rowo + kc64(u0);
         *(uint4*)(sAh + off) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
@@ -565,7 +576,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
     // ============================ layer 2
     if (ht == 0) issue_layer(128, 64, w2h, w2l, kTcH * 16, kTcH / 16, id64);
-    mbar_wait(bar, phase);
+    if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
+    bar_half(h);
     PMARK(3);
     phase ^= 1;
     tc_fence_after();
@@ -591,7 +603,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         }
       }
     }
-    mbar_wait(bar, phase);
+    if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
+    bar_half(h);
     PMARK(5);
     phase ^= 1;
     tc_fence_after();
