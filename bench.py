@@ -64,26 +64,58 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region through NVML
+    (in-process, every 0.2 s; nvidia-smi's CLI is the fallback: forking it every
+    sample adds host stalls to the measured region)."""
 
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, [reason names])
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                bus = torch.cuda.get_device_properties(index).pci_bus_id
+                pci = f"00000000:{bus:02x}:00.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(pci)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nv = (pynvml, h)
+        except Exception:
+            self._nv = None
+
+    def _sample(self):
+        if self._nv:
+            nv, h = self._nv
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return float(sm), float(mx), [n for n, b in self.REASONS if bits & b]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        r = [x.strip() for x in out.split(",")]
+        names = [n for n, _ in self.REASONS]
+        return (float(r[0]), float(r[1]), [n for n, v in zip(names, r[3:7]) if v.lower() == "active"])
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self.rows.append(self._sample())
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -99,13 +131,10 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"]}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({n for r in self.rows for n in r[2]}), "samples": len(self.rows),
+                "source": "nvml" if self._nv else "nvidia-smi"}
 
 
 PARTITIONS = {
@@ -265,11 +294,26 @@ def main():
     mlp_evals = tm["tc_rows"] if tc else tm["total_evals"]
     achieved_tflops = mlp_evals * F / (sweep_ms / 1000.0) / 1e12 if sweep_ms > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    # DRAM traffic of the sweep from the committed ncu --set full capture
+    # (profiles/r01_ncu_sweep_pp.json: bytes per policy evaluation) x this
+    # run's evaluations per launch
+    traffic, hbm_view = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_sweep_pp.json")) as f:
+            prof = json.load(f)
+        per_launch_evals = mlp_evals / max(1, tm["sweep_launches"])
+        traffic = prof["dram_bytes_per_eval"] * per_launch_evals
+        gbs = traffic / (sweep_ms / max(1, tm["sweep_launches"]) / 1000.0) / 1e9
+        hbm_view = {"achieved_gbs": gbs, "peak_gbs": peaks.get("hbm_gbs"),
+                    "frac": gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
+                    "source": "profiles/r01_ncu_sweep_pp.json (dram bytes / evaluation) x evaluations / launch"}
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved_tflops / peak, "traffic": None,
-                "kernel": ("k_sweep_product_tc (tcgen05.mma kind::f16, fp16x3 split, TMEM accumulators; "
-                           "FP64 exact re-evaluation of rows with margin < guard)") if tc else
-                          "k_sweep_product<kDual> (FP64 SIMT, exact op order)",
+                "frac": achieved_tflops / peak, "traffic": traffic, "hbm_view": hbm_view,
+                "kernel": ("pp::k_sweep_pp (tc_pp.cu: two 64-row halves per SM, tcgen05.mma kind::f16 M=64 "
+                           "fp16x3 split, TMEM accumulators; FP64 exact re-evaluation of rows with margin "
+                           "< guard)") if tc else "k_sweep_product<kDual> (FP64 SIMT, exact op order)",
                 "per_launch": {"launches": tm["sweep_launches"], "avg_ms": sweep_ms / max(1, tm["sweep_launches"]),
                                "flops_per_eval": F, "mlp_evals": mlp_evals,
                                "algorithmic_flops_per_launch": mlp_evals * F / max(1, tm["sweep_launches"]),
@@ -279,8 +323,9 @@ def main():
                              "fp16x3_wrong_when_flagged": tm["tc_disagree"], "tiles": tm["tc_tiles"]},
                 "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json; fp16 dense = bf16)",
                 "note": "algorithmic FLOPs = MLP evaluations x (512J+8320); the fp16x3 split issues 3x "
-                        "these MACs. The sweep is a latency-bound lockstep of `critical_steps` dependent "
-                        "policy steps (128-row MMA tiles), not a throughput GEMM"}
+                        "these MACs. Neither roofline binds: each SM runs two 64-row pipelines of dependent "
+                        "policy steps (feature build -> 3 MMAs -> argmax) whose latency chains, not tensor "
+                        "or HBM throughput, set the step time (ncu: ~39% issue-active, tensor pipe ~16%)"}
 
     # ---- e2e through the public one-shot API from pinned host memory
     e2e = None
