@@ -452,7 +452,8 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     CK(cudaStreamSynchronize(h->stream));
     fprintf(stderr, "tcprof steps=%lld F=%lld(own %lld) L1=%lld E1=%lld L2=%lld E2=%lld L3=%lld S=%lld fin=%lld chk=%lld U=%lld\n",
             v[10], v[0], v[11], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
-    fprintf(stderr, "tcprof F: loads=%lld feat=%lld x=%lld\n", v[12], v[13], v[14]);
+    fprintf(stderr, "tcprof F: loads=%lld feat=%lld x=%lld | recheck feat=%lld L1=%lld L2=%lld L3=%lld score=%lld\n",
+            v[12], v[13], v[14], v[15], v[16], v[17], v[18], v[19]);
   }
 }
 

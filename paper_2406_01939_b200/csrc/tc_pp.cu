@@ -138,13 +138,14 @@ constexpr int kScratchCols = ((kRcScratchHi > kRcScratchLo ? kRcScratchHi : kRcS
 __device__ void rc_layer(const double* __restrict__ W, const double* __restrict__ bias, int K, int width,
                          const double* xin, double* outv, bool act_tanh, int tanh_fma, int ht, int h) {
   if (ht < width) {
+    const uint64_t pol = l2_policy_evict_last();  // the FP64 weights stay L2-resident
     double acc = __ldg(bias + ht);
     const double* w = W + ht;
     int c = 0;
     for (; c + 16 <= K; c += 16) {
       double wv[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) wv[u] = __ldg(w + (size_t)(c + u) * width);
+      for (int u = 0; u < 16; ++u) wv[u] = ldg_f64_el(w + (size_t)(c + u) * width, pol);
 #pragma unroll
       for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, __dmul_rn(wv[u], xin[c + u]));
     }
@@ -156,7 +157,11 @@ __device__ void rc_layer(const double* __restrict__ W, const double* __restrict_
 
 // res[0] = exact decision, res[1] = non-finite score flag
 __device__ void half_recheck(const DevModel& P, unsigned char* sAh, const int* caps, const int* xrow, int t,
-                             int* res, int ht, int h) {
+                             int* res, int ht, int h, long long* rprof = nullptr) {
+  long long t0 = rprof ? clock64() : 0;
+  auto mark = [&](int k) {
+    if (rprof) { const long long n = clock64(); rprof[k] += n - t0; t0 = n; }
+  };
   const int J = P.J, H = P.H, in = P.in, out = P.out;
   double* vec = (double*)(sAh + kAH);
   for (int j = ht; j < in; j += kHalfThreads) {
@@ -174,10 +179,14 @@ __device__ void half_recheck(const DevModel& P, unsigned char* sAh, const int* c
     vec[j] = f;
   }
   bar_half(h);
+  mark(0);
   const int oh1 = 2 * kMaxJ + 2, oh2 = oh1 + kTcH, opr = oh2 + kTcH;
   rc_layer(P.w1t, P.b1, in, H, vec, vec + oh1, true, P.tanh_fma, ht, h);
+  mark(1);
   rc_layer(P.w2t, P.b2, H, H, vec + oh1, vec + oh2, true, P.tanh_fma, ht, h);
+  mark(2);
   rc_layer(P.w3t, P.b3, H, out, vec + oh2, vec + opr, false, P.tanh_fma, ht, h);
+  mark(3);
   if (ht < 32) {  // scores and argmax as warp_policy_eval<kDual>
     const int lane = ht;
     const double* rw = P.rtab + (size_t)P.rrow[t] * J;
@@ -208,6 +217,7 @@ __device__ void half_recheck(const DevModel& P, unsigned char* sAh, const int* c
     }
   }
   bar_half(h);
+  mark(4);
 }
 
 template <bool PROF>
@@ -400,11 +410,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         evt = inf[RI_EVT];
         b = (t - base) >> kLogK;
         // streamed rows bypass L1, so the reward table (read every step) stays there
+        // (and leave L2 first: read about once per iteration)
         const int* hr = S.hck + (size_t)b * HJ;
-        ldg256_na(S.ev + base + (b << kLogK), e8);
+        const uint64_t pol = l2_policy_evict_first();
+        ldg256_na_ef(S.ev + base + (b << kLogK), e8, pol);
 #pragma unroll
         for (int i = 0; i < kMaxCI; ++i)
-          if (i < ni && 8 * (g + 4 * i) < J) ldg256_na(hr + 8 * (g + 4 * i), hv[i]);
+          if (i < ni && 8 * (g + 4 * i) < J) ldg256_na_ef(hr + 8 * (g + 4 * i), hv[i], pol);
         if (!xd && my_ci(xu) >= 0) {
           xuv = S.xloc[(size_t)x * J + xu];
           xui = __ldg(a.inv_x0 + (size_t)p * J + xu);
@@ -710,7 +722,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
       const int* infF = sInfo + Rf * kInfo;
       for (int j = ht; j < J; j += kHalfThreads) xrow[j] = S.xloc[(size_t)infF[RI_X] * J + j];
       bar_half(h);
-      half_recheck(S.model, sAh, caps, xrow, infF[RI_T], res, ht, h);
+      half_recheck(S.model, sAh, caps, xrow, infF[RI_T], res, ht, h, (PROF && prof_on) ? pacc + 15 : nullptr);
       if (ht == 0) {
         int* infw = sInfo + Rf * kInfo;
         const int exact = res[0], nonfinite = res[1];
@@ -799,7 +811,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   // ---------------------------------------------------------------- teardown
   __syncthreads();
   if (PROF && prof_on)
-    for (int k = 0; k < 17; ++k) a.prof[k] = pacc[k];
+    for (int k = 0; k < 20; ++k) a.prof[k] = pacc[k];
 #undef PMARK
   if (agent) {
     const int* cn = sCnt + R;
