@@ -775,8 +775,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         const int pos = inf[RI_POS] + 1;
         inf[RI_POS] = pos;
         if (pos < inf[RI_END]) {
-          {  // warm L2 with the next step's checkpoint row and event block
-            const int bn = (inf[RI_TN] - base) >> kLogK;
+          const int tp = inf[RI_UTNN];
+          if (tp >= 0) {  // warm L2 with the checkpoint row and event block of the step after next
+            const int bn = (tp - base) >> kLogK;
             const int* hbn = S.hck + (size_t)bn * HJ;
             for (int k = 0; k < HJ; k += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(hbn + k));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(S.ev + base + (bn << kLogK)));
