@@ -36,6 +36,8 @@ struct DevModel {
   const int* order_t;  // [T] or nullptr
   const int* rrow;     // [T]
   const double* rtab;  // [R*J]
+  const double* w3s;   // [H][J] W3[j] + W3[J+j] (transposed) for the order-free recheck, or nullptr
+  double fast_margin;  // decision margin above which the order-free FP64 recheck is exact (0 = off)
 };
 
 // ---------------------------------------------------------------- glibc tanh

@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <cstdio>
@@ -168,7 +169,8 @@ struct pcd_handle {
   int kind = 0, H = 64;
   double gamma = 0.0;
   int64_t p_horizon = 0;
-  pcd::DBuf<double> w1t, b1, w2t, b2, w3t, b3;
+  pcd::DBuf<double> w1t, b1, w2t, b2, w3t, b3, w3s;
+  double fast_margin = 0.0;  // see fast_margin_bound
   pcd::DBuf<int> pcap0, pinv0;
   // plan
   int32_t M = 0;
@@ -214,6 +216,8 @@ struct pcd_handle {
     m.w1t = w1t.p; m.b1 = b1.p; m.w2t = w2t.p; m.b2 = b2.p; m.w3t = w3t.p; m.b3 = b3.p;
     m.pcap0 = pcap0.p; m.pinv0 = pinv0.p; m.horizon = p_horizon; m.tanh_fma = tanh_fma;
     m.product = product.p; m.order_t = order_t.p; m.rrow = rrow.p; m.rtab = rtab.p;
+    m.w3s = w3s.n ? w3s.p : nullptr;
+    m.fast_margin = fast_margin;
     return m;
   }
   ~pcd_handle() {
@@ -800,6 +804,44 @@ static void exchange(pcd_handle* h, int* buf, bool reduce) {
   h->timing.kernel_launches += reduce ? 4 : 2;
 }
 
+// Rounding bound E between two FP64 evaluations of the dual network's scores
+// that differ only in summation order / FMA use (the reference's ordered
+// acc = b; acc += w*x vs the order-free recheck), for features in [0, 1]:
+//   layer 1: |dz1| <= 2 g(in+1) S1,                 S1 = max_n |b1| + sum|W1[n]|
+//   h1:      |dh1| <= |dz1| + 2u                    (tanh 1-Lipschitz, <= 1 ulp each)
+//   layer 2: |dz2| <= A2 |dh1| + 2 g(H+1) S2,       A2 = max_n sum|W2[n]|
+//   score:   |ds|  <= A3 |dh2| + 2 g(H+2) S3 + 4u (|r| + S3)
+// with g(n) = n u / (1 - n u), u = 2^-53; the fast path needs both decision
+// margins above 4E (pp::half_recheck). Returns 4E, or 0 (fast path off) when
+// the bound is not small.
+static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax) {
+  const int in = 2 * J + 1, out = 2 * J;
+  const double u = std::ldexp(1.0, -53);
+  auto g = [&](double n) { return n * u / (1.0 - n * u); };
+  double S1 = 0, A2 = 0, S2 = 0, A3 = 0, S3 = 0;
+  for (int n = 0; n < H; ++n) {
+    double a = std::fabs(pol->b1[n]);
+    for (int c = 0; c < in; ++c) a += std::fabs(pol->w1[(size_t)n * in + c]);
+    S1 = std::max(S1, a);
+    double b = 0;
+    for (int c = 0; c < H; ++c) b += std::fabs(pol->w2[(size_t)n * H + c]);
+    A2 = std::max(A2, b);
+    S2 = std::max(S2, b + std::fabs(pol->b2[n]));
+  }
+  for (int j = 0; j < J; ++j) {
+    double a = 0;
+    for (int l = 0; l < H; ++l) a += std::fabs(pol->w3[(size_t)j * H + l]) + std::fabs(pol->w3[(size_t)(J + j) * H + l]);
+    A3 = std::max(A3, a);
+    S3 = std::max(S3, a + std::fabs(pol->b3[j]) + std::fabs(pol->b3[J + j]));
+  }
+  (void)out;
+  const double dz1 = 2 * g(in + 1) * S1, dh1 = dz1 + 2 * u;
+  const double dz2 = A2 * dh1 + 2 * g(H + 1) * S2, dh2 = dz2 + 2 * u;
+  const double ds = A3 * dh2 + 2 * g(H + 2) * S3 + 4 * u * (rmax + S3);
+  const double m = 4 * ds;
+  return (std::isfinite(m) && m < 1e-6) ? std::max(m, 1e-13) : 0.0;
+}
+
 // Weight images for the tcgen05 sweep (tc_sweep.cuh): fp16 hi + 2^11-scaled lo
 // parts in the canonical K-major no-swizzle UMMA layout, W3' = W3[:J] + W3[J:]
 // (the score needs only p_j + p_{J+j}), fp32 biases and feature reciprocals.
@@ -900,6 +942,17 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
     upload_t(pol->w1, H, inw, h->w1t);
     upload_t(pol->w2, H, H, h->w2t);
     upload_t(pol->w3, outw, H, h->w3t);
+    {  // W3s[l][j] = W3[j][l] + W3[J+j][l]: summed prices for the order-free recheck
+      const int Jn = h->J;
+      std::vector<double> w3s((size_t)H * Jn);
+      for (int l = 0; l < H; ++l)
+        for (int j = 0; j < Jn; ++j)
+          w3s[(size_t)l * Jn + j] = pol->w3[(size_t)j * H + l] + pol->w3[(size_t)(Jn + j) * H + l];
+      h->w3s.upload(w3s.data(), w3s.size(), s);
+      double rmax = 0;
+      for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i) rmax = std::max(rmax, std::fabs(in->reward_table[i]));
+      h->fast_margin = fast_margin_bound(pol, Jn, H, rmax);
+    }
     h->b1.upload(pol->b1, H, s);
     h->b2.upload(pol->b2, H, s);
     h->b3.upload(pol->b3, outw, s);
