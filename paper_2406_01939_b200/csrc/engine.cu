@@ -473,7 +473,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     const int J = h->J;
     const int wpb = 8;  // warps (products) per block
     const int pgrid = (h->I + wpb - 1) / wpb;
-    k_effective<<<pgrid, wpb * 32, (size_t)wpb * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi,
+    k_effective<<<pgrid, wpb * 32, (size_t)wpb * 2 * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi,
                                                                      h->cache.p, h->ckinv.p, J, h->ev.p);
     const int nb = hck_rows(lo, hi);
     const int nseg = (nb + kSegRows - 1) / kSegRows;
@@ -493,7 +493,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     }
     k_hist_prefix<<<nseg, 256, hsm, h->stream>>>(h->ev.p, lo, hi, J, nb, h->seg.p, h->hck.p);
     k_tau<<<(J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
-    k_xinit<<<pgrid, wpb * 32, (size_t)wpb * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
+    k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
                                                                  h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
     CK(cudaGetLastError());
     h->timing.prep_ms += tm.stop_ms();

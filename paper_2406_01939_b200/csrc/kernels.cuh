@@ -85,32 +85,41 @@ __device__ __forceinline__ void product_window(const int* __restrict__ qstart, c
 static __global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
                                    int lo, int hi, const int* __restrict__ cache,
                                    const int* __restrict__ ckinv, int J, int* __restrict__ ev) {
-  extern __shared__ int cnt_smem[];
+  extern __shared__ int cnt_smem[];  // per warp: cnt[J], x0[J]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * (blockDim.x >> 5) + warp;
   if (p >= I) return;  // warp-uniform
-  int* cnt = cnt_smem + warp * J;
-  for (int j = lane; j < J; j += 32) cnt[j] = 0;
+  int* cnt = cnt_smem + warp * 2 * J;
+  int* x0 = cnt + J;
+  for (int j = lane; j < J; j += 32) {
+    cnt[j] = 0;
+    x0[j] = ckinv[(size_t)p * J + j];
+  }
   const int* sl;
   int k0, k1;
   product_window(qstart, qslots, p, lo, hi, sl, k0, k1);
-  const int* x0 = ckinv + (size_t)p * J;
   const unsigned lt = (1u << lane) - 1u;
   __syncwarp();
-  for (int b = k0; b < k1; b += 32) {
-    const int k = b + lane;
-    const bool valid = k < k1;
-    const int t = valid ? sl[k] : 0;
-    const int a = valid ? cache[t] : -1;
-    const bool att = valid && a >= 0 && a < J;
-    const unsigned peers = __match_any_sync(0xffffffffu, att ? a : -1);
-    const int rank = __popc(peers & lt);
-    const int c = att ? cnt[a] : 0;
-    const int e = att && c + rank < x0[a] ? a : -1;
-    if (valid) ev[t] = e;
-    __syncwarp();
-    if (att && rank == 0) cnt[a] = c + __popc(peers);
-    __syncwarp();
+  // 64 slots per round, both halves' loads in flight before either is ranked
+  for (int b = k0; b < k1; b += 64) {
+    const int kA = b + lane, kB = b + 32 + lane;
+    const bool vA = kA < k1, vB = kB < k1;
+    const int tA = vA ? sl[kA] : 0, tB = vB ? sl[kB] : 0;
+    const int aA = vA ? cache[tA] : -1, aB = vB ? cache[tB] : -1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool valid = h ? vB : vA;
+      const int t = h ? tB : tA, a = h ? aB : aA;
+      const bool att = valid && a >= 0 && a < J;
+      const unsigned peers = __match_any_sync(0xffffffffu, att ? a : -1);
+      const int rank = __popc(peers & lt);
+      const int c = att ? cnt[a] : 0;
+      const int e = att && c + rank < x0[a] ? a : -1;
+      if (valid) ev[t] = e;
+      __syncwarp();
+      if (att && rank == 0) cnt[a] = c + __popc(peers);
+      __syncwarp();
+    }
   }
 }
 
@@ -151,11 +160,14 @@ static __global__ void k_xinit(const int* __restrict__ qstart, const int* __rest
                                int hi, const int* __restrict__ ev, const int* __restrict__ rid,
                                const int* __restrict__ tau, const int* __restrict__ ckinv, int J,
                                int* __restrict__ xloc) {
-  extern __shared__ int cnt_smem[];
+  extern __shared__ int cnt_smem[];  // tau[J] (block), then cnt[J] per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* stau = cnt_smem;
+  for (int j = threadIdx.x; j < J; j += blockDim.x) stau[j] = tau[j];
+  __syncthreads();
   const int p = blockIdx.x * (blockDim.x >> 5) + warp;
   if (p >= I) return;  // warp-uniform
-  int* cnt = cnt_smem + warp * J;
+  int* cnt = cnt_smem + J + warp * J;
   for (int j = lane; j < J; j += 32) cnt[j] = 0;
   const int* sl;
   int k0, k1;
@@ -163,31 +175,36 @@ static __global__ void k_xinit(const int* __restrict__ qstart, const int* __rest
   const int* x0 = ckinv + (size_t)p * J;
   int prev_run = -1;
   __syncwarp();
-  for (int b = k0; b < k1; b += 32) {
-    const int k = b + lane;
-    const bool valid = k < k1;
-    const int t = valid ? sl[k] : 0;
-    const int e = valid ? ev[t] : -1;
-    const int r = valid ? rid[t] : -1;
-    const bool contrib = e >= 0 && t < tau[e];
-    int pr = __shfl_up_sync(0xffffffffu, r, 1);
-    if (lane == 0) pr = prev_run;
-    unsigned starts = __ballot_sync(0xffffffffu, valid && r != pr);
-    int done = 0;
-    while (starts) {
-      const int L = __ffs(starts) - 1;
-      starts &= starts - 1;
-      if (contrib && lane >= done && lane < L) atomicAdd(&cnt[e], 1);
+  for (int b0 = k0; b0 < k1; b0 += 64) {
+    const int kA = b0 + lane, kB = b0 + 32 + lane;
+    const bool vA = kA < k1, vB = kB < k1;
+    const int tA = vA ? sl[kA] : 0, tB = vB ? sl[kB] : 0;
+    const int eA = vA ? ev[tA] : -1, eB = vB ? ev[tB] : -1;
+    const int rA = vA ? rid[tA] : -1, rB = vB ? rid[tB] : -1;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const bool valid = hh ? vB : vA;
+      const int t = hh ? tB : tA, e = hh ? eB : eA, r = hh ? rB : rA;
+      const bool contrib = e >= 0 && t < stau[e];
+      int pr = __shfl_up_sync(0xffffffffu, r, 1);
+      if (lane == 0) pr = prev_run;
+      unsigned starts = __ballot_sync(0xffffffffu, valid && r != pr);
+      int done = 0;
+      while (starts) {
+        const int L = __ffs(starts) - 1;
+        starts &= starts - 1;
+        if (contrib && lane >= done && lane < L) atomicAdd(&cnt[e], 1);
+        __syncwarp();
+        const int rr = __shfl_sync(0xffffffffu, r, L);
+        int* xr = xloc + (size_t)rr * J;
+        for (int j = lane; j < J; j += 32) xr[j] = x0[j] - cnt[j];
+        __syncwarp();
+        done = L;
+      }
+      if (contrib && lane >= done) atomicAdd(&cnt[e], 1);
+      prev_run = __shfl_sync(0xffffffffu, r, 31);
       __syncwarp();
-      const int rr = __shfl_sync(0xffffffffu, r, L);
-      int* xr = xloc + (size_t)rr * J;
-      for (int j = lane; j < J; j += 32) xr[j] = x0[j] - cnt[j];
-      __syncwarp();
-      done = L;
     }
-    if (contrib && lane >= done) atomicAdd(&cnt[e], 1);
-    prev_run = __shfl_sync(0xffffffffu, r, 31);
-    __syncwarp();
   }
 }
 
