@@ -179,6 +179,13 @@ int64_t pcd_last_error_time_step(void);
 /* Number of CUDA devices visible (0 on a CPU-only host; never fails). */
 int pcd_device_count(void);
 
+/* Page-locked host buffers from a process-wide pool (no reference
+ * counterpart): result arrays allocated here are written by the device at
+ * full PCIe bandwidth and recycled by pcd_host_free instead of being pinned
+ * and unpinned per call. NULL on failure. */
+void* pcd_host_alloc(size_t bytes);
+void pcd_host_free(void* p);
+
 /* ------------------------------------------------------- host-side inputs
  * These run on the host CPU (they are serial-RNG bound and must reproduce the
  * reference's mt19937_64 streams bit for bit). */

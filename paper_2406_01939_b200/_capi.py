@@ -72,6 +72,8 @@ SIGNATURES = {
     "pcd_generate_instance": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_double,
                                         C.c_uint64, C.c_int32, I32P, I32P, F64P, I32P, I32P]),
     "pcd_product_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),
+    "pcd_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "pcd_host_free": (None, [C.c_void_p]),
     "pcd_product_chunk_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),
     "pcd_uniform_partition": (C.c_int, [C.c_int64, C.c_int32, C.c_uint64, I32P]),
     "pcd_seeded_mlp": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_int32,

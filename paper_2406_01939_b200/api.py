@@ -102,6 +102,21 @@ def _i32(a):
     return None if a is None else np.ascontiguousarray(a, dtype=np.int32)
 
 
+def _pinned_i32(n: int) -> np.ndarray:
+    """int32 array in page-locked host memory from the library's pool (the
+    device writes results into it at full bandwidth); the buffer returns to
+    the pool when the array is garbage collected. Falls back to pageable."""
+    import weakref
+    nbytes = max(int(n), 1) * 4
+    ptr = LIB.pcd_host_alloc(nbytes)
+    if not ptr:
+        return np.zeros(max(int(n), 1), np.int32)
+    buf = (C.c_int32 * max(int(n), 1)).from_address(ptr)
+    arr = np.frombuffer(buf, dtype=np.int32)
+    weakref.finalize(buf, LIB.pcd_host_free, C.c_void_p(ptr))
+    return arr
+
+
 # --------------------------------------------------------------- instances
 @dataclass
 class Instance:
@@ -489,7 +504,7 @@ class Simulator:
             raise ContractViolation("initial cache length must equal the horizon")
         if ref is not None and ref.size != T:
             raise ContractViolation("reference action length must equal the horizon")
-        actions = np.zeros(max(T, 1), np.int32)
+        actions = _pinned_i32(T)
         res = K.pcd_result()
         trace, cap = self._trace_buf(config)
         cfg = config.to_c()

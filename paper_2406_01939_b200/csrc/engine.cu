@@ -708,6 +708,37 @@ int translate_exception();  // capi.cpp
   }               \
   catch (...) { return pcd::translate_exception(); }
 
+// pinned host pool (pcd_host_alloc / pcd_host_free)
+static std::mutex g_hmu;
+static std::multimap<size_t, void*> g_hfree;
+static std::map<void*, size_t> g_hsize;
+extern "C" void* pcd_host_alloc(size_t bytes) {
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  {
+    std::lock_guard<std::mutex> lk(g_hmu);
+    auto it = g_hfree.lower_bound(bytes);
+    if (it != g_hfree.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      g_hfree.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_hmu);
+  g_hsize[p] = bytes;
+  return p;
+}
+extern "C" void pcd_host_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_hmu);
+  auto it = g_hsize.find(p);
+  if (it != g_hsize.end()) g_hfree.insert({it->second, p});
+}
+
 extern "C" int pcd_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
