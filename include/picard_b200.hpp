@@ -268,4 +268,20 @@ SequentialOutput<fo::FoAction> sequential_simulate(const fo::FoEnv& env, const P
   return out;
 }
 
+// Product-chunk plan (no reference counterpart; pcd_product_chunk_partition):
+// every product's orders cut into contiguous near-equal chunks, one process
+// each, so up to `processes` processes carry work. A valid PartitionPlan for
+// picard_simulate (same trajectory); falls back to make_product_partition
+// when processes < ordered products.
+inline PartitionPlan make_product_chunk_partition(const fo::FoEnv& env, std::span<const fo::Order> orders,
+                                                  std::int32_t processes, std::uint64_t seed = 1) {
+  auto m = detail::marshal(env, orders);
+  PartitionPlan plan;
+  plan.processes = processes;
+  plan.owner.assign(orders.size(), 0);
+  const int rc = pcd_product_chunk_partition(&m.view, processes, seed, plan.owner.data());
+  if (rc) detail::raise(rc);
+  return plan;
+}
+
 }  // namespace picard::b200

@@ -148,6 +148,26 @@ int main() {
     compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, 5),
             make_uniform_time_partition(inst.horizon, 16, 3), {});
   }
+  // product-chunk plans (b200::make_product_chunk_partition) through the
+  // unmodified reference engine and the B200 engine
+  {
+    const auto inst = generate_instance(30, 200, 6000, -0.3, 0.8, 7);
+    const auto env = inst.make_env();
+    const auto plan = b200::make_product_chunk_partition(env, std::span<const Order>(inst.orders), 900);
+    compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, 5), plan, {});
+    PicardConfig cfg;
+    cfg.max_steps = 700;
+    compare(inst, GreedyPolicy{}, plan, cfg);
+  }
+  for (std::uint64_t seed = 300; seed < 316; ++seed) {
+    const auto inst = small_random(seed);
+    const auto env = inst.make_env();
+    auto gen = rng::make(seed * 31);
+    const auto M = static_cast<std::int32_t>(inst.products + rng::below(gen, 3 * inst.products + 4));
+    const auto plan = b200::make_product_chunk_partition(env, std::span<const Order>(inst.orders), M);
+    compare(inst, CapacityPenalizedPolicy{0.7}, plan, {});
+    if (seed % 2 == 0) compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, seed), plan, {});
+  }
   // iteration cap (test_engine.cpp:525-545)
   {
     const auto inst = toy();
