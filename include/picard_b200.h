@@ -179,6 +179,39 @@ int64_t pcd_last_error_time_step(void);
 /* Number of CUDA devices visible (0 on a CPU-only host; never fails). */
 int pcd_device_count(void);
 
+/* ------------------------------------------------------------------------
+ * Non-SCO environment (picard::linear, linear.hpp / linear.cpp): the
+ * time-varying linear system s_{t+1} = A_t s_t + B_t a_t + w_t under the
+ * linear feedback a_t = G s_t (GainPolicy). Row-major flat arrays:
+ * dynamics[T][n][n], input[T][n][p], disturbances[T][n], gain[p][n]. */
+typedef struct pcd_linear_spec {
+  int32_t state_dim;            /* n (<= 8 on the device) */
+  int32_t input_dim;            /* p */
+  int64_t horizon;              /* T */
+  const double* dynamics;
+  const double* input;
+  const double* disturbances;
+  const double* gain;
+} pcd_linear_spec;
+
+/* make_contractive_spec (linear.cpp:126-218), bit-identical streams: fills
+ * the four arrays and the closed-loop contraction max_t ||A_t + B_t G||_2. */
+int pcd_linear_contractive_spec(int32_t state_dim, int32_t input_dim, int64_t horizon, double rho,
+                                uint64_t seed, double state_coupling, double* dynamics, double* input,
+                                double* disturbances, double* gain, double* contraction);
+
+/* picard_convergence_curve (linear.cpp:279-330) on the device: single-step
+ * partitions (M = T), curve[k] = relative RMSE of the cache-induced state
+ * trajectory after iteration k+1 (normalization 1 = draft, 0 = reference),
+ * stopping once it is <= tolerance or after max_iterations (0 = T).
+ * initial_cache[T][p] or NULL (zero actions). *curve_len = iterations run;
+ * final_cache[T][p] (optional) receives the last cache; *elapsed_ms
+ * (optional) the device time of the iterations. */
+int pcd_linear_convergence_curve(const pcd_linear_spec* spec, const double* initial_cache,
+                                 double tolerance, int64_t max_iterations, int32_t normalization,
+                                 int32_t device, double* curve, int64_t curve_cap, int64_t* curve_len,
+                                 double* final_cache, double* elapsed_ms);
+
 /* Page-locked host buffers from a process-wide pool (no reference
  * counterpart): result arrays allocated here are written by the device at
  * full PCIe bandwidth and recycled by pcd_host_free instead of being pinned

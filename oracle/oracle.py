@@ -320,6 +320,38 @@ class _Lib:
                                            C.byref(it), C.byref(se), C.byref(sec)))
         return actions[:int(inst.horizon)], it.value, se.value, sec.value
 
+    # ---------------------------------------------------------- linear env
+    # (reference harness only: ref_linear_* in ref_harness.cpp)
+    def linear_spec(self, n, p, T, rho, seed, coupling=0.0):
+        A = np.zeros((max(T, 1), n, n)); B = np.zeros((max(T, 1), n, p)); W = np.zeros((max(T, 1), n))
+        G = np.zeros((p, n)); c = C.c_double()
+        self.check(self.fn("linear_spec")(C.c_int32(n), C.c_int32(p), C.c_int64(T), C.c_double(rho),
+                                          C.c_uint64(seed), C.c_double(coupling), _p(A, C.c_double),
+                                          _p(B, C.c_double), _p(W, C.c_double), _p(G, C.c_double), C.byref(c)))
+        return A[:T], B[:T], W[:T], G, c.value
+
+    def linear_curve(self, spec, initial_cache=None, tolerance=1e-3, max_iterations=0, normalization="draft"):
+        n, p, T = spec.state_dim, spec.input_dim, spec.horizon
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (spec.dynamics, spec.input, spec.disturbances, spec.gain)]
+        init = None if initial_cache is None else np.ascontiguousarray(initial_cache, np.float64)
+        cap = max(max_iterations if max_iterations > 0 else T, 1)
+        curve = np.zeros(cap); ln = C.c_int64()
+        self.check(self.fn("linear_curve")(C.c_int32(n), C.c_int32(p), C.c_int64(T),
+                                           *[_p(a, C.c_double) for a in arrs], _p(init, C.c_double),
+                                           C.c_double(tolerance), C.c_int64(max_iterations),
+                                           C.c_int32(1 if normalization == "draft" else 0), _p(curve, C.c_double),
+                                           C.c_int64(cap), C.byref(ln)))
+        return curve[:ln.value].copy()
+
+    def linear_sequential(self, spec):
+        n, p, T = spec.state_dim, spec.input_dim, spec.horizon
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (spec.dynamics, spec.input, spec.disturbances, spec.gain)]
+        acts = np.zeros((max(T, 1), p)); states = np.zeros((T + 1, n))
+        self.check(self.fn("linear_sequential")(C.c_int32(n), C.c_int32(p), C.c_int64(T),
+                                                *[_p(a, C.c_double) for a in arrs], _p(acts, C.c_double),
+                                                _p(states, C.c_double)))
+        return acts[:T], states
+
     def total_reward(self, inst, actions):
         ci, k1 = self._inst(inst)
         a = np.ascontiguousarray(actions, np.int32)

@@ -13,6 +13,8 @@
 //   picard::fo::make_product_partition instance.cpp:142-186
 //   picard::fo::MlpParams            mlp.cpp:104-169
 //   picard::fo::{Greedy,CapacityPenalized,DualNetwork}Policy policies.hpp
+//   picard::linear::{make_contractive_spec, picard_convergence_curve,
+//     rollout_states, GainPolicy, LinearEnv}   linear.hpp / linear.cpp
 // The only logic of our own is (a) the J>30 synthetic geometry (SURVEY.md
 // §8(d)) assembled from the reference's building blocks exactly as
 // generate_instance does (instance.cpp:95-138), and (b) the fixture recipe of
@@ -32,6 +34,7 @@
 #include "picard/fo/instance.hpp"
 #include "picard/fo/mlp.hpp"
 #include "picard/fo/policies.hpp"
+#include "picard/linear.hpp"
 #include "picard/rng.hpp"
 
 #include "oracle.h"
@@ -498,6 +501,74 @@ int ref_total_reward(const orc_instance* in, const int32_t* actions, double* tot
     std::vector<FoAction> a;
     for (int64_t t = 0; t < in->horizon; ++t) a.push_back(FoAction{actions[t]});
     *total = fo_total_reward(std::span<const Order>(inst.orders), std::span<const FoAction>(a));
+    return 0;
+  });
+}
+
+// ---------------------------------------------------------------- linear env
+// Flat layout: A[T][n][n], B[T][n][p], w[T][n], G[p][n] (row-major).
+static linear::LinearSystemSpec make_linear(int32_t n, int32_t p, int64_t T, const double* A, const double* B,
+                                            const double* w, const double* G) {
+  linear::LinearSystemSpec s;
+  s.state_dim = n;
+  s.input_dim = p;
+  s.horizon = T;
+  s.gain.assign(G, G + (size_t)p * n);
+  for (int64_t t = 0; t < T; ++t) {
+    s.dynamics.emplace_back(A + (size_t)t * n * n, A + (size_t)(t + 1) * n * n);
+    s.input.emplace_back(B + (size_t)t * n * p, B + (size_t)(t + 1) * n * p);
+    s.disturbances.emplace_back(w + (size_t)t * n, w + (size_t)(t + 1) * n);
+  }
+  s.contraction = linear::closed_loop_contraction(s);
+  return s;
+}
+
+int ref_linear_spec(int32_t n, int32_t p, int64_t T, double rho, uint64_t seed, double coupling, double* A,
+                    double* B, double* w, double* G, double* contraction) {
+  return guarded([&] {
+    const auto s = linear::make_contractive_spec(n, p, T, rho, seed, coupling);
+    std::memcpy(G, s.gain.data(), sizeof(double) * s.gain.size());
+    for (int64_t t = 0; t < T; ++t) {
+      std::memcpy(A + (size_t)t * n * n, s.dynamics[(size_t)t].data(), sizeof(double) * n * n);
+      std::memcpy(B + (size_t)t * n * p, s.input[(size_t)t].data(), sizeof(double) * n * p);
+      std::memcpy(w + (size_t)t * n, s.disturbances[(size_t)t].data(), sizeof(double) * n);
+    }
+    *contraction = s.contraction;
+    return 0;
+  });
+}
+
+// picard_convergence_curve (linear.cpp): curve[k] for k < *len (<= cap)
+int ref_linear_curve(int32_t n, int32_t p, int64_t T, const double* A, const double* B, const double* w,
+                     const double* G, const double* init, double tolerance, int64_t max_iterations,
+                     int32_t normalization, double* curve, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    const auto s = make_linear(n, p, T, A, B, w, G);
+    std::vector<std::vector<double>> ic;
+    if (init)
+      for (int64_t t = 0; t < T; ++t) ic.emplace_back(init + (size_t)t * p, init + (size_t)(t + 1) * p);
+    linear::ConvergenceCurveOptions o;
+    o.tolerance = tolerance;
+    o.max_iterations = max_iterations;
+    o.normalization = normalization ? linear::RmseNormalization::draft : linear::RmseNormalization::reference;
+    const auto c = linear::picard_convergence_curve(s, ic, o);
+    *len = (int64_t)c.size();
+    for (size_t k = 0; k < c.size() && (int64_t)k < cap; ++k) curve[k] = c[k];
+    return 0;
+  });
+}
+
+// sequential_simulate of (LinearEnv, GainPolicy): actions[T][p], states[T+1][n]
+int ref_linear_sequential(int32_t n, int32_t p, int64_t T, const double* A, const double* B, const double* w,
+                          const double* G, double* actions, double* states) {
+  return guarded([&] {
+    const auto s = make_linear(n, p, T, A, B, w, G);
+    linear::LinearEnv env(s);
+    linear::GainPolicy pol(s);
+    const auto steps = linear::make_steps(s);
+    const auto r = sequential_simulate_with_states(env, pol, std::span<const linear::LinearStep>(steps));
+    for (int64_t t = 0; t < T; ++t) std::memcpy(actions + (size_t)t * p, r.actions[(size_t)t].data(), sizeof(double) * p);
+    for (int64_t t = 0; t <= T; ++t) std::memcpy(states + (size_t)t * n, r.states[(size_t)t].data(), sizeof(double) * n);
     return 0;
   });
 }

@@ -22,6 +22,11 @@ PCD_POLICY_GREEDY, PCD_POLICY_CAPACITY, PCD_POLICY_DUAL, PCD_POLICY_NULL = range
 PCD_ENGINE_AUTO, PCD_ENGINE_REPLAY, PCD_ENGINE_PRODUCT, PCD_ENGINE_PRODUCT_FP64 = range(4)
 
 
+class pcd_linear_spec(C.Structure):
+    _fields_ = [("state_dim", C.c_int32), ("input_dim", C.c_int32), ("horizon", C.c_int64),
+                ("dynamics", F64P), ("input", F64P), ("disturbances", F64P), ("gain", F64P)]
+
+
 class pcd_instance(C.Structure):
     _fields_ = [("nodes", C.c_int32), ("products", C.c_int32), ("horizon", C.c_int64),
                 ("product", I32P), ("order_t", I32P), ("reward_row", I32P),
@@ -72,6 +77,11 @@ SIGNATURES = {
     "pcd_generate_instance": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_double,
                                         C.c_uint64, C.c_int32, I32P, I32P, F64P, I32P, I32P]),
     "pcd_product_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),
+    "pcd_linear_contractive_spec": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_uint64, C.c_double,
+                                               F64P, F64P, F64P, F64P, C.POINTER(C.c_double)]),
+    "pcd_linear_convergence_curve": (C.c_int, [C.POINTER(pcd_linear_spec), F64P, C.c_double, C.c_int64, C.c_int32,
+                                                C.c_int32, F64P, C.c_int64, C.POINTER(C.c_int64), F64P,
+                                                C.POINTER(C.c_double)]),
     "pcd_host_alloc": (C.c_void_p, [C.c_size_t]),
     "pcd_host_free": (None, [C.c_void_p]),
     "pcd_product_chunk_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),

@@ -10,6 +10,8 @@ fo::generate_instance (instance.cpp:80) :func:`generate_instance`
 fo::make_product_partition (:142-186)  :func:`make_product_partition`
 (ours, no reference counterpart)       :func:`make_product_chunk_partition`
 make_uniform_time_partition (engine.hpp:99-114) :func:`make_uniform_time_partition`
+linear::make_contractive_spec (linear.cpp:126) :func:`make_contractive_spec`
+linear::picard_convergence_curve (linear.cpp:279) :func:`picard_convergence_curve`
 PartitionPlan (engine.hpp:74-96)       :class:`PartitionPlan`
 PicardConfig (engine.hpp:120-126)      :class:`PicardConfig`
 PicardResult / PicardTraceRow          :class:`PicardResult` / :class:`PicardTraceRow`
@@ -632,3 +634,74 @@ def fo_total_reward(instance: Instance, actions) -> float:
 
 def device_count() -> int:
     return int(LIB.pcd_device_count())
+
+
+# ------------------------------------------------------------ linear env
+@dataclass
+class LinearSystemSpec:
+    """picard::linear::LinearSystemSpec (linear.hpp:16-31): s_{t+1} = A_t s_t +
+    B_t a_t + w_t with dynamics[T, n, n], input[T, n, p], disturbances[T, n],
+    gain[p, n] (the GainPolicy a = G s)."""
+    state_dim: int
+    input_dim: int
+    horizon: int
+    dynamics: np.ndarray
+    input: np.ndarray
+    disturbances: np.ndarray
+    gain: np.ndarray
+    contraction: float = 0.0
+
+    def contractive(self) -> bool:
+        return self.contraction < 1.0
+
+    def to_c(self):
+        n, p, T = int(self.state_dim), int(self.input_dim), int(self.horizon)
+        self._keep = [np.ascontiguousarray(a, np.float64).reshape(-1)
+                      for a in (self.dynamics, self.input, self.disturbances, self.gain)]
+        if any(k.size != want for k, want in zip(self._keep, (T * n * n, T * n * p, T * n, p * n))):
+            raise ContractViolation("linear spec: matrix dimensions disagree")
+        return K.pcd_linear_spec(n, p, T, *[_ptr(k, C.c_double) for k in self._keep])
+
+
+def make_contractive_spec(state_dim: int, input_dim: int, horizon: int, rho: float, seed: int,
+                          state_coupling: float = 0.0) -> LinearSystemSpec:
+    """linear::make_contractive_spec (linear.cpp:126-218), bit-identical."""
+    n, p, T = int(state_dim), int(input_dim), int(horizon)
+    A = np.zeros((max(T, 1), n, n))
+    B = np.zeros((max(T, 1), n, p))
+    W = np.zeros((max(T, 1), n))
+    G = np.zeros((p, n))
+    rho_out = C.c_double()
+    _check(LIB.pcd_linear_contractive_spec(n, p, T, float(rho), int(seed) & (2**64 - 1), float(state_coupling),
+                                           _ptr(A, C.c_double), _ptr(B, C.c_double), _ptr(W, C.c_double),
+                                           _ptr(G, C.c_double), C.byref(rho_out)))
+    return LinearSystemSpec(n, p, T, A[:T], B[:T], W[:T], G, rho_out.value)
+
+
+@dataclass
+class LinearCurve:
+    curve: np.ndarray          # relative RMSE after each iteration
+    final_cache: np.ndarray    # [T, p] actions after the last iteration
+    device_ms: float
+
+
+def picard_convergence_curve(spec: LinearSystemSpec, initial_cache=None, tolerance: float = 1e-3,
+                             max_iterations: int = 0, normalization: str = "draft",
+                             device: int = 0) -> LinearCurve:
+    """linear::picard_convergence_curve (linear.cpp:279-330) on the B200:
+    single-step partitions (M = T), one affine time-scan per iteration."""
+    T, p = int(spec.horizon), int(spec.input_dim)
+    cs = spec.to_c()
+    init = None if initial_cache is None else np.ascontiguousarray(initial_cache, np.float64).reshape(-1)
+    if init is not None and init.size != T * p:
+        raise ContractViolation("initial cache length must equal the horizon")
+    cap = max(int(max_iterations) if max_iterations > 0 else T, 1)
+    curve = np.zeros(cap)
+    fin = np.zeros(max(T * p, 1))
+    n_out = C.c_int64()
+    ms = C.c_double()
+    _check(LIB.pcd_linear_convergence_curve(C.byref(cs), _ptr(init, C.c_double), float(tolerance),
+                                            int(max_iterations), 1 if normalization == "draft" else 0,
+                                            int(device), _ptr(curve, C.c_double), cap, C.byref(n_out),
+                                            _ptr(fin, C.c_double), C.byref(ms)))
+    return LinearCurve(curve[:n_out.value].copy(), fin[:T * p].reshape(T, p), ms.value)

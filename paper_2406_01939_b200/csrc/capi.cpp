@@ -95,6 +95,18 @@ int pcd_product_chunk_partition(const pcd_instance* inst, int32_t processes, uin
   PCD_CATCH
 }
 
+int pcd_linear_contractive_spec(int32_t state_dim, int32_t input_dim, int64_t horizon, double rho, uint64_t seed,
+                                double state_coupling, double* dynamics, double* input, double* disturbances,
+                                double* gain, double* contraction) {
+  PCD_TRY
+  if (horizon > 0 && (!dynamics || !input || !disturbances)) throw pcd::InvalidArgument("null argument");
+  if (!gain || !contraction) throw pcd::InvalidArgument("null argument");
+  pcd::linear_contractive_spec(state_dim, input_dim, horizon, rho, seed, state_coupling, dynamics, input,
+                               disturbances, gain, contraction);
+  return PCD_OK;
+  PCD_CATCH
+}
+
 int pcd_uniform_partition(int64_t horizon, int32_t processes, uint64_t seed, int32_t* owner) {
   PCD_TRY
   if (horizon > 0 && !owner) throw pcd::InvalidArgument("null argument");

@@ -43,6 +43,8 @@ void product_chunk_partition(const int32_t* product, int64_t T, int32_t I, int32
 void uniform_partition(int64_t T, int32_t M, uint64_t seed, int32_t* owner);
 void seeded_mlp(int32_t in, int32_t out, uint64_t seed, int32_t h, double* w1, double* b1,
                 double* w2, double* b2, double* w3, double* b3);
+void linear_contractive_spec(int32_t n, int32_t p, int64_t T, double rho, uint64_t seed, double coupling,
+                             double* A, double* B, double* W, double* G, double* contraction);
 void shard_processes(const int32_t* owner, int64_t T, int32_t M, int32_t ranks, int32_t* rank_of);
 
 }  // namespace pcd

@@ -250,6 +250,101 @@ void uniform_partition(int64_t T, int32_t M, uint64_t seed, int32_t* owner) {
   for (int64_t t = 0; t < T; ++t) owner[t] = static_cast<int32_t>(below(gen, (uint64_t)M));
 }
 
+// ---------------------------------------------------------------- linear env
+namespace {
+// spectral_norm (linear.cpp:68-98): 200 power iterations on M^T M
+double lin_spectral_norm(const double* m, int rows, int cols) {
+  const size_t r = (size_t)rows, c = (size_t)cols;
+  std::vector<double> v(c, 1.0 / std::sqrt(static_cast<double>(c)));
+  std::vector<double> mv(r, 0.0), mtmv(c, 0.0);
+  auto norm2 = [](const std::vector<double>& x) {
+    double acc = 0.0;
+    for (double e : x) acc += e * e;
+    return std::sqrt(acc);
+  };
+  double sigma = 0.0;
+  for (int iter = 0; iter < 200; ++iter) {
+    for (size_t i = 0; i < r; ++i) {
+      double acc = 0.0;
+      for (size_t j = 0; j < c; ++j) acc += m[i * c + j] * v[j];
+      mv[i] = acc;
+    }
+    const double mv_norm = norm2(mv);
+    if (mv_norm < 1e-300) return 0.0;
+    std::fill(mtmv.begin(), mtmv.end(), 0.0);
+    for (size_t i = 0; i < r; ++i)
+      for (size_t j = 0; j < c; ++j) mtmv[j] += m[i * c + j] * mv[i];
+    const double mtmv_norm = norm2(mtmv);
+    if (mtmv_norm < 1e-300) return mv_norm;
+    for (size_t j = 0; j < c; ++j) v[j] = mtmv[j] / mtmv_norm;
+    sigma = mv_norm;
+  }
+  return sigma;
+}
+}  // namespace
+
+// make_contractive_spec (linear.cpp:126-218) and closed_loop_contraction
+// (linear.cpp:100-117), in the reference's operation order.
+void linear_contractive_spec(int32_t n_, int32_t p_, int64_t T, double rho, uint64_t seed, double coupling,
+                             double* A, double* B, double* W, double* G, double* contraction) {
+  if (rho <= 0.0) throw ContractViolation("rho must be positive");
+  if (coupling < 0.0 || coupling >= 1.0) throw ContractViolation("state_coupling must be in [0, 1)");
+  if (n_ < 1 || p_ < 1 || T < 0) throw ContractViolation("linear spec: dimensions must be positive");
+  const size_t n = (size_t)n_, p = (size_t)p_;
+  Engine gen(seed);
+  for (size_t i = 0; i < p * n; ++i) G[i] = range(gen, -1.0, 1.0);
+  std::vector<double> a(n * n), b(n * p), bg(n * n), closed(n * n);
+  for (int64_t t = 0; t < T; ++t) {
+    std::fill(a.begin(), a.end(), 0.0);
+    if (coupling > 0.0) {
+      for (auto& x : a) x = range(gen, -1.0, 1.0);
+      const double norm = lin_spectral_norm(a.data(), n_, n_);
+      const double target = coupling * rho;
+      for (auto& x : a) x *= norm > 0.0 ? target / norm : 0.0;
+    }
+    for (auto& x : b) x = range(gen, -1.0, 1.0);
+    for (size_t r = 0; r < n; ++r)
+      for (size_t c = 0; c < n; ++c) {
+        double acc = 0.0;
+        for (size_t k = 0; k < p; ++k) acc += b[r * p + k] * G[k * n + c];
+        bg[r * n + c] = acc;
+      }
+    const double bg_norm = lin_spectral_norm(bg.data(), n_, n_);
+    if (bg_norm < 1e-12) throw ContractViolation("degenerate random draw: B_t G is zero");
+    double scale;
+    if (coupling == 0.0) {
+      scale = rho / bg_norm;
+    } else {
+      auto closed_norm = [&](double s) {
+        for (size_t i = 0; i < n * n; ++i) closed[i] = a[i] + s * bg[i];
+        return lin_spectral_norm(closed.data(), n_, n_);
+      };
+      double lo = 0.0, hi = (rho + coupling * rho + 1.0) / bg_norm;
+      while (closed_norm(hi) < rho) hi *= 2.0;
+      for (int iter = 0; iter < 120; ++iter) {
+        const double mid = 0.5 * (lo + hi);
+        (closed_norm(mid) < rho ? lo : hi) = mid;
+      }
+      scale = 0.5 * (lo + hi);
+    }
+    for (auto& x : b) x *= scale;
+    std::copy(a.begin(), a.end(), A + (size_t)t * n * n);
+    std::copy(b.begin(), b.end(), B + (size_t)t * n * p);
+    for (size_t i = 0; i < n; ++i) W[(size_t)t * n + i] = range(gen, -1.0, 1.0);
+  }
+  double worst = 0.0;
+  for (int64_t t = 0; t < T; ++t) {
+    for (size_t r = 0; r < n; ++r)
+      for (size_t c = 0; c < n; ++c) {
+        double acc = A[(size_t)t * n * n + r * n + c];
+        for (size_t k = 0; k < p; ++k) acc += B[(size_t)t * n * p + r * p + k] * G[k * n + c];
+        closed[r * n + c] = acc;
+      }
+    worst = std::max(worst, lin_spectral_norm(closed.data(), n_, n_));
+  }
+  *contraction = worst;
+}
+
 void seeded_mlp(int32_t in, int32_t out, uint64_t seed, int32_t h, double* w1, double* b1,
                 double* w2, double* b2, double* w3, double* b3) {
   Engine gen(seed);
