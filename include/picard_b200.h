@@ -180,6 +180,30 @@ int64_t pcd_last_error_time_step(void);
 int pcd_device_count(void);
 
 /* ------------------------------------------------------------------------
+ * Time Warp safe-window baseline (timewarp::time_warp_simulate,
+ * fo/timewarp.hpp:56-181) on the device: product partition of `processes`
+ * (seed), windows [t0, t0 + delta) with delta the minimum remaining capacity
+ * (rule 0: over all nodes, clamped to >= 1; rule 1: over still-stocked
+ * nodes), every process evaluating its own steps against the synchronized
+ * state with all other steps declined, then an in-order merge; an infeasible
+ * merge rolls the window back and re-executes it serially. Replaces the
+ * handle's plan. */
+typedef struct pcd_tw_result {
+  int64_t sync_rounds;
+  int64_t rollbacks;
+  int64_t policy_eval_count_sequential_equivalent;
+  int64_t total_policy_evals;
+  int64_t trace_rows;
+  int64_t error_time_step;
+} pcd_tw_result;
+typedef struct pcd_tw_trace_row {
+  int64_t round, t_start, window_length, max_process_evals;
+  int32_t rolled_back, pad;
+} pcd_tw_trace_row;
+int pcd_time_warp(pcd_handle* h, int32_t processes, uint64_t seed, int32_t rule, int32_t record_trace,
+                  int32_t* actions_out, pcd_tw_result* result, pcd_tw_trace_row* trace, int64_t trace_cap);
+
+/* ------------------------------------------------------------------------
  * Non-SCO environment (picard::linear, linear.hpp / linear.cpp): the
  * time-varying linear system s_{t+1} = A_t s_t + B_t a_t + w_t under the
  * linear feedback a_t = G s_t (GainPolicy). Row-major flat arrays:

@@ -320,6 +320,25 @@ class _Lib:
                                            C.byref(it), C.byref(se), C.byref(sec)))
         return actions[:int(inst.horizon)], it.value, se.value, sec.value
 
+    # ---------------------------------------------------------- Time Warp
+    # (reference harness only: ref_time_warp, fo/timewarp.hpp:56-181)
+    def time_warp(self, inst, pol, processes, seed, rule=0, record_trace=True):
+        ci, k1 = self._inst(inst)
+        cp, k2 = self._pol(pol)
+        T = int(inst.horizon)
+        actions = np.zeros(max(T, 1), np.int32)
+        counters = np.zeros(4, np.int64)
+        cap = 2 * T + 4
+        trace = np.zeros((cap, 5), np.int64)
+        rows = C.c_int64()
+        et = C.c_int64(-1)
+        rc = self.fn("time_warp")(C.byref(ci), C.byref(cp), C.c_int32(processes), C.c_uint64(seed), C.c_int32(rule),
+                                  C.c_int32(1 if record_trace else 0), _p(actions, C.c_int32),
+                                  _p(counters, C.c_int64), _p(trace, C.c_int64), C.c_int64(cap), C.byref(rows),
+                                  C.byref(et))
+        self.check(rc, et.value)
+        return actions[:T], counters, trace[:min(rows.value, cap)]
+
     # ---------------------------------------------------------- linear env
     # (reference harness only: ref_linear_* in ref_harness.cpp)
     def linear_spec(self, n, p, T, rho, seed, coupling=0.0):

@@ -13,6 +13,7 @@
 //   picard::fo::make_product_partition instance.cpp:142-186
 //   picard::fo::MlpParams            mlp.cpp:104-169
 //   picard::fo::{Greedy,CapacityPenalized,DualNetwork}Policy policies.hpp
+//   picard::timewarp::time_warp_simulate     fo/timewarp.hpp:56-181
 //   picard::linear::{make_contractive_spec, picard_convergence_curve,
 //     rollout_states, GainPolicy, LinearEnv}   linear.hpp / linear.cpp
 // The only logic of our own is (a) the J>30 synthetic geometry (SURVEY.md
@@ -34,6 +35,7 @@
 #include "picard/fo/instance.hpp"
 #include "picard/fo/mlp.hpp"
 #include "picard/fo/policies.hpp"
+#include "picard/fo/timewarp.hpp"
 #include "picard/linear.hpp"
 #include "picard/rng.hpp"
 
@@ -503,6 +505,37 @@ int ref_total_reward(const orc_instance* in, const int32_t* actions, double* tot
     *total = fo_total_reward(std::span<const Order>(inst.orders), std::span<const FoAction>(a));
     return 0;
   });
+}
+
+// ---------------------------------------------------------------- Time Warp
+// counters = {sync_rounds, rollbacks, seq_equiv, total_evals}; trace rows of
+// 5 int64 {round, t_start, window_length, max_process_evals, rolled_back}
+int ref_time_warp(const orc_instance* in, const orc_policy* pol, int32_t processes, uint64_t seed, int32_t rule,
+                  int32_t record_trace, int32_t* actions, int64_t* counters, int64_t* trace, int64_t trace_cap,
+                  int64_t* trace_rows, int64_t* error_t) {
+  return guarded(
+      [&] {
+        Instance inst = make_instance(in);
+        return with_policy(in, pol, inst, [&](const auto& policy) {
+          const auto r = timewarp::time_warp_simulate(inst, policy, processes, seed, record_trace != 0,
+                                                      rule ? timewarp::WindowRule::min_stocked_capacity
+                                                           : timewarp::WindowRule::min_capacity);
+          for (size_t t = 0; t < r.actions.size(); ++t) actions[t] = r.actions[t].node;
+          counters[0] = r.sync_rounds;
+          counters[1] = r.rollbacks;
+          counters[2] = r.policy_eval_count_sequential_equivalent;
+          counters[3] = r.total_policy_evals;
+          *trace_rows = (int64_t)r.trace.size();
+          for (size_t i = 0; i < r.trace.size() && (int64_t)i < trace_cap; ++i) {
+            const auto& row = r.trace[i];
+            int64_t* o = trace + 5 * i;
+            o[0] = row.round; o[1] = row.t_start; o[2] = row.window_length; o[3] = row.max_process_evals;
+            o[4] = row.rolled_back ? 1 : 0;
+          }
+          return 0;
+        });
+      },
+      error_t);
 }
 
 // ---------------------------------------------------------------- linear env

@@ -27,6 +27,17 @@ class pcd_linear_spec(C.Structure):
                 ("dynamics", F64P), ("input", F64P), ("disturbances", F64P), ("gain", F64P)]
 
 
+class pcd_tw_result(C.Structure):
+    _fields_ = [("sync_rounds", C.c_int64), ("rollbacks", C.c_int64),
+                ("policy_eval_count_sequential_equivalent", C.c_int64), ("total_policy_evals", C.c_int64),
+                ("trace_rows", C.c_int64), ("error_time_step", C.c_int64)]
+
+
+class pcd_tw_trace_row(C.Structure):
+    _fields_ = [("round", C.c_int64), ("t_start", C.c_int64), ("window_length", C.c_int64),
+                ("max_process_evals", C.c_int64), ("rolled_back", C.c_int32), ("pad", C.c_int32)]
+
+
 class pcd_instance(C.Structure):
     _fields_ = [("nodes", C.c_int32), ("products", C.c_int32), ("horizon", C.c_int64),
                 ("product", I32P), ("order_t", I32P), ("reward_row", I32P),
@@ -82,6 +93,8 @@ SIGNATURES = {
     "pcd_linear_convergence_curve": (C.c_int, [C.POINTER(pcd_linear_spec), F64P, C.c_double, C.c_int64, C.c_int32,
                                                 C.c_int32, F64P, C.c_int64, C.POINTER(C.c_int64), F64P,
                                                 C.POINTER(C.c_double)]),
+    "pcd_time_warp": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32, I32P,
+                                 C.POINTER(pcd_tw_result), C.POINTER(pcd_tw_trace_row), C.c_int64]),
     "pcd_host_alloc": (C.c_void_p, [C.c_size_t]),
     "pcd_host_free": (None, [C.c_void_p]),
     "pcd_product_chunk_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),

@@ -705,3 +705,50 @@ def picard_convergence_curve(spec: LinearSystemSpec, initial_cache=None, toleran
                                             int(device), _ptr(curve, C.c_double), cap, C.byref(n_out),
                                             _ptr(fin, C.c_double), C.byref(ms)))
     return LinearCurve(curve[:n_out.value].copy(), fin[:T * p].reshape(T, p), ms.value)
+
+
+# ------------------------------------------------------------ Time Warp
+@dataclass
+class TimeWarpTraceRow:
+    round: int
+    t_start: int
+    window_length: int
+    max_process_evals: int
+    rolled_back: bool
+
+    def astuple(self):
+        return (self.round, self.t_start, self.window_length, self.max_process_evals, int(self.rolled_back))
+
+
+@dataclass
+class TimeWarpResult:
+    """timewarp::TimeWarpResult (fo/timewarp.hpp:36-43)."""
+    actions: np.ndarray
+    sync_rounds: int
+    rollbacks: int
+    policy_eval_count_sequential_equivalent: int
+    total_policy_evals: int
+    trace: List[TimeWarpTraceRow]
+
+
+def time_warp_simulate(instance: Instance, policy: Policy, processes: int, seed: int, record_trace: bool = False,
+                       rule: str = "min_capacity", device: int = 0) -> TimeWarpResult:
+    """timewarp::time_warp_simulate (fo/timewarp.hpp:56-181) on the B200: the
+    safe-window baseline over make_product_partition(processes, seed);
+    ``rule`` is "min_capacity" or "min_stocked_capacity"."""
+    if rule not in ("min_capacity", "min_stocked_capacity"):
+        raise InvalidArgument("unknown window rule")
+    T = int(instance.horizon)
+    with Simulator(instance, policy, device) as sim:
+        actions = _pinned_i32(T)
+        res = K.pcd_tw_result()
+        cap = 2 * T + 4 if record_trace else 0
+        trace = (K.pcd_tw_trace_row * max(cap, 1))()
+        rc = LIB.pcd_time_warp(sim._h, int(processes), int(seed) & (2**64 - 1),
+                               1 if rule == "min_stocked_capacity" else 0, 1 if record_trace else 0,
+                               _ptr(actions), C.byref(res), trace, cap)
+        _check(rc, res.error_time_step)
+        rows = [TimeWarpTraceRow(r.round, r.t_start, r.window_length, r.max_process_evals, bool(r.rolled_back))
+                for r in trace[:min(res.trace_rows, cap)]]
+        return TimeWarpResult(actions[:T].copy(), res.sync_rounds, res.rollbacks,
+                              res.policy_eval_count_sequential_equivalent, res.total_policy_evals, rows)

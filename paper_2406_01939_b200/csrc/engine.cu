@@ -171,6 +171,7 @@ struct pcd_handle {
   int64_t p_horizon = 0;
   pcd::DBuf<double> w1t, b1, w2t, b2, w3t, b3, w3s;
   double fast_margin = 0.0;  // see fast_margin_bound
+  int nocache = 0;           // Time Warp windows (pcd_time_warp)
   pcd::DBuf<int> pcap0, pinv0;
   // plan
   int32_t M = 0;
@@ -334,6 +335,7 @@ static void launch_product_sweep(pcd_handle* h, int lo, int hi, long long* evals
   a.M = h->M; a.J = h->J; a.lo = lo; a.hi = hi;
   a.pstart = h->pstart.p; a.pslots = h->pslots.p;
   a.ckcap = h->ckcap.p; a.hck = h->hck.p; a.ev = h->ev.p; a.xloc = h->xloc.p; a.rid = h->rid.p;
+  a.nocache = h->nocache;
   a.cache = h->cache.p; a.written = h->written.p; a.ref = h->ref.n ? h->ref.p : nullptr;
   a.scal = h->scal; a.evals_out = evals_out;
   a.mine = h->comm ? h->d_mine.p : nullptr;
@@ -405,6 +407,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   s.M = h->M; s.J = h->J; s.lo = lo; s.hi = hi;
   s.pstart = h->pstart.p; s.pslots = h->pslots.p;
   s.ckcap = h->ckcap.p; s.hck = h->hck.p; s.ev = h->ev.p; s.xloc = h->xloc.p; s.rid = h->rid.p;
+  s.nocache = h->nocache;
   s.cache = h->cache.p; s.written = h->written.p; s.ref = h->ref.n ? h->ref.p : nullptr;
   s.scal = h->scal; s.evals_out = evals_out;
   // work list: this rank's processes with window slots, heaviest first; the
@@ -1252,6 +1255,129 @@ extern "C" int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* poli
   if (had) pcd_set_plan(h, saved.data(), savedM);
   if (policy_evals) *policy_evals = h->T;
   return rc;
+  PCD_CATCH
+}
+
+// time_warp_simulate (fo/timewarp.hpp:56-181). Each window is one sweep of
+// the run-partition engine with the cache treated as all-declined (nocache:
+// H = 0, so a process sees the synchronized state minus its own decisions),
+// then the merge is the checkpoint advance over the window; a merge that
+// would go negative is undone and the window re-executed serially.
+extern "C" int pcd_time_warp(pcd_handle* h, int32_t processes, uint64_t seed, int32_t rule, int32_t record_trace,
+                             int32_t* actions_out, pcd_tw_result* res, pcd_tw_trace_row* trace, int64_t trace_cap) {
+  pcd_tw_result dummy;
+  if (!res) res = &dummy;
+  *res = pcd_tw_result{0, 0, 0, 0, 0, -1};
+  PCD_TRY
+  if (!h) throw InvalidArgument("handle is null");
+  CK(cudaSetDevice(h->device));
+  const int64_t T = h->T;
+  // the plan: make_product_partition(instance, processes, seed)
+  std::vector<int32_t> prod((size_t)std::max<int64_t>(T, 1)), owner((size_t)std::max<int64_t>(T, 1));
+  if (T) CK(cudaMemcpy(prod.data(), h->product.p, sizeof(int32_t) * (size_t)T, cudaMemcpyDeviceToHost));
+  product_partition(prod.data(), T, h->I, processes, seed, owner.data());
+  {
+    const int rc = pcd_set_plan(h, owner.data(), processes);
+    if (rc) return rc;
+  }
+  ensure_state_buffers(h);
+  const size_t IJ = (size_t)h->I * h->J;
+  CK(cudaMemcpyAsync(h->ckcap.p, h->cap0.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->ckinv.p, h->inv0.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+  if (T) k_fill<<<grid_for(T, 256), 256, 0, h->stream>>>(h->cache.p, -1, (long long)T);
+  if (T) CK(cudaMemsetAsync(h->written.p, 0, (size_t)T, h->stream));
+  h->ref.release();
+  h->timing = pcd_timing{};
+  h->nocache = 1;
+  struct Reset {
+    pcd_handle* h;
+    ~Reset() { h->nocache = 0; }
+  } reset{h};
+  DBuf<long long> derr;
+  derr.alloc(2);
+  std::vector<int32_t> caps((size_t)h->J);
+  std::vector<pcd_tw_trace_row> rows;
+  const bool tc = h->tc_ok && h->kind == kDual;
+  int64_t t0 = 0;
+  while (t0 < T) {
+    CK(cudaMemcpyAsync(caps.data(), h->ckcap.p, sizeof(int32_t) * h->J, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    int64_t delta = 0;
+    if (rule == 0) {
+      int32_t mc = caps.empty() ? 0 : caps[0];
+      for (int32_t c : caps) mc = std::min(mc, c);
+      delta = std::max<int64_t>(1, mc);
+    } else {
+      int32_t ms = 0;
+      bool any = false;
+      for (int32_t c : caps) {
+        if (c <= 0) continue;
+        ms = any ? std::min(ms, c) : c;
+        any = true;
+      }
+      delta = any ? std::max<int64_t>(1, ms) : T - t0;
+    }
+    const int64_t hi = std::min(T, t0 + delta);
+    const int lo32 = (int)t0, hi32 = (int)hi;
+    // local decisions of every process over the window
+    reset_scalars(h);
+    k_xinit_plain<<<(h->I * 32 + 255) / 256, 256, 0, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo32, hi32,
+                                                                   h->rid.p, h->ckinv.p, h->J, h->xloc.p);
+    if (tc) launch_tc(h, lo32, hi32, nullptr, 0.0, 0);
+    else dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo32, hi32, nullptr); });
+    exchange(h, h->cache.p, true);
+    read_scalars(h);
+    throw_sweep_error(h);
+    const int64_t max_evals = (int64_t)h->h_scal->max_evals, sum_evals = (int64_t)h->h_scal->total_evals;
+    res->policy_eval_count_sequential_equivalent += max_evals;
+    res->total_policy_evals += sum_evals;
+    h->timing.kernel_launches += 3;
+    // synchronize: apply the merged decisions in time order
+    bool merged = true;
+    {
+      CK(cudaMemcpyAsync(h->ckbak.p, h->ckinv.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+      CK(cudaMemcpyAsync(h->ckbak.p + IJ, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+      k_advance<<<grid_for(hi - t0, 256), 256, (size_t)h->J * 4, h->stream>>>(h->cache.p, h->product.p, lo32, hi32,
+                                                                              h->J, h->ckcap.p, h->ckinv.p);
+      CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
+      k_advance_check<<<grid_for(std::max<long long>((long long)IJ, hi - t0), 256), 256, 0, h->stream>>>(
+          h->cache.p, lo32, hi32, h->J, h->ckcap.p, h->ckinv.p, (long long)IJ, h->scal);
+      int flag = 0;
+      CK(cudaMemcpyAsync(&flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      merged = flag == 0;
+    }
+    if (!merged) {  // roll back, re-execute the window serially (charged at serial cost)
+      CK(cudaMemcpyAsync(h->ckinv.p, h->ckbak.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+      CK(cudaMemcpyAsync(h->ckcap.p, h->ckbak.p + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+      CK(cudaMemsetAsync(derr.p, 0xff, 2 * sizeof(long long), h->stream));
+      const size_t smem = ((size_t)2 * h->J * 4 + 15 & ~(size_t)15) +
+                          (size_t)(2 * h->J + 1 + 2 * h->H + 2 * h->J) * 8;
+      dispatch_kind(h->kind, [&](auto k) {
+        k_serial_window<decltype(k)::value><<<1, 32, smem, h->stream>>>(h->model(), lo32, hi32, h->ckcap.p,
+                                                                          h->ckinv.p, h->cache.p, derr.p);
+      });
+      CK(cudaGetLastError());
+      long long e[2];
+      CK(cudaMemcpyAsync(e, derr.p, sizeof e, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      if (e[1] == 2) throw ContractViolation("dual network produced a non-finite score", e[0]);
+      if (e[1] == 1)
+        throw ContractViolation("policy returned an infeasible action at t=" + std::to_string(e[0]), e[0]);
+      res->rollbacks += 1;
+      res->policy_eval_count_sequential_equivalent += hi - t0;
+      res->total_policy_evals += hi - t0;
+    }
+    res->sync_rounds += 1;
+    if (record_trace) rows.push_back({res->sync_rounds, t0, hi - t0, max_evals, merged ? 0 : 1, 0});
+    t0 = hi;
+  }
+  if (actions_out && T)
+    CK(cudaMemcpyAsync(actions_out, h->cache.p, sizeof(int32_t) * (size_t)T, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  res->trace_rows = (int64_t)rows.size();
+  for (int64_t i = 0; i < (int64_t)rows.size() && i < trace_cap; ++i) trace[i] = rows[(size_t)i];
+  return PCD_OK;
   PCD_CATCH
 }
 

@@ -208,6 +208,66 @@ static __global__ void k_xinit(const int* __restrict__ qstart, const int* __rest
   }
 }
 
+// Time Warp windows on product partitions: every product is one run, whose
+// inventory at its first window slot is the checkpoint's.
+static __global__ void k_xinit_plain(const int* __restrict__ qstart, const int* __restrict__ qslots, int I, int lo,
+                                     int hi, const int* __restrict__ rid, const int* __restrict__ ckinv, int J,
+                                     int* __restrict__ xloc) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= I) return;
+  const int* sl;
+  int k0, k1;
+  product_window(qstart, qslots, warp, lo, hi, sl, k0, k1);
+  if (k0 >= k1) return;
+  int* xr = xloc + (size_t)rid[sl[k0]] * J;
+  for (int j = lane; j < J; j += 32) xr[j] = ckinv[(size_t)warp * J + j];
+}
+
+// Time Warp rollback (fo/timewarp.hpp:150-170): re-execute [lo, hi) strictly
+// serially against the global state (one warp, the exact FP64 policy).
+// err[0] = time step of the first failure, err[1] = 1 infeasible / 2 non-finite
+template <int KIND>
+static __global__ void k_serial_window(DevModel model, int lo, int hi, int* __restrict__ ckcap,
+                                       int* __restrict__ ckinv, int* __restrict__ cache, long long* err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, J = model.J;
+  int* caps = (int*)smem;
+  int* row = caps + J;
+  WarpScratch ws;
+  double* d = (double*)(smem + ((2 * J * 4 + 15) & ~15));
+  ws.f = d;
+  ws.h1 = d + model.in;
+  ws.h2 = ws.h1 + model.H;
+  ws.pr = ws.h2 + model.H;
+  for (int j = lane; j < J; j += 32) caps[j] = ckcap[j];
+  __syncwarp();
+  for (int t = lo; t < hi; ++t) {
+    const int p = model.product[t];
+    for (int j = lane; j < J; j += 32) row[j] = ckinv[(size_t)p * J + j];
+    __syncwarp();
+    int nonfinite = 0;
+    const int a = warp_policy_eval<KIND>(model, caps, row, t, ws, lane, &nonfinite);
+    const bool bad = nonfinite || a >= J || (a >= 0 && !(caps[a] > 0 && row[a] > 0));
+    __syncwarp();
+    if (bad) {
+      if (lane == 0) {
+        err[0] = nonfinite ? (model.order_t ? model.order_t[t] : t) : t;
+        err[1] = nonfinite ? 2 : 1;
+      }
+      return;
+    }
+    if (lane == 0) {
+      if (a >= 0) {
+        caps[a] -= 1;
+        ckinv[(size_t)p * J + a] -= 1;
+      }
+      cache[t] = a;
+    }
+    __syncwarp();
+  }
+  for (int j = lane; j < J; j += 32) ckcap[j] = caps[j];
+}
+
 // Run structure of a plan along the product slot lists (qslots, time order
 // per product): run_start[k] = 1 where a product's list starts or the owner
 // changes.
@@ -369,6 +429,7 @@ struct SweepArgs {
   const int* ev;
   int* xloc;
   const int* rid;
+  int nocache;  // Time Warp windows: every other process's step counts as declined (H = 0)
   int* cache;
   unsigned char* written;
   const int* ref;
@@ -436,19 +497,20 @@ static __global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
     const int t = sl[k];
     if (t >= a.hi) break;
     const int aold = a.cache[t];
-    const int evt = a.ev[t];
+    const int evt = a.nocache ? -1 : a.ev[t];
     const int b = (t - hck_base(a.lo)) >> kLogK;
-    const int* hrow = a.hck + (size_t)b * hck_stride(J);
+    const int* hrow = a.nocache ? nullptr : a.hck + (size_t)b * hck_stride(J);
     int* xrow = a.xloc + (size_t)a.rid[t] * J;
     for (int j = lane; j < J; j += 32) {
-      crow[j] = a.ckcap[j] - hrow[j] + D[j];
+      crow[j] = a.ckcap[j] - (hrow ? hrow[j] : 0) + D[j];
       prow[j] = xrow[j];
     }
     __syncwarp();
-    for (int s = max(a.lo, hck_base(a.lo) + (b << kLogK)) + lane; s < t; s += 32) {
-      const int e = a.ev[s];
-      if (e >= 0) atomicSub(&crow[e], 1);
-    }
+    if (!a.nocache)
+      for (int s = max(a.lo, hck_base(a.lo) + (b << kLogK)) + lane; s < t; s += 32) {
+        const int e = a.ev[s];
+        if (e >= 0) atomicSub(&crow[e], 1);
+      }
     __syncwarp();
     for (int j = lane; j < J; j += 32) crow[j] = max(crow[j], 0);
     __syncwarp();

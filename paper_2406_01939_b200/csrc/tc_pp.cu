@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
       const int pos = inf[RI_POS], end = inf[RI_END];
       if (pos < end) {
         const int t = inf[RI_T];
-        u_ev = S.ev[t];
+        u_ev = S.nocache ? -1 : S.ev[t];
         u_old = S.cache[t];
         u_wr = S.written[t];
         if (S.ref) u_ref = S.ref[t];
@@ -502,12 +502,14 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         b = (t - base) >> kLogK;
         // streamed rows bypass L1, so the reward table (read every step) stays there
         // (and leave L2 first: read about once per iteration)
-        const int* hr = S.hck + (size_t)b * HJ;
-        const uint64_t pol = l2_policy_evict_first();
-        ldg256_na_ef(S.ev + base + (b << kLogK), e8, pol);
+        if (!S.nocache) {  // nocache (Time Warp): other processes' steps count as declined
+          const int* hr = S.hck + (size_t)b * HJ;
+          const uint64_t pol = l2_policy_evict_first();
+          ldg256_na_ef(S.ev + base + (b << kLogK), e8, pol);
 #pragma unroll
-        for (int i = 0; i < kMaxCI; ++i)
-          if (i < ni && 8 * (g + 4 * i) < J) ldg256_na_ef(hr + 8 * (g + 4 * i), hv[i], pol);
+          for (int i = 0; i < kMaxCI; ++i)
+            if (i < ni && 8 * (g + 4 * i) < J) ldg256_na_ef(hr + 8 * (g + 4 * i), hv[i], pol);
+        }
         if (!xd && my_ci(xu) >= 0) {
           xuv = S.xloc[(size_t)x * J + xu];
           xui = __ldg(a.inv_x0 + (size_t)p * J + xu);
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         inf[RI_POS] = pos;
         if (pos < inf[RI_END]) {
           const int tp = inf[RI_UTNN];
-          if (tp >= 0) {  // warm L2 with the checkpoint row and event block of the step after next
+          if (tp >= 0 && !S.nocache) {  // warm L2 with the checkpoint row and event block of the step after next
             const int bn = (tp - base) >> kLogK;
             const int* hbn = S.hck + (size_t)bn * HJ;
             for (int k = 0; k < HJ; k += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(hbn + k));
