@@ -372,6 +372,31 @@ def test_full_scale_c3_prefix_and_feasibility():
     assert int(ok.sum()) == int(inst.capacity.sum() - cap.sum())
 
 
+def test_c3_full_trajectory_chunk_vs_product_vs_fp64():
+    """The bench workload itself (C3: J=100, I=1e4, T=1e7): the product-chunk
+    plan on the tensor-core engine, the reference's product plan, and the
+    FP64 SIMT engine all reach the same trajectory (the serial one, Prop. 1);
+    its first 1e5 orders equal the serial oracle; chunks change the plan's
+    counters but not the 66 iterations at this shape."""
+    J, I, T = 100, 10_000, 10_000_000
+    inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
+    pol = P.DualNetworkPolicy.seeded(inst, 5)
+    cfg = P.PicardConfig(max_steps=300 * 65536)
+    chunk = P.picard_simulate(inst, pol, P.make_product_chunk_partition(inst, 65536, 1), cfg)
+    prod = P.picard_simulate(inst, pol, P.make_product_partition(inst, 65536, 1), cfg)
+    assert np.array_equal(chunk.actions, prod.actions)
+    assert chunk.iterations_to_converged == prod.iterations_to_converged == 66
+    assert chunk.timing["tc_unflagged_bad"] == 0 and chunk.timing["tc_used"] == 1
+    n = 100_000
+    ons = NS(nodes=J, products=I, horizon=n, product=inst.product[:n], order_t=None,
+             reward_row=inst.reward_row[:n], reward_table=inst.reward_table.ravel(),
+             capacity=inst.capacity, inventory=inst.inventory.ravel())
+    opol = NS(kind=2, hidden=64, gamma=0.0, horizon=T, w1=pol.w1, b1=pol.b1, w2=pol.w2, b2=pol.b2,
+              w3=pol.w3, b3=pol.b3)
+    seq_prefix, _ = ORC.sequential(ons, opol)
+    assert chunk.actions[:n].tolist() == seq_prefix.tolist()
+
+
 @pytest.mark.parametrize("J,I,T,M", [(10, 300, 20000, 512), (30, 200, 12000, 256), (100, 40, 4000, 64),
                                      (100, 300, 30000, 512), (1, 10, 10000, 16), (3, 7, 900, 5)])
 def test_tensor_core_sweep_matches_oracle(J, I, T, M):
