@@ -1,6 +1,6 @@
 """Small driver for ncu captures / phase profiles of the sweep kernels (not a test).
 
-  python tests/tc_ncu_target.py J I T M [engine] [--cap] [--chunk]
+  python tools/tc_ncu_target.py J I T M [engine] [--cap] [--chunk]
 """
 import sys
 
