@@ -180,6 +180,26 @@ int64_t pcd_last_error_time_step(void);
 int pcd_device_count(void);
 
 /* ------------------------------------------------------------------------
+ * Depletion profile (theory::compute_depletion, theory.hpp:21-86) of a
+ * trajectory on the device: first_depleted_at[j] = first t in [0, T) whose
+ * entering capacity of node j is 0, T when never; *depleted_count = nodes
+ * that deplete (theory::DepletionProfile::iteration_bound() = count + 1).
+ * actions[T] (host) or NULL for the handle's resident cache. */
+int pcd_depletion_profile(pcd_handle* h, const int32_t* actions, int64_t* first_depleted_at,
+                          int64_t* depleted_count);
+
+/* Binary SoA instance files (no reference counterpart; the reference's CSV
+ * carries a J-vector of rewards per order, ~10^9 fields at C3): a 48-byte
+ * header ("PCDINST1", J, I, T, R, has_order_t) followed by product[T],
+ * reward_row[T], order_t[T] (if present) as int32, reward_table[R*J] as f64,
+ * capacity[J] and inventory[I*J] as int32, little endian. */
+int pcd_save_instance_bin(const pcd_instance* inst, const char* path);
+int pcd_instance_bin_info(const char* path, int32_t* nodes, int32_t* products, int64_t* horizon,
+                          int64_t* reward_rows, int32_t* has_order_t);
+int pcd_load_instance_bin(const char* path, int32_t* product, int32_t* reward_row, int32_t* order_t,
+                          double* reward_table, int32_t* capacity, int32_t* inventory);
+
+/* ------------------------------------------------------------------------
  * Time Warp safe-window baseline (timewarp::time_warp_simulate,
  * fo/timewarp.hpp:56-181) on the device: product partition of `processes`
  * (seed), windows [t0, t0 + delta) with delta the minimum remaining capacity

@@ -320,6 +320,13 @@ class _Lib:
                                            C.byref(it), C.byref(se), C.byref(sec)))
         return actions[:int(inst.horizon)], it.value, se.value, sec.value
 
+    def depletion(self, inst, actions):
+        ci, k1 = self._inst(inst)
+        out = np.zeros(int(inst.nodes), np.int64)
+        a = np.ascontiguousarray(actions, np.int32)
+        self.check(self.fn("depletion")(C.byref(ci), _p(a, C.c_int32), _p(out, C.c_int64)))
+        return out
+
     # ---------------------------------------------------------- Time Warp
     # (reference harness only: ref_time_warp, fo/timewarp.hpp:56-181)
     def time_warp(self, inst, pol, processes, seed, rule=0, record_trace=True):

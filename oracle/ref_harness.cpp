@@ -38,6 +38,7 @@
 #include "picard/fo/timewarp.hpp"
 #include "picard/linear.hpp"
 #include "picard/rng.hpp"
+#include "picard/theory.hpp"
 
 #include "oracle.h"
 
@@ -503,6 +504,24 @@ int ref_total_reward(const orc_instance* in, const int32_t* actions, double* tot
     std::vector<FoAction> a;
     for (int64_t t = 0; t < in->horizon; ++t) a.push_back(FoAction{actions[t]});
     *total = fo_total_reward(std::span<const Order>(inst.orders), std::span<const FoAction>(a));
+    return 0;
+  });
+}
+
+// theory::compute_depletion_from_capacities on the capacities of the
+// trajectory `actions` replayed from the initial state (fo_transition)
+int ref_depletion(const orc_instance* in, const int32_t* actions, int64_t* first_depleted_at) {
+  return guarded([&] {
+    Instance inst = make_instance(in);
+    FoState s = inst.initial;
+    std::vector<std::vector<int32_t>> caps;
+    caps.push_back(s.capacity);
+    for (int64_t t = 0; t < in->horizon; ++t) {
+      apply_in_place(s, inst.orders[(size_t)t], FoAction{actions[t]});
+      caps.push_back(s.capacity);
+    }
+    const auto prof = theory::compute_depletion_from_capacities(caps);
+    for (size_t j = 0; j < prof.first_depleted_at.size(); ++j) first_depleted_at[j] = prof.first_depleted_at[j];
     return 0;
   });
 }

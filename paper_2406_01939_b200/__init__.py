@@ -7,7 +7,8 @@ the Python mirror of the reference interface (see :mod:`.api`).
 """
 from .api import (  # noqa: F401
     NO_FULFILL, CapacityPenalizedPolicy, LinearCurve, LinearSystemSpec, make_contractive_spec,
-    picard_convergence_curve, TimeWarpResult, time_warp_simulate, ContractViolation, CudaError, DualNetworkPolicy, GreedyPolicy,
+    picard_convergence_curve, TimeWarpResult, time_warp_simulate, DepletionProfile, depletion_profile,
+    check_iteration_bound, save_instance_binary, load_instance_binary, ContractViolation, CudaError, DualNetworkPolicy, GreedyPolicy,
     Instance, InvalidArgument, IterationLimitError, IterationOutcome, MlpParams, NullOnlyPolicy,
     PartitionPlan, PicardConfig, PicardError, PicardResult, PicardTraceRow, Policy, SequentialOutput,
     Simulator, compare_to_oracle, device_count, fo_total_reward, generate_instance,

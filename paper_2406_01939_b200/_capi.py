@@ -95,6 +95,11 @@ SIGNATURES = {
                                                 C.POINTER(C.c_double)]),
     "pcd_time_warp": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32, I32P,
                                  C.POINTER(pcd_tw_result), C.POINTER(pcd_tw_trace_row), C.c_int64]),
+    "pcd_depletion_profile": (C.c_int, [C.c_void_p, I32P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "pcd_save_instance_bin": (C.c_int, [C.POINTER(pcd_instance), C.c_char_p]),
+    "pcd_instance_bin_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "pcd_load_instance_bin": (C.c_int, [C.c_char_p, I32P, I32P, I32P, F64P, I32P, I32P]),
     "pcd_host_alloc": (C.c_void_p, [C.c_size_t]),
     "pcd_host_free": (None, [C.c_void_p]),
     "pcd_product_chunk_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),

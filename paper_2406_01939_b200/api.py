@@ -752,3 +752,66 @@ def time_warp_simulate(instance: Instance, policy: Policy, processes: int, seed:
                 for r in trace[:min(res.trace_rows, cap)]]
         return TimeWarpResult(actions[:T].copy(), res.sync_rounds, res.rollbacks,
                               res.policy_eval_count_sequential_equivalent, res.total_policy_evals, rows)
+
+
+# ------------------------------------------------------------ theory / files
+@dataclass
+class DepletionProfile:
+    """theory::DepletionProfile (theory.hpp:30-51)."""
+    horizon: int
+    first_depleted_at: np.ndarray
+    depleted_nodes: np.ndarray
+    sorted_depletion_times: np.ndarray
+
+    def depleted_count(self) -> int:
+        return int(self.depleted_nodes.size)
+
+    def depleted_before_order(self, node: int, t: int) -> bool:
+        return bool(self.first_depleted_at[node] <= t)
+
+    def iteration_bound(self) -> int:
+        return self.depleted_count() + 1
+
+
+def depletion_profile(instance: Instance, actions, device: int = 0) -> DepletionProfile:
+    """theory::compute_depletion (theory.hpp:53-86) of the trajectory
+    ``actions`` (computed on the device)."""
+    T, J = int(instance.horizon), int(instance.nodes)
+    a = _i32(actions)
+    if a.size != T:
+        raise ContractViolation("trajectory length must equal the horizon")
+    out = np.zeros(J, np.int64)
+    cnt = C.c_int64()
+    with Simulator(instance, NullOnlyPolicy(), device) as sim:
+        _check(LIB.pcd_depletion_profile(sim._h, _ptr(a), _ptr(out, C.c_int64), C.byref(cnt)))
+    nodes = np.flatnonzero(out < T).astype(np.int32)
+    return DepletionProfile(T, out, nodes, np.sort(out))
+
+
+def check_iteration_bound(iterations_to_correct, profile: DepletionProfile):
+    """theory::check_iteration_bound (theory.hpp:228-236) -> (bound, satisfied)."""
+    bound = profile.iteration_bound()
+    return bound, iterations_to_correct is not None and iterations_to_correct <= bound
+
+
+def save_instance_binary(instance: Instance, path: str) -> None:
+    """Binary SoA instance file (pcd_save_instance_bin)."""
+    c = instance.to_c()
+    _check(LIB.pcd_save_instance_bin(C.byref(c), str(path).encode()))
+
+
+def load_instance_binary(path: str) -> Instance:
+    J, I, T, R, ho = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64(), C.c_int32()
+    _check(LIB.pcd_instance_bin_info(str(path).encode(), C.byref(J), C.byref(I), C.byref(T), C.byref(R),
+                                     C.byref(ho)))
+    J, I, T, R = J.value, I.value, T.value, R.value
+    product = np.zeros(max(T, 1), np.int32)
+    rrow = np.zeros(max(T, 1), np.int32)
+    ot = np.zeros(max(T, 1), np.int32) if ho.value else None
+    table = np.zeros(max(R * J, 1))
+    cap = np.zeros(J, np.int32)
+    inv = np.zeros(I * J, np.int32)
+    _check(LIB.pcd_load_instance_bin(str(path).encode(), _ptr(product), _ptr(rrow), _ptr(ot),
+                                     _ptr(table, C.c_double), _ptr(cap), _ptr(inv)))
+    return Instance(J, I, T, product[:T], rrow[:T], table[:R * J].reshape(R, J), cap, inv.reshape(I, J),
+                    None if ot is None else ot[:T])

@@ -1,5 +1,6 @@
 // capi.cpp — host-only entry points of the C ABI (include/picard_b200.h) and
 // the exception -> status-code translation shared with engine.cu.
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -103,6 +104,99 @@ int pcd_linear_contractive_spec(int32_t state_dim, int32_t input_dim, int64_t ho
   if (!gain || !contraction) throw pcd::InvalidArgument("null argument");
   pcd::linear_contractive_spec(state_dim, input_dim, horizon, rho, seed, state_coupling, dynamics, input,
                                disturbances, gain, contraction);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+// ---------------------------------------------------------------- binary instances
+namespace {
+struct InstHeader {
+  char magic[8];
+  int32_t nodes, products;
+  int64_t horizon, reward_rows;
+  int32_t has_order_t, pad;
+  int64_t reserved;
+};
+static_assert(sizeof(InstHeader) == 48, "header layout");
+struct File {
+  FILE* f;
+  ~File() { if (f) std::fclose(f); }
+};
+void write_all(FILE* f, const void* p, size_t bytes) {
+  if (bytes && std::fwrite(p, 1, bytes, f) != bytes) throw pcd::InvalidArgument("instance file: write failed");
+}
+void read_all(FILE* f, void* p, size_t bytes) {
+  if (bytes && std::fread(p, 1, bytes, f) != bytes) throw pcd::InvalidArgument("instance file: truncated");
+}
+InstHeader read_header(FILE* f) {
+  InstHeader h{};
+  read_all(f, &h, sizeof h);
+  if (std::memcmp(h.magic, "PCDINST1", 8) != 0) throw pcd::InvalidArgument("instance file: bad magic");
+  if (h.nodes < 1 || h.products < 1 || h.horizon < 0 || h.reward_rows < 0)
+    throw pcd::InvalidArgument("instance file: bad header");
+  return h;
+}
+}  // namespace
+
+int pcd_save_instance_bin(const pcd_instance* in, const char* path) {
+  PCD_TRY
+  if (!in || !path) throw pcd::InvalidArgument("null argument");
+  File fw{std::fopen(path, "wb")};
+  if (!fw.f) throw pcd::InvalidArgument(std::string("cannot open ") + path);
+  InstHeader h{};
+  std::memcpy(h.magic, "PCDINST1", 8);
+  h.nodes = in->nodes;
+  h.products = in->products;
+  h.horizon = in->horizon;
+  h.reward_rows = in->reward_rows;
+  h.has_order_t = in->order_t ? 1 : 0;
+  write_all(fw.f, &h, sizeof h);
+  const size_t T = (size_t)in->horizon, J = (size_t)in->nodes;
+  write_all(fw.f, in->product, T * 4);
+  write_all(fw.f, in->reward_row, T * 4);
+  if (in->order_t) write_all(fw.f, in->order_t, T * 4);
+  write_all(fw.f, in->reward_table, (size_t)in->reward_rows * J * 8);
+  write_all(fw.f, in->capacity, J * 4);
+  write_all(fw.f, in->inventory, (size_t)in->products * J * 4);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_instance_bin_info(const char* path, int32_t* nodes, int32_t* products, int64_t* horizon,
+                          int64_t* reward_rows, int32_t* has_order_t) {
+  PCD_TRY
+  if (!path) throw pcd::InvalidArgument("null argument");
+  File fr{std::fopen(path, "rb")};
+  if (!fr.f) throw pcd::InvalidArgument(std::string("cannot open ") + path);
+  const InstHeader h = read_header(fr.f);
+  if (nodes) *nodes = h.nodes;
+  if (products) *products = h.products;
+  if (horizon) *horizon = h.horizon;
+  if (reward_rows) *reward_rows = h.reward_rows;
+  if (has_order_t) *has_order_t = h.has_order_t;
+  return PCD_OK;
+  PCD_CATCH
+}
+
+int pcd_load_instance_bin(const char* path, int32_t* product, int32_t* reward_row, int32_t* order_t,
+                          double* reward_table, int32_t* capacity, int32_t* inventory) {
+  PCD_TRY
+  if (!path) throw pcd::InvalidArgument("null argument");
+  File fr{std::fopen(path, "rb")};
+  if (!fr.f) throw pcd::InvalidArgument(std::string("cannot open ") + path);
+  const InstHeader h = read_header(fr.f);
+  const size_t T = (size_t)h.horizon, J = (size_t)h.nodes;
+  if ((T && (!product || !reward_row)) || !reward_table || !capacity || !inventory)
+    throw pcd::InvalidArgument("null argument");
+  read_all(fr.f, product, T * 4);
+  read_all(fr.f, reward_row, T * 4);
+  if (h.has_order_t) {
+    if (order_t) read_all(fr.f, order_t, T * 4);
+    else if (std::fseek(fr.f, (long)(T * 4), SEEK_CUR) != 0) throw pcd::InvalidArgument("instance file: truncated");
+  }
+  read_all(fr.f, reward_table, (size_t)h.reward_rows * J * 8);
+  read_all(fr.f, capacity, J * 4);
+  read_all(fr.f, inventory, (size_t)h.products * J * 4);
   return PCD_OK;
   PCD_CATCH
 }

@@ -1381,6 +1381,47 @@ extern "C" int pcd_time_warp(pcd_handle* h, int32_t processes, uint64_t seed, in
   PCD_CATCH
 }
 
+extern "C" int pcd_depletion_profile(pcd_handle* h, const int32_t* actions, int64_t* first_depleted_at,
+                                     int64_t* depleted_count) {
+  PCD_TRY
+  if (!h || !first_depleted_at) throw InvalidArgument("null argument");
+  CK(cudaSetDevice(h->device));
+  const int64_t T = h->T;
+  const int J = h->J;
+  DBuf<int> acts, keys, start, slots;
+  DBuf<long long> out;
+  out.alloc(std::max(1, J));
+  const int* a = h->cache.p;
+  if (actions) {
+    acts.upload(actions, (size_t)std::max<int64_t>(T, 1), h->stream);
+    a = acts.p;
+  } else if (!h->cache.p) {
+    throw InvalidArgument("no resident trajectory (run pcd_simulate first or pass actions)");
+  }
+  if (T > 0) {
+    keys.alloc((size_t)T);
+    k_fulfil_keys<<<grid_for(T, 256), 256, 0, h->stream>>>(a, T, J, keys.p);
+    build_csr(h, keys.p, J + 1, start, slots);
+  } else {
+    start.alloc((size_t)J + 2);
+    CK(cudaMemsetAsync(start.p, 0, sizeof(int) * ((size_t)J + 2), h->stream));
+    slots.alloc(1);
+  }
+  k_depletion<<<(J + 127) / 128, 128, 0, h->stream>>>(start.p, slots.p, h->cap0.p, J, T, out.p);
+  CK(cudaGetLastError());
+  std::vector<long long> d((size_t)J);
+  CK(cudaMemcpyAsync(d.data(), out.p, sizeof(long long) * (size_t)J, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  int64_t cnt = 0;
+  for (int j = 0; j < J; ++j) {
+    first_depleted_at[j] = d[(size_t)j];
+    cnt += d[(size_t)j] < T;
+  }
+  if (depleted_count) *depleted_count = cnt;
+  return PCD_OK;
+  PCD_CATCH
+}
+
 extern "C" int pcd_set_history(pcd_handle* h, int32_t* history, int64_t cap_iterations) {
   if (!h) return PCD_INVALID_ARGUMENT;
   h->history = history;

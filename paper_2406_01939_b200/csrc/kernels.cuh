@@ -268,6 +268,27 @@ static __global__ void k_serial_window(DevModel model, int lo, int hi, int* __re
   for (int j = lane; j < J; j += 32) ckcap[j] = caps[j];
 }
 
+// Depletion profile: keys = node of every fulfilment (J for declines) so a
+// stable radix sort lists each node's fulfilments in time order; then
+// first_depleted_at[j] = (slot of the cap0[j]-th fulfilment) + 1, or 0 when
+// cap0[j] == 0, or T when the node never empties before the last order.
+static __global__ void k_fulfil_keys(const int* __restrict__ a, long long T, int J, int* __restrict__ keys) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+    const int v = a[t];
+    keys[t] = (v >= 0 && v < J) ? v : J;
+  }
+}
+static __global__ void k_depletion(const int* __restrict__ start, const int* __restrict__ slots,
+                                   const int* __restrict__ cap0, int J, long long T, long long* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  const int c = cap0[j], n = start[j + 1] - start[j];
+  long long d = T;
+  if (c <= 0) d = T > 0 ? 0 : T;
+  else if (n >= c) d = min(T, (long long)slots[start[j] + c - 1] + 1);
+  out[j] = d;
+}
+
 // Run structure of a plan along the product slot lists (qslots, time order
 // per product): run_start[k] = 1 where a product's list starts or the owner
 // changes.
