@@ -14,6 +14,9 @@
 //   picard::picard_simulate      engine.hpp:458-590
 //   picard::picard_iterate_once  engine.hpp:358-444
 //   picard::sequential_simulate  engine.hpp:237-267
+// and, when the reference's headers are on the include path,
+//   picard::timewarp::time_warp_simulate    fo/timewarp.hpp:56-181
+//   picard::linear::picard_convergence_curve linear.cpp:279-330
 // for FoEnv x {GreedyPolicy, CapacityPenalizedPolicy, DualNetworkPolicy}.
 // Observers are not supported on the device path (they need per-step host
 // callbacks); the per-iteration cache history is available through
@@ -267,6 +270,86 @@ SequentialOutput<fo::FoAction> sequential_simulate(const fo::FoEnv& env, const P
   out.policy_evals = evals;
   return out;
 }
+
+#if __has_include("picard/fo/timewarp.hpp")
+}  // namespace picard::b200
+#include "picard/fo/timewarp.hpp"
+namespace picard::b200 {
+// timewarp::time_warp_simulate (fo/timewarp.hpp:56-181) on the B200: same
+// arguments, same TimeWarpResult (actions, counters, trace), same errors.
+template <typename P>
+timewarp::TimeWarpResult time_warp_simulate(const fo::Instance& instance, const P& policy, std::int32_t processes,
+                                            std::uint64_t seed, bool record_trace = false,
+                                            timewarp::WindowRule rule = timewarp::WindowRule::min_capacity,
+                                            DualNormalization norm = {}, int device = 0) {
+  const auto env = instance.make_env();
+  const std::span<const fo::Order> orders(instance.orders);
+  auto m = detail::marshal(env, orders);
+  auto ps = detail::policy_spec(policy, m, norm);
+  detail::Handle h(m.view, ps.view, device);
+  std::vector<std::int32_t> actions(orders.size());
+  std::vector<pcd_tw_trace_row> rows(record_trace ? 2 * orders.size() + 4 : 1);
+  pcd_tw_result res{};
+  const int rc = pcd_time_warp(h.h, processes, seed, rule == timewarp::WindowRule::min_stocked_capacity ? 1 : 0,
+                               record_trace ? 1 : 0, actions.data(), &res, rows.data(),
+                               record_trace ? static_cast<std::int64_t>(rows.size()) : 0);
+  if (rc) detail::raise(rc);
+  timewarp::TimeWarpResult out;
+  for (auto a : actions) out.actions.push_back(fo::FoAction{a});
+  out.sync_rounds = res.sync_rounds;
+  out.rollbacks = res.rollbacks;
+  out.policy_eval_count_sequential_equivalent = res.policy_eval_count_sequential_equivalent;
+  out.total_policy_evals = res.total_policy_evals;
+  if (record_trace)
+    for (std::int64_t i = 0; i < res.trace_rows && i < static_cast<std::int64_t>(rows.size()); ++i) {
+      const auto& r = rows[static_cast<std::size_t>(i)];
+      out.trace.push_back({r.round, r.t_start, r.window_length, r.max_process_evals, r.rolled_back != 0});
+    }
+  return out;
+}
+#endif
+
+#if __has_include("picard/linear.hpp")
+}  // namespace picard::b200
+#include "picard/linear.hpp"
+namespace picard::b200 {
+// linear::picard_convergence_curve (linear.cpp:279-330) on the B200: the
+// GainPolicy system under single-step partitions, one affine time-scan per
+// iteration; curve values within 1e-9 relative of the reference's.
+inline std::vector<double> picard_convergence_curve(const linear::LinearSystemSpec& spec,
+                                                    std::span<const std::vector<double>> initial_cache = {},
+                                                    const linear::ConvergenceCurveOptions& options = {},
+                                                    int device = 0) {
+  spec.validate();
+  const auto n = static_cast<std::size_t>(spec.state_dim), p = static_cast<std::size_t>(spec.input_dim);
+  const auto T = static_cast<std::size_t>(spec.horizon);
+  std::vector<double> A, B, W, init;
+  A.reserve(T * n * n);
+  B.reserve(T * n * p);
+  W.reserve(T * n);
+  for (std::size_t t = 0; t < T; ++t) {
+    A.insert(A.end(), spec.dynamics[t].begin(), spec.dynamics[t].end());
+    B.insert(B.end(), spec.input[t].begin(), spec.input[t].end());
+    W.insert(W.end(), spec.disturbances[t].begin(), spec.disturbances[t].end());
+  }
+  if (!initial_cache.empty()) {
+    if (initial_cache.size() != T) throw ContractViolation("initial cache length must equal the horizon");
+    for (const auto& a : initial_cache) init.insert(init.end(), a.begin(), a.end());
+  }
+  const pcd_linear_spec c{spec.state_dim, spec.input_dim, spec.horizon, A.data(), B.data(), W.data(),
+                          spec.gain.data()};
+  const std::int64_t cap = options.max_iterations > 0 ? options.max_iterations : spec.horizon;
+  std::vector<double> curve(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)));
+  std::int64_t len = 0;
+  const int rc = pcd_linear_convergence_curve(
+      &c, init.empty() ? nullptr : init.data(), options.tolerance, options.max_iterations,
+      options.normalization == linear::RmseNormalization::draft ? 1 : 0, device, curve.data(),
+      static_cast<std::int64_t>(curve.size()), &len, nullptr, nullptr);
+  if (rc) detail::raise(rc);
+  curve.resize(static_cast<std::size_t>(len));
+  return curve;
+}
+#endif
 
 // Product-chunk plan (no reference counterpart; pcd_product_chunk_partition):
 // every product's orders cut into contiguous near-equal chunks, one process

@@ -168,6 +168,42 @@ int main() {
     compare(inst, CapacityPenalizedPolicy{0.7}, plan, {});
     if (seed % 2 == 0) compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, seed), plan, {});
   }
+  // Time Warp (fo/timewarp.hpp) through the drop-in vs the unmodified reference
+  for (std::uint64_t seed = 60; seed < 66; ++seed) {
+    const auto inst = small_random(seed);
+    for (auto rule : {timewarp::WindowRule::min_capacity, timewarp::WindowRule::min_stocked_capacity}) {
+      auto check_tw = [&](const auto& policy) {
+        const auto want = timewarp::time_warp_simulate(inst, policy, 4, seed, true, rule);
+        const auto got = b200::time_warp_simulate(inst, policy, 4, seed, true, rule);
+        CHECK(got.actions == want.actions);
+        CHECK(got.sync_rounds == want.sync_rounds);
+        CHECK(got.rollbacks == want.rollbacks);
+        CHECK(got.policy_eval_count_sequential_equivalent == want.policy_eval_count_sequential_equivalent);
+        CHECK(got.total_policy_evals == want.total_policy_evals);
+        CHECK(got.trace.size() == want.trace.size());
+        for (std::size_t i = 0; i < std::min(got.trace.size(), want.trace.size()); ++i) {
+          CHECK(got.trace[i].t_start == want.trace[i].t_start);
+          CHECK(got.trace[i].window_length == want.trace[i].window_length);
+          CHECK(got.trace[i].max_process_evals == want.trace[i].max_process_evals);
+          CHECK(got.trace[i].rolled_back == want.trace[i].rolled_back);
+        }
+      };
+      check_tw(GreedyPolicy{});
+      check_tw(CapacityPenalizedPolicy{5.0});
+      check_tw(DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, seed));
+    }
+  }
+  // linear env convergence curve (linear.cpp:279-330) vs the unmodified reference
+  for (double coupling : {0.0, 0.4}) {
+    const auto spec = linear::make_contractive_spec(4, 3, 400, 0.6, 17, coupling);
+    linear::ConvergenceCurveOptions o;
+    o.tolerance = 1e-7;
+    const auto want = linear::picard_convergence_curve(spec, {}, o);
+    const auto got = b200::picard_convergence_curve(spec, {}, o);
+    CHECK(got.size() == want.size());
+    for (std::size_t k = 0; k < std::min(got.size(), want.size()); ++k)
+      CHECK(std::abs(got[k] - want[k]) <= 1e-9 * std::max(1.0, std::abs(want[k])));
+  }
   // iteration cap (test_engine.cpp:525-545)
   {
     const auto inst = toy();
