@@ -196,7 +196,7 @@ struct pcd_handle {
   // tensor-core policy (tc_sweep.cu)
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   pcd::DBuf<unsigned char> tc_wimg;
-  pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf;
+  pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf, tc_rtq;
   pcd::DBuf<unsigned long long> tc_stats;
   int32_t tc_tiles = 0;
   int64_t max_load = 0;
@@ -432,7 +432,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   }
   a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
-  a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p;
+  a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p; a.rtabq = h->tc_rtq.p;
   a.guard = (float)(guard > 0 ? guard : 5e-5);
   a.verify = verify;
   a.stats = h->tc_stats.p;
@@ -917,6 +917,13 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
   for (int64_t rr = 0; rr < h->R; ++rr)
     for (int j = 0; j < J; ++j) rtf[(size_t)rr * RJ + j] = (float)rtab[(size_t)rr * J + j];
   h->tc_rtf.upload(rtf.data(), rtf.size(), h->stream);
+  // score = r - (q + b3) is computed as (r - b3) - q: one rounding of the
+  // FP64 difference instead of a bias add per node per step
+  std::vector<float> rtq((size_t)h->R * RJ, 0.f);
+  for (int64_t rr = 0; rr < h->R; ++rr)
+    for (int j = 0; j < J; ++j)
+      rtq[(size_t)rr * RJ + j] = (float)(rtab[(size_t)rr * J + j] - (pol->b3[j] + pol->b3[J + j]));
+  h->tc_rtq.upload(rtq.data(), rtq.size(), h->stream);
   h->tc_stats.alloc(4);
   CK(cudaStreamSynchronize(h->stream));
   h->tc_ok = true;

@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   float* sInvC0 = (float*)(smem + Layout::cst);
   float* sB1 = sInvC0 + kScrJ;
   float* sB2 = sB1 + 64;
-  float* sB3 = sB2 + 64;
   const int tile = blockIdx.x;
   // half / row / node-group of this thread
   const int h = warp >> 3, wq = warp & 7, q = wq & 3, p2 = wq >> 2, th = lane >> 4;
@@ -363,7 +362,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     sB1[i] = a.b1f[i];
     sB2[i] = a.b2f[i];
   }
-  for (int i = tid; i < kTcN3; i += kBlock) sB3[i] = a.b3f[i];
   const int nq = a.wctl[0], dealt = (int)gridDim.x * kTcRows;
   auto begin_proc = [&](int* inf, int m) {
     int pos = 0, end = 0;
@@ -697,7 +695,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     // this thread's reward loads while layer 3 runs
     uint32_t rwv[kMaxCI][8];
     {
-      const float* rw = a.rtabf + (size_t)(fmask ? inf[RI_RR] : 0) * RJ;
+      const float* rw = a.rtabq + (size_t)(fmask ? inf[RI_RR] : 0) * RJ;
 #pragma unroll
       for (int i = 0; i < kMaxCI; ++i) {
         if ((fmask >> (8 * i)) & 0xffu) {
@@ -716,9 +714,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
     // ============================ S: scores, argmax, margin (row, group)
     {
-      float v1 = -INFINITY, v2 = -INFINITY;
+      float v1 = -INFINITY, v2 = -INFINITY, ssum = 0.f;  // ssum: non-finite iff some score is (or overflow: flagged, safe)
       int i1 = -1;
-      bool bad = false;
       if (qact) {
 #pragma unroll
         for (int i0 = 0; i0 < kMaxCI; i0 += 2) {
@@ -740,15 +737,16 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               if (!((fmask >> (8 * i + k)) & 1u)) continue;  // feasible implies node < J
-              const float qv = fmaf(__uint_as_float(vx[u][k]), kLoInv, __uint_as_float(vh[u][k])) + sB3[j0 + k];
+              const float qv = fmaf(__uint_as_float(vx[u][k]), kLoInv, __uint_as_float(vh[u][k]));
               const float sc = __uint_as_float(rwv[i][k]) - qv;
-              if (!isfinite(sc)) bad = true;
+              ssum += sc;
               if (sc > v1) { v2 = v1; v1 = sc; i1 = j0 + k; }
               else if (sc > v2) v2 = sc;
             }
           }
         }
       }
+      const bool bad = !isfinite(ssum);
       float* bs = sBest + R * 12 + g * 3;
       bs[0] = v1;
       bs[1] = __int_as_float(bad ? -2 : i1);

@@ -57,6 +57,7 @@ struct TcArgs {
   const float* inv_c0;  // [J]
   const float* inv_x0;  // [I*J]
   const float* rtabf;   // [R*J] rewards in fp32 (scores of the tensor-core path)
+  const float* rtabq;   // [R*J] rewards minus the combined output bias b3f, in fp32 (ping-pong sweep)
   float guard;
   int verify;           // debug: exact re-evaluation of every row
   long long* prof;      // debug: per-phase clock64 totals of CTA 0 (or nullptr)
