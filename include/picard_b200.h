@@ -68,13 +68,17 @@ enum {
 
 /* Sweep engine selection for pcd_simulate / pcd_iterate_once. */
 enum {
-  PCD_ENGINE_AUTO = 0,          /* closed form when the plan is a run partition;
-                                   tensor-core policy when eligible               */
+  PCD_ENGINE_AUTO = 0,          /* run-partition closed form when the plan is a run
+                                   partition (tensor-core policy when eligible),
+                                   else the general closed form                   */
   PCD_ENGINE_REPLAY = 1,        /* exact per-process window replay (any plan)     */
   PCD_ENGINE_PRODUCT = 2,       /* closed-form run-partition sweep (checked): each
                                    process owns one contiguous stretch of a
                                    product's orders, or only whole products      */
-  PCD_ENGINE_PRODUCT_FP64 = 3   /* ... with the FP64 SIMT policy only             */
+  PCD_ENGINE_PRODUCT_FP64 = 3,  /* ... with the FP64 SIMT policy only             */
+  PCD_ENGINE_GENERAL = 4        /* closed form for any plan and any cache: every
+                                   process walks only its own slots (FP64 SIMT
+                                   policy); AUTO's choice for non-run plans       */
 };
 
 /* A fulfillment-optimization instance (fo/instance.hpp:25-37). */
@@ -158,7 +162,7 @@ typedef struct pcd_timing {
   int64_t sweep_launches;
   int64_t steps_critical; /* sum over iterations of max per-process evals */
   int64_t total_evals;
-  int32_t engine_used;    /* PCD_ENGINE_REPLAY / PRODUCT / PRODUCT_FP64 */
+  int32_t engine_used;    /* PCD_ENGINE_REPLAY / PRODUCT / PRODUCT_FP64 / GENERAL */
   int32_t device;
   int64_t tc_rows;        /* policy evaluations through the tcgen05 path */
   int64_t tc_flagged;     /* ... re-evaluated exactly (margin < guard) */

@@ -19,7 +19,7 @@ F64P = C.POINTER(C.c_double)
 
 PCD_OK, PCD_INVALID_ARGUMENT, PCD_CONTRACT_VIOLATION, PCD_ITERATION_LIMIT, PCD_CUDA_ERROR = range(5)
 PCD_POLICY_GREEDY, PCD_POLICY_CAPACITY, PCD_POLICY_DUAL, PCD_POLICY_NULL = range(4)
-PCD_ENGINE_AUTO, PCD_ENGINE_REPLAY, PCD_ENGINE_PRODUCT, PCD_ENGINE_PRODUCT_FP64 = range(4)
+PCD_ENGINE_AUTO, PCD_ENGINE_REPLAY, PCD_ENGINE_PRODUCT, PCD_ENGINE_PRODUCT_FP64, PCD_ENGINE_GENERAL = range(5)
 
 
 class pcd_linear_spec(C.Structure):

@@ -44,7 +44,7 @@ from . import _capi as K
 LIB = K.LIB
 NO_FULFILL = -1
 ENGINES = {"auto": K.PCD_ENGINE_AUTO, "replay": K.PCD_ENGINE_REPLAY, "product": K.PCD_ENGINE_PRODUCT,
-           "product_fp64": K.PCD_ENGINE_PRODUCT_FP64}
+           "product_fp64": K.PCD_ENGINE_PRODUCT_FP64, "general": K.PCD_ENGINE_GENERAL}
 
 
 # ------------------------------------------------------------------ errors
@@ -380,7 +380,7 @@ class DualNetworkPolicy(Policy):
 # ------------------------------------------------------------ config/result
 @dataclass
 class PicardConfig:
-    """PicardConfig (engine.hpp:120-126) + ``engine`` ("auto"/"replay"/"product")."""
+    """PicardConfig (engine.hpp:120-126) + ``engine`` ("auto"/"replay"/"product"/"product_fp64"/"general")."""
     processes: int = 0
     max_steps: int = 0
     max_iterations: int = 0

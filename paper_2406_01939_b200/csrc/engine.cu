@@ -24,6 +24,7 @@
 #include <cuda_fp16.h>
 
 #include "capi_internal.h"
+#include "general.cuh"
 #include "kernels.cuh"
 #include "tc_sweep.cuh"
 
@@ -186,6 +187,12 @@ struct pcd_handle {
   pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, segtot, scratch, tau;
   pcd::DBuf<unsigned char> written;
   pcd::DBuf<long long> evals;
+  // general closed form (general.cuh): same-product chains of the plan,
+  // per-iteration (product, node) entry lists, per-position actions, deltas
+  bool gen_plan = false;
+  pcd::DBuf<int> gprev, gkeys, gkeys_s, gvals, gslots, gstart, ocache, ofresh;
+  pcd::DBuf<int4> gdl;
+  pcd::DBuf<unsigned char> gtmp;
   pcd::Scalars* scal = nullptr;  // device
   pcd::Scalars* h_scal = nullptr;  // pinned host
   long long* d_errt = nullptr;
@@ -464,6 +471,105 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   }
 }
 
+// Effective attempts of the frozen cache and their checkpointed per-node
+// prefix counts H (k_effective, k_seg_*, k_hist_prefix); returns the row count.
+static int build_hck(pcd_handle* h, int lo, int hi) {
+  const int J = h->J;
+  const int wpb = 8;  // warps (products) per block
+  const int pgrid = (h->I + wpb - 1) / wpb;
+  k_effective<<<pgrid, wpb * 32, (size_t)wpb * 2 * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi,
+                                                                   h->cache.p, h->ckinv.p, J, h->ev.p);
+  const int nb = hck_rows(lo, hi);
+  const int nseg = (nb + kSegRows - 1) / kSegRows;
+  const size_t hsm = (size_t)kSegRows * J * 4;
+  static size_t hsm_set = 0;
+  if (hsm > 48 * 1024 && hsm > hsm_set) {
+    CK(cudaFuncSetAttribute(k_hist_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    hsm_set = hsm;
+  }
+  k_seg_count<<<nseg, 256, (size_t)J * 4, h->stream>>>(h->ev.p, lo, hi, J, h->seg.p);
+  {
+    const int nblk = std::max(1, std::min(256, nseg));
+    h->segtot.alloc((size_t)nblk * seg_stride(J));
+    k_seg_scan_a<<<nblk, 128, 0, h->stream>>>(h->seg.p, nseg, J, h->segtot.p);
+    k_seg_scan_b<<<seg_stride(J), 256, 0, h->stream>>>(h->segtot.p, nblk, J);
+    k_seg_scan_c<<<nblk, 128, 0, h->stream>>>(h->seg.p, nseg, J, h->segtot.p);
+  }
+  k_hist_prefix<<<nseg, 256, hsm, h->stream>>>(h->ev.p, lo, hi, J, nb, h->seg.p, h->hck.p);
+  CK(cudaGetLastError());
+  h->timing.kernel_launches += 6;
+  return nb;
+}
+
+// General closed form: same-product chains of the plan (once per plan) and the
+// window's entry lists by (product, node) (every iteration).
+static void build_gen_lists(pcd_handle* h, int lo, int hi) {
+  const int64_t T = h->T;
+  const int W = hi - lo;
+  if (!h->gen_plan) {
+    h->gprev.alloc((size_t)std::max<int64_t>(T, 1));
+    h->ocache.alloc((size_t)std::max<int64_t>(T, 1));
+    h->ofresh.alloc((size_t)std::max<int64_t>(T, 1));
+    h->gdl.alloc(2 * (size_t)std::max<int64_t>(T, 1));
+    if (T > 0) {
+      DBuf<int> k0, v0, k1, v1;
+      k0.alloc(T); v0.alloc(T); k1.alloc(T); v1.alloc(T);
+      k_plan_pkeys<<<grid_for(T, 256), 256, 0, h->stream>>>(h->pslots.p, h->product.p, T, k0.p, v0.p);
+      int bits = 1;
+      while ((1LL << bits) < (long long)h->I) ++bits;
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, v0.p, v1.p, (int)T, 0, bits, h->stream));
+      h->gtmp.alloc(tb);
+      CK(cub::DeviceRadixSort::SortPairs(h->gtmp.p, tb, k0.p, k1.p, v0.p, v1.p, (int)T, 0, bits, h->stream));
+      k_prev_same<<<grid_for(T, 256), 256, 0, h->stream>>>(k1.p, v1.p, h->pslots.p, h->owner.p, T, h->gprev.p);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    h->gen_plan = true;
+  }
+  const long long nkeys = (long long)h->I * h->J + 1;  // + the null bucket
+  if (nkeys >= INT32_MAX) throw InvalidArgument("general engine: products x nodes must fit int32");
+  h->gstart.alloc((size_t)nkeys + 1);
+  h->gkeys.alloc((size_t)std::max(W, 1)); h->gkeys_s.alloc((size_t)std::max(W, 1));
+  h->gvals.alloc((size_t)std::max(W, 1)); h->gslots.alloc((size_t)std::max(W, 1));
+  k_gen_keys<<<grid_for(W, 256), 256, 0, h->stream>>>(h->cache.p, h->product.p, lo, hi, h->J, (int)(nkeys - 1),
+                                                     h->gkeys.p, h->gvals.p);
+  int bits = 1;
+  while ((1LL << bits) < nkeys) ++bits;
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->gkeys.p, h->gkeys_s.p, h->gvals.p, h->gslots.p, W, 0, bits,
+                                     h->stream));
+  h->gtmp.alloc(tb);
+  CK(cub::DeviceRadixSort::SortPairs(h->gtmp.p, tb, h->gkeys.p, h->gkeys_s.p, h->gvals.p, h->gslots.p, W, 0, bits,
+                                     h->stream));
+  k_csr_starts<<<(int)((W + 1 + 255) / 256), 256, 0, h->stream>>>(h->gkeys_s.p, W, (int)nkeys, h->gstart.p);
+  CK(cudaGetLastError());
+  h->timing.kernel_launches += 5;
+}
+
+template <int KIND>
+static void launch_general_sweep(pcd_handle* h, int lo, int hi, long long* evals_out) {
+  GenArgs a{};
+  a.model = h->model();
+  a.M = h->M; a.J = h->J; a.lo = lo; a.hi = hi;
+  a.pstart = h->pstart.p; a.pslots = h->pslots.p; a.prev = h->gprev.p;
+  a.ckcap = h->ckcap.p; a.ckinv = h->ckinv.p; a.hck = h->hck.p; a.ev = h->ev.p;
+  a.gstart = h->gstart.p; a.gslots = h->gslots.p;
+  a.ocache = h->ocache.p; a.ofresh = h->ofresh.p; a.dl = h->gdl.p;
+  a.cache = h->cache.p; a.written = h->written.p; a.ref = h->ref.n ? h->ref.p : nullptr;
+  a.scal = h->scal; a.evals_out = evals_out;
+  a.mine = h->comm ? h->d_mine.p : nullptr;
+  const int wpb = 4;
+  const size_t smem = gen_warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
+  static bool attr_set[4] = {false, false, false, false};
+  if (smem > 48 * 1024 && !attr_set[KIND]) {
+    CK(cudaFuncSetAttribute(k_sweep_general<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set[KIND] = true;
+  }
+  k_sweep_general<KIND><<<(h->M + wpb - 1) / wpb, wpb * 32, smem, h->stream>>>(a);
+  CK(cudaGetLastError());
+}
+
 static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
                              double guard = 0.0, int verify = 0) {
   IterOut out;
@@ -471,36 +577,30 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   reset_scalars(h);
   if (W <= 0) return out;
   PhaseTimer tm(h->stream);
-  if (engine == PCD_ENGINE_PRODUCT || engine == PCD_ENGINE_PRODUCT_FP64) {
+  if (engine == PCD_ENGINE_GENERAL) {
+    tm.start();
+    build_hck(h, lo, hi);
+    build_gen_lists(h, lo, hi);
+    h->timing.prep_ms += tm.stop_ms();
+    tm.start();
+    dispatch_kind(h->kind, [&](auto k) { launch_general_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
+    exchange(h, h->cache.p, true);  // N>1: owned slots + convergence scalars
+    if (h->comm) CK(cudaMemsetAsync(h->written.p + lo, 1, (size_t)W, h->stream));
+    h->timing.sweep_ms += tm.stop_ms();
+    h->timing.kernel_launches += 1;
+    h->timing.sweep_launches += 1;
+  } else if (engine == PCD_ENGINE_PRODUCT || engine == PCD_ENGINE_PRODUCT_FP64) {
     tm.start();
     const int J = h->J;
     const int wpb = 8;  // warps (products) per block
     const int pgrid = (h->I + wpb - 1) / wpb;
-    k_effective<<<pgrid, wpb * 32, (size_t)wpb * 2 * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi,
-                                                                     h->cache.p, h->ckinv.p, J, h->ev.p);
-    const int nb = hck_rows(lo, hi);
-    const int nseg = (nb + kSegRows - 1) / kSegRows;
-    const size_t hsm = (size_t)kSegRows * J * 4;
-    static size_t hsm_set = 0;
-    if (hsm > 48 * 1024 && hsm > hsm_set) {
-      CK(cudaFuncSetAttribute(k_hist_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-      hsm_set = hsm;
-    }
-    k_seg_count<<<nseg, 256, (size_t)J * 4, h->stream>>>(h->ev.p, lo, hi, J, h->seg.p);
-    {
-      const int nblk = std::max(1, std::min(256, nseg));
-      h->segtot.alloc((size_t)nblk * seg_stride(J));
-      k_seg_scan_a<<<nblk, 128, 0, h->stream>>>(h->seg.p, nseg, J, h->segtot.p);
-      k_seg_scan_b<<<seg_stride(J), 256, 0, h->stream>>>(h->segtot.p, nblk, J);
-      k_seg_scan_c<<<nblk, 128, 0, h->stream>>>(h->seg.p, nseg, J, h->segtot.p);
-    }
-    k_hist_prefix<<<nseg, 256, hsm, h->stream>>>(h->ev.p, lo, hi, J, nb, h->seg.p, h->hck.p);
+    const int nb = build_hck(h, lo, hi);
     k_tau<<<(J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
     k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
                                                                  h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
     CK(cudaGetLastError());
     h->timing.prep_ms += tm.stop_ms();
-    h->timing.kernel_launches += 8;
+    h->timing.kernel_launches += 2;
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {
@@ -584,13 +684,14 @@ static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to) {
 }
 
 static int choose_engine(pcd_handle* h, int requested) {
-  if (requested == PCD_ENGINE_REPLAY) return PCD_ENGINE_REPLAY;
+  if (requested == PCD_ENGINE_REPLAY || requested == PCD_ENGINE_GENERAL) return requested;
   if (requested == PCD_ENGINE_PRODUCT || requested == PCD_ENGINE_PRODUCT_FP64) {
     if (!h->is_product)
       throw InvalidArgument("engine=PRODUCT requires a run partition (each process owns one contiguous stretch of a product's orders, or whole products)");
     return requested;
   }
-  return h->is_product ? PCD_ENGINE_PRODUCT : PCD_ENGINE_REPLAY;
+  if (requested != PCD_ENGINE_AUTO) throw InvalidArgument("unknown engine " + std::to_string(requested));
+  return h->is_product ? PCD_ENGINE_PRODUCT : PCD_ENGINE_GENERAL;
 }
 
 static void ensure_state_buffers(pcd_handle* h) {
@@ -1073,6 +1174,7 @@ extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
     if ((double)nr * h->J * 4 > 8e9) hf = 1;
   }
   h->is_product = hf == 0;
+  h->gen_plan = false;
   h->have_plan = true;
   ensure_state_buffers(h);
   rebuild_shards(h);

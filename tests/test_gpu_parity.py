@@ -56,6 +56,25 @@ def test_replay_engine_matches_reference_golden(name, case):
     check(case, r)
 
 
+@pytest.mark.parametrize("name,case", CASES, ids=[n for n, _ in CASES])
+def test_general_engine_matches_reference_golden(name, case):
+    """The general closed form (any plan, any cache) on every golden case,
+    run partitions included."""
+    _, r = run_gpu(case, "general")
+    check(case, r)
+    assert r.timing["engine_used"] == 4
+
+
+def test_auto_engine_choice(golden):
+    """AUTO: run partitions take the run-partition closed form, every other
+    plan the general closed form."""
+    for name, case in CASES[::4]:
+        owner = np.array(case["owner"])
+        prod = oracle_instance(case["instance"], ORC).product
+        _, r = run_gpu(case, "auto", history=False)
+        assert r.timing["engine_used"] == (2 if is_run_partition(owner, prod) else 4), name
+
+
 def test_product_engine_is_used_for_product_partitions(golden):
     """engine=PRODUCT on every golden case: run partitions (product partitions
     and any plan whose per-product stretches qualify) give the golden result,
@@ -89,7 +108,7 @@ def test_toy_iterate_once_hand_trace(golden):
     assert P.sequential_simulate(toy, P.GreedyPolicy()).actions.tolist() == [0, 1]
 
 
-@pytest.mark.parametrize("engine", ["replay", "auto"])
+@pytest.mark.parametrize("engine", ["replay", "auto", "general"])
 def test_iterate_once_random_caches_match_oracle(engine):
     """Arbitrary (even garbage) caches, windows and checkpoints: one iteration
     must reproduce picard_iterate_once exactly (engine.hpp:358-444)."""
@@ -435,6 +454,28 @@ def test_tensor_core_and_fp64_sweeps_agree_with_warm_start_and_windows():
         assert [x.astuple() for x in a.trace] == [x.astuple() for x in b.trace]
 
 
+@pytest.mark.parametrize("J,I,T,M,kind", [(10, 100, 6000, 64, 2), (30, 300, 8000, 200, 2), (12, 50, 5000, 40, 0),
+                                           (12, 50, 5000, 40, 1), (6, 20, 4000, 7, 2)])
+def test_general_engine_uniform_plans_match_replay(J, I, T, M, kind):
+    """Uniform plans (not run partitions): the general closed form reproduces
+    the exact replay sweep iteration by iteration and converges to the serial
+    trajectory."""
+    ons = NS(**ORC.generate_instance_arrays(J, I, T, 0.0, 0.8, 3, geometry=0))
+    inst = product_instance(ons)
+    owner = ORC.uniform_partition(T, M, 2)
+    spec = dict(kind=kind, gamma=1.3, seed=5)
+    opol, pol = oracle_policy(spec, ons, ORC), product_policy(spec, inst)
+    seq, _ = ORC.sequential(ons, opol)
+    rs = {e: P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(record_trace=True, engine=e),
+                               reference_actions=seq) for e in ("replay", "general")}
+    for r in rs.values():
+        assert r.actions.tolist() == seq.tolist()
+    assert [x.astuple() for x in rs["general"].trace] == [x.astuple() for x in rs["replay"].trace]
+    assert (rs["general"].conflicts, rs["general"].total_policy_evals) == (rs["replay"].conflicts,
+                                                                         rs["replay"].total_policy_evals)
+    assert rs["general"].timing["engine_used"] == 4
+
+
 def test_cpp_dropin_matches_reference_engine():
     """The reference's own engine scenarios through include/picard_b200.hpp,
     checked against the UNMODIFIED reference CPU engine (tests/cpp)."""
@@ -456,7 +497,7 @@ def test_single_rank_nccl_path_matches():
     want = P.picard_simulate(inst, pol, P.PartitionPlan(256, owner), P.PicardConfig(record_trace=True),
                              reference_actions=seq)
     uid = P.nccl_unique_id()
-    for engine in ("auto", "product_fp64", "replay"):
+    for engine in ("auto", "product_fp64", "replay", "general"):
         with P.Simulator(inst, pol) as sim:
             sim.set_plan(P.PartitionPlan(256, owner))
             sim.attach_comm(uid if engine == "auto" else P.nccl_unique_id(), 0, 1)
