@@ -540,7 +540,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         uint32_t dv[8];
         ld8s(tmem + tl + kColD + 16 * p2 + 32 * i, dv);
         tmem_wait_ld();
-        const int eE = ciE == i ? (evt & 7) : -1, eX = ciX == i ? (xu & 7) : -1;
+        // D deltas of the chunk as biased nibbles (1 + [k == evt] - [k == xu]); dres clears D
+        const uint32_t dpk = 0x11111111u + (ciE == i ? 1u << (4 * (evt & 7)) : 0u) - (ciX == i ? 1u << (4 * (xu & 7)) : 0u);
+        const uint32_t dmask = dres ? 0u : 0xffffffffu;
         const int4 cp0 = *(const int4*)(sCap + jc), cp1 = *(const int4*)(sCap + jc + 4);
         const float4 iv0 = *(const float4*)(sInvC0 + jc), iv1 = *(const float4*)(sInvC0 + jc + 4);
         const int capv[8] = {cp0.x, cp0.y, cp0.z, cp0.w, cp1.x, cp1.y, cp1.z, cp1.w};
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
         float fv[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int d = (dres ? 0 : (int)dv[k]) + (k == eE ? 1 : 0) - (k == eX ? 1 : 0);
+          const int d = (int)(dv[k] & dmask) + (int)((dpk >> (4 * k)) & 15u) - 1;
           dv[k] = (uint32_t)d;
           const int cc = max(capv[k] - (int)hv[i][k] + d - (int)((pk[i] >> (4 * k)) & 15u), 0);
           cv[k] = (uint32_t)cc;
