@@ -122,7 +122,9 @@ typedef struct pcd_config {
   int32_t threads;         /* accepted for API parity; the device ignores it */
   int32_t engine;          /* PCD_ENGINE_* */
   double tc_guard;         /* tensor-core decision margin below which a row is
-                              re-evaluated in exact FP64 (0 = default 5e-5)   */
+                              re-evaluated in exact FP64 (0 = default: 5e-5,
+                              scaled up for policies with larger weights or
+                              features than the reference's seeded ones)      */
   int32_t tc_verify;       /* debug: re-evaluate EVERY row in FP64 and count
                               unflagged disagreements (pcd_timing.tc_unflagged_bad) */
   int32_t reserved;

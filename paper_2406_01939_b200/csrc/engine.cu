@@ -202,6 +202,7 @@ struct pcd_handle {
   int64_t history_cap = 0;
   // tensor-core policy (tc_sweep.cu)
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
+  double tc_guard = 5e-5;                // tc_scaled_guard
   pcd::DBuf<unsigned char> tc_wimg;
   pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf, tc_rtq;
   pcd::DBuf<unsigned long long> tc_stats;
@@ -440,7 +441,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p; a.rtabq = h->tc_rtq.p;
-  a.guard = (float)(guard > 0 ? guard : 5e-5);
+  a.guard = (float)(guard > 0 ? guard : h->tc_guard);
   a.verify = verify;
   a.stats = h->tc_stats.p;
   static const int pf = getenv("PCD_TC_PF") ? atoi(getenv("PCD_TC_PF")) : 0;  // tuning knob
@@ -949,6 +950,70 @@ static void exchange(pcd_handle* h, int* buf, bool reduce) {
 // with g(n) = n u / (1 - n u), u = 2^-53; the fast path needs both decision
 // margins above 4E (pp::half_recheck). Returns 4E, or 0 (fast path off) when
 // the bound is not small.
+// Guard of the tensor-core sweep for this policy and instance, or 0 when the
+// tensor-core path must not be used. The fp16x3 / fp32 scores carry an error
+// proportional to the magnitudes flowing through the network; the default
+// guard 5e-5 was validated (verify mode: every row re-evaluated in FP64, 0
+// unflagged disagreements) on the reference's seeded policies, U(-0.1, 0.1)
+// weights and features <= 1. Other policies get the guard scaled by the
+// ratio of their first-order error propagation
+//   E = A3 (A2 Z1 + Z2) + Z3,  Z1 = max_n (fmax sum_c |W1| + |b1|), Z2 = max_n (sum |W2| + |b2|),
+//   A2 = max_n sum |W2|,  A3 / Z3 = max_j sum_l |W3'| (+ |b3'| + rmax)
+// to the seeded one. Non-finite weights (the reference reports a non-finite
+// score), weights outside the fp16 hi/lo split's range, huge features or a
+// guard so large that most rows would be re-evaluated keep the FP64 path.
+static double tc_scaled_guard(const pcd_policy* pol, const pcd_instance* in, const int32_t* pcap,
+                              const int32_t* pinv, int64_t horizon, int J, int H) {
+  const int inw = 2 * J + 1;
+  double wmax = 0;
+  auto scan = [&](const double* w, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+      if (!std::isfinite(w[i])) return false;
+      wmax = std::max(wmax, std::fabs(w[i]));
+    }
+    return true;
+  };
+  if (!scan(pol->w1, (size_t)H * inw) || !scan(pol->b1, H) || !scan(pol->w2, (size_t)H * H) || !scan(pol->b2, H) ||
+      !scan(pol->w3, (size_t)2 * J * H) || !scan(pol->b3, 2 * J))
+    return 0.0;
+  if (wmax > 3.0e4) return 0.0;
+  // largest feature: c / c0, x / x0 (states never exceed the instance's), t / T
+  double fmax = 1.0, rmax = 0.0;
+  for (int j = 0; j < J; ++j)
+    if (pcap[j] > 0) fmax = std::max(fmax, (double)in->capacity[j] / pcap[j]);
+  for (size_t i = 0; i < (size_t)in->products * J; ++i)
+    if (pinv[i] > 0) fmax = std::max(fmax, (double)in->inventory[i] / pinv[i]);
+  if (horizon > 0) {
+    double tmax = (double)std::max<int64_t>(in->horizon - 1, 0);
+    if (in->order_t)
+      for (int64_t t = 0; t < in->horizon; ++t) tmax = std::max(tmax, (double)in->order_t[t]);
+    fmax = std::max(fmax, tmax / (double)horizon);
+  }
+  for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i) rmax = std::max(rmax, std::fabs(in->reward_table[i]));
+  if (!(fmax <= 1.0e4) || !(rmax <= 1.0e6)) return 0.0;
+  double Z1 = 0, A2 = 0, Z2 = 0, A3 = 0, Z3 = 0;
+  for (int n = 0; n < H; ++n) {
+    double a = 0, b = 0;
+    for (int c = 0; c < inw; ++c) a += std::fabs(pol->w1[(size_t)n * inw + c]);
+    for (int c = 0; c < H; ++c) b += std::fabs(pol->w2[(size_t)n * H + c]);
+    Z1 = std::max(Z1, fmax * a + std::fabs(pol->b1[n]));
+    A2 = std::max(A2, b);
+    Z2 = std::max(Z2, b + std::fabs(pol->b2[n]));
+  }
+  for (int j = 0; j < J; ++j) {
+    double a = 0;
+    for (int l = 0; l < H; ++l) a += std::fabs(pol->w3[(size_t)j * H + l] + pol->w3[(size_t)(J + j) * H + l]);
+    A3 = std::max(A3, a);
+    Z3 = std::max(Z3, a + std::fabs(pol->b3[j] + pol->b3[J + j]) + rmax);
+  }
+  const double E = A3 * (A2 * Z1 + Z2) + Z3;
+  // the seeded reference policy: |w| ~ U(0, 0.1) (mean 0.05), features <= 1, rewards <= 1
+  const double s1 = 0.05 * (inw + 1), s2 = 0.05 * H, s3 = 0.1 * H;
+  const double E0 = s3 * (s2 * s1 + s2 + 0.05) + s3 + 0.1 + 1.0;
+  const double guard = 5e-5 * std::max(1.0, E / (1.5 * E0));  // 1.5: row maxima above the means
+  return guard <= 1e-2 ? guard : 0.0;
+}
+
 static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax) {
   const int in = 2 * J + 1, out = 2 * J;
   const double u = std::ldexp(1.0, -53);
@@ -1107,10 +1172,14 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
     }
     h->p_horizon = pol->horizon >= 0 ? pol->horizon : in->horizon;
     if (2 * h->J + 1 <= kTcK1 && h->J <= kTcN3 && H == kTcH) {
-      prepare_tc(h.get(), pol, pol->init_capacity ? pol->init_capacity : in->capacity,
-                 pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
-                                    : in->inventory,
-                 in->reward_table);
+      const int32_t* pc = pol->init_capacity ? pol->init_capacity : in->capacity;
+      const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
+                                             : in->inventory;
+      const double g = tc_scaled_guard(pol, in, pc, pi, h->p_horizon, h->J, H);
+      if (g > 0) {
+        prepare_tc(h.get(), pol, pc, pi, in->reward_table);
+        h->tc_guard = g;
+      }
     }
   }
   CK(cudaMalloc(&h->scal, sizeof(Scalars)));

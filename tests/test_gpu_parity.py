@@ -476,6 +476,39 @@ def test_general_engine_uniform_plans_match_replay(J, I, T, M, kind):
     assert rs["general"].timing["engine_used"] == 4
 
 
+@pytest.mark.parametrize("scale,shrink,tc", [(2.0, 1, 1), (1.0, 4, 1), (3.0, 2, 1), (8.0, 1, 0), (float("nan"), 1, 0)])
+def test_tensor_core_guard_scales_with_policy(scale, shrink, tc):
+    """Policies with larger weights / features than the reference's seeded
+    ones: the tensor-core guard grows with their error propagation (verify
+    mode: no unflagged disagreement), and policies whose error bound is too
+    large, or whose weights are not finite, keep the exact FP64 path."""
+    ons, inst, owner, _, _ = _dual_case(30, 200, 12000, 256, "product")
+    p = P.MlpParams.seeded_uniform(61, 60, 5)
+    for a in (p.w1, p.b1, p.w2, p.b2, p.w3, p.b3):
+        a *= 1.0 if scale != scale else scale
+    if scale != scale:
+        p.w1[3 * 61 + 7] = float("nan")
+    cap0 = np.maximum(np.asarray(inst.capacity) // shrink, 1)
+    inv0 = np.asarray(inst.inventory) // shrink
+    pol = P.DualNetworkPolicy(p, cap0, inv0, inst.horizon, 30)
+    plan = P.PartitionPlan(256, owner)
+    runs = {}
+    for engine, verify in (("product", False), ("product", True), ("product_fp64", False)):
+        try:
+            r = P.picard_simulate(inst, pol, plan, P.PicardConfig(record_trace=True, engine=engine, tc_verify=verify))
+            runs[(engine, verify)] = (r.actions.tolist(), [x.astuple() for x in r.trace], r.timing)
+        except P.ContractViolation as e:
+            runs[(engine, verify)] = ("ContractViolation", e.time_step, None)
+    base = runs[("product_fp64", False)]
+    for key in (("product", False), ("product", True)):
+        assert runs[key][:2] == base[:2], key
+        if runs[key][2] is not None:
+            assert runs[key][2]["tc_used"] == tc
+            assert runs[key][2]["tc_unflagged_bad"] == 0
+    if tc:
+        assert runs[("product", False)][2]["tc_flagged"] > 0
+
+
 def test_cpp_dropin_matches_reference_engine():
     """The reference's own engine scenarios through include/picard_b200.hpp,
     checked against the UNMODIFIED reference CPU engine (tests/cpp)."""
