@@ -1,5 +1,5 @@
 // general.cuh — closed-form sweep for ANY partition and any cache
-// (PCD_ENGINE_GENERAL; SURVEY §7.3(3), DESIGN.md §4.9).
+// (PCD_ENGINE_GENERAL; SURVEY §7.3(3), DESIGN.md §4.2c).
 //
 // The reference's sweep_one_process (engine.hpp:299-342) replays the frozen
 // cache over the whole window for every process. Every attempt on (product i,
@@ -84,7 +84,7 @@ struct GenArgs {
 };
 
 __host__ __device__ inline size_t gen_warp_smem_bytes(int J, int in, int H, int out) {
-  const size_t ibytes = ((size_t)4 * J * 4 + 15) & ~(size_t)15;
+  const size_t ibytes = ((size_t)5 * J * 4 + 15) & ~(size_t)15;
   return ibytes + (size_t)(in + 2 * H + out) * 8;
 }
 
@@ -117,12 +117,13 @@ static __global__ void __launch_bounds__(128) k_sweep_general(GenArgs a) {
   const int m = blockIdx.x * (blockDim.x >> 5) + warp;
   if (m >= a.M || (a.mine && !a.mine[m])) return;
   const int J = a.J, lo = a.lo, hi = a.hi;
-  const size_t ibytes = ((size_t)4 * J * 4 + 15) & ~(size_t)15;
+  const size_t ibytes = ((size_t)5 * J * 4 + 15) & ~(size_t)15;
   unsigned char* w = smem + gen_warp_smem_bytes(J, a.model.in, a.model.H, a.model.out) * warp;
   int* cv = (int*)w;    // C_t, then c_t
   int* xr = cv + J;     // x_t[p]
   int* corr = xr + J;   // sum of the delta terms per node
   int* tau = corr + J;  // death slots (INT_MAX: alive so far)
+  int* dp = tau + J;    // delta[p][.] of the current product p over own slots in [lo, t)
   WarpScratch ws;
   {
     double* d = (double*)(w + ibytes);
@@ -141,6 +142,7 @@ static __global__ void __launch_bounds__(128) k_sweep_general(GenArgs a) {
   const int HJ = hck_stride(J), base = hck_base(lo);
   const unsigned ltmask = (1u << lane) - 1u;
   int sprev = lo - 1;
+  int curp = -1;  // product of the previous own slot (dp and the dead nodes' x are its)
   unsigned long long changed = 0, conflicts = 0, first = ~0ull, nev = 0;
   long long mism = 0;
   __syncwarp();
@@ -211,16 +213,22 @@ static __global__ void __launch_bounds__(128) k_sweep_general(GenArgs a) {
       }
       nd = wr;
     }
-    // local state at t: capacities and the order's inventory row
+    // local state at t: capacities and the order's inventory row. Runs of own
+    // slots of one product update dp incrementally and keep the frozen x of
+    // nodes that were already dead; a product switch walks the chain once.
+    const bool same = p == curp;
+    if (!same)
+      for (int j = lane; j < J; j += 32) dp[j] = gen_chain_delta(a, pos, j, t);
     for (int j = lane; j < J; j += 32) {
       const int c = cv[j];
-      const int u = c > 0 ? t : tau[j];
+      cv[j] = max(c, 0);
+      if (c <= 0 && same && tau[j] <= sprev) continue;  // dead before the previous own slot: x frozen
       const int key = p * J + j;
       const int kb = a.gstart[key], ke = a.gstart[key + 1];
-      const int A = lower_bound_i32(a.gslots + kb, ke - kb, u) + gen_chain_delta(a, pos, j, u);
+      const int A = c > 0 ? lower_bound_i32(a.gslots + kb, ke - kb, t) + dp[j]
+                          : lower_bound_i32(a.gslots + kb, ke - kb, tau[j]) + gen_chain_delta(a, pos, j, tau[j]);
       const int x0 = a.ckinv[key];
       xr[j] = x0 - min(x0, A);
-      cv[j] = max(c, 0);
     }
     __syncwarp();
     int nonfinite = 0;
@@ -243,7 +251,7 @@ static __global__ void __launch_bounds__(128) k_sweep_general(GenArgs a) {
       for (int q = 0; q < 2; ++q) {
         const int j = q ? anew : cold;
         if (j < 0) continue;  // warp-uniform
-        const int dlt = gen_chain_delta(a, pos, j, t) + (anew == j ? 1 : 0) - (cold == j ? 1 : 0);
+        const int dlt = dp[j] + (anew == j ? 1 : 0) - (cold == j ? 1 : 0);
         const int key = p * J + j;
         int found = -1;
         for (int e0 = 0; e0 < nd; e0 += 32) {
@@ -267,6 +275,8 @@ static __global__ void __launch_bounds__(128) k_sweep_general(GenArgs a) {
       }
     }
     if (lane == 0) {
+      if (cold >= 0) dp[cold] -= 1;
+      if (anew >= 0) dp[anew] += 1;
       a.ocache[pos] = cold;
       a.ofresh[pos] = anew;
       if (anew != aold) {
@@ -280,6 +290,7 @@ static __global__ void __launch_bounds__(128) k_sweep_general(GenArgs a) {
     }
     __syncwarp();
     sprev = t;
+    curp = p;
   }
   if (lane == 0) {
     if (changed) {
