@@ -434,10 +434,18 @@ static __global__ void k_hist_prefix(const int* __restrict__ ev, int lo, int hi,
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nrows * HJ; i += blockDim.x) {
-    const int r = i / HJ, j = i - r * HJ;
-    hck[(size_t)b0 * HJ + i] = j < J ? hs[r * J + j] : 0;
-  }
+  // rows of HJ ints as 16-byte stores: lane -> 4-column group, warp -> rows
+  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31, HJ4 = HJ >> 2;
+  for (int c = lane; c < HJ4; c += 32)
+    for (int r = threadIdx.x >> 5; r < nrows; r += nw) {
+      const int j = 4 * c;
+      int4 v;
+      v.x = j < J ? hs[r * J + j] : 0;
+      v.y = j + 1 < J ? hs[r * J + j + 1] : 0;
+      v.z = j + 2 < J ? hs[r * J + j + 2] : 0;
+      v.w = j + 3 < J ? hs[r * J + j + 3] : 0;
+      *(int4*)(hck + (size_t)(b0 + r) * HJ + j) = v;
+    }
 }
 
 struct SweepArgs {
