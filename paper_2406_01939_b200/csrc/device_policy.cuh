@@ -235,25 +235,52 @@ __device__ int warp_policy_eval(const DevModel& P, const int* caps, const int* r
   }
   __syncwarp();
   const int H = P.H, in = P.in, out = P.out;
-  for (int r = lane; r < H; r += 32) {
-    double acc = __ldg(P.b1 + r);
+  // Each output keeps the reference's sequential acc += w * x chain
+  // (mlp.cpp:141-169, no contraction); a lane runs several outputs' chains
+  // side by side for instruction-level parallelism.
+  for (int r = lane; r < H; r += 64) {
+    const bool two = r + 32 < H;
+    double a0 = __ldg(P.b1 + r), a1 = two ? __ldg(P.b1 + r + 32) : 0.0;
     const double* w = P.w1t + r;
-    for (int c = 0; c < in; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(w + (size_t)c * H), s.f[c]));
-    s.h1[r] = gt_tanh(acc, P.tanh_fma);
+    for (int c = 0; c < in; ++c) {
+      const double f = s.f[c];
+      a0 = __dadd_rn(a0, __dmul_rn(__ldg(w + (size_t)c * H), f));
+      if (two) a1 = __dadd_rn(a1, __dmul_rn(__ldg(w + (size_t)c * H + 32), f));
+    }
+    s.h1[r] = gt_tanh(a0, P.tanh_fma);
+    if (two) s.h1[r + 32] = gt_tanh(a1, P.tanh_fma);
   }
   __syncwarp();
-  for (int r = lane; r < H; r += 32) {
-    double acc = __ldg(P.b2 + r);
+  for (int r = lane; r < H; r += 64) {
+    const bool two = r + 32 < H;
+    double a0 = __ldg(P.b2 + r), a1 = two ? __ldg(P.b2 + r + 32) : 0.0;
     const double* w = P.w2t + r;
-    for (int c = 0; c < H; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(w + (size_t)c * H), s.h1[c]));
-    s.h2[r] = gt_tanh(acc, P.tanh_fma);
+    for (int c = 0; c < H; ++c) {
+      const double x = s.h1[c];
+      a0 = __dadd_rn(a0, __dmul_rn(__ldg(w + (size_t)c * H), x));
+      if (two) a1 = __dadd_rn(a1, __dmul_rn(__ldg(w + (size_t)c * H + 32), x));
+    }
+    s.h2[r] = gt_tanh(a0, P.tanh_fma);
+    if (two) s.h2[r + 32] = gt_tanh(a1, P.tanh_fma);
   }
   __syncwarp();
-  for (int r = lane; r < out; r += 32) {
-    double acc = __ldg(P.b3 + r);
+  for (int r = lane; r < out; r += 128) {
+    const bool v1 = r + 32 < out, v2 = r + 64 < out, v3 = r + 96 < out;
+    double a0 = __ldg(P.b3 + r), a1 = v1 ? __ldg(P.b3 + r + 32) : 0.0;
+    double a2 = v2 ? __ldg(P.b3 + r + 64) : 0.0, a3 = v3 ? __ldg(P.b3 + r + 96) : 0.0;
     const double* w = P.w3t + r;
-    for (int c = 0; c < H; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(w + (size_t)c * out), s.h2[c]));
-    s.pr[r] = acc;
+    for (int c = 0; c < H; ++c) {
+      const double x = s.h2[c];
+      const double* wc = w + (size_t)c * out;
+      a0 = __dadd_rn(a0, __dmul_rn(__ldg(wc), x));
+      if (v1) a1 = __dadd_rn(a1, __dmul_rn(__ldg(wc + 32), x));
+      if (v2) a2 = __dadd_rn(a2, __dmul_rn(__ldg(wc + 64), x));
+      if (v3) a3 = __dadd_rn(a3, __dmul_rn(__ldg(wc + 96), x));
+    }
+    s.pr[r] = a0;
+    if (v1) s.pr[r + 32] = a1;
+    if (v2) s.pr[r + 64] = a2;
+    if (v3) s.pr[r + 96] = a3;
   }
   __syncwarp();
   double bv = 0.0;
