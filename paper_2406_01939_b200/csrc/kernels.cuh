@@ -505,7 +505,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int J, int in, int H, int out)
 // owner and no other process reads cache[t] after the effective pass.
 // ---------------------------------------------------------------------------
 template <int KIND>
-static __global__ void __launch_bounds__(128) k_sweep_product(SweepArgs a) {
+static __global__ void __launch_bounds__(128, 8) k_sweep_product(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + warp;
