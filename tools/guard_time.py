@@ -7,7 +7,7 @@ import paper_2406_01939_b200 as P  # noqa: E402
 
 inst = P.generate_instance(100, 10000, 10_000_000, 0.0, 0.8, 7)
 pol = P.DualNetworkPolicy.seeded(inst, 5)
-plan = P.make_product_partition(inst, 65536, 1)
+plan = P.make_product_chunk_partition(inst, 65536, 1)
 guards = [float(g) for g in sys.argv[1:]] or [5e-5]
 with P.Simulator(inst, pol) as sim:
     sim.set_plan(plan)
