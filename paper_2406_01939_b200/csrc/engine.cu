@@ -203,7 +203,7 @@ struct pcd_handle {
   // tensor-core policy (tc_sweep.cu)
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   double tc_guard = 5e-5;                // tc_scaled_guard
-  pcd::DBuf<unsigned char> tc_wimg;
+  pcd::DBuf<unsigned char> tc_wimg, tc_wimg2;
   pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf, tc_rtq;
   pcd::DBuf<unsigned long long> tc_stats;
   int32_t tc_tiles = 0;
@@ -438,7 +438,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
                                                  bits, h->stream));
     h->timing.kernel_launches += 2;
   }
-  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p;
+  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p; a.wimg2 = h->tc_wimg2.p;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p; a.rtabq = h->tc_rtq.p;
   a.guard = (float)(guard > 0 ? guard : h->tc_guard);
@@ -1048,7 +1048,7 @@ static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax
 static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap, const int32_t* pinv,
                        const double* rtab) {
   const int J = h->J, I = h->I, in = 2 * J + 1;
-  std::vector<unsigned char> img(kWImgBytes, 0);
+  std::vector<unsigned char> img(kWImgBytes, 0), img2(kWImgBytes, 0);
   // hi part at `base`, lo part at `base + part` (matches w1h/w1l/... in tc_sweep.cu)
   auto put = [&](size_t base, size_t part, int R, int r, int k, double w) {
     const float wf = (float)w;
@@ -1057,6 +1057,10 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
     const size_t off = (size_t)canon_off(R, r, k);
     std::memcpy(&img[base + off], &hi, 2);
     std::memcpy(&img[base + part + off], &lo, 2);
+    // ping-pong image: the layer's hi rows 0..R-1 and lo rows R..2R-1 as one
+    // 2R-row K-major operand, so hi.hi and hi.lo are one N = 2R MMA
+    std::memcpy(&img2[base + (size_t)canon_off(2 * R, r, k)], &hi, 2);
+    std::memcpy(&img2[base + (size_t)canon_off(2 * R, R + r, k)], &lo, 2);
   };
   const size_t w2base = 2 * (size_t)kW1Bytes, w3base = w2base + 2 * (size_t)kW2Bytes;
   for (int r = 0; r < kTcH; ++r)
@@ -1073,6 +1077,7 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
   for (int j = 0; j < J; ++j) ic0[j] = pcap[j] > 0 ? (float)(1.0 / pcap[j]) : 0.f;
   for (size_t i = 0; i < (size_t)I * J; ++i) ix0[i] = pinv[i] > 0 ? (float)(1.0 / pinv[i]) : 0.f;
   h->tc_wimg.upload(img.data(), img.size(), h->stream);
+  h->tc_wimg2.upload(img2.data(), img2.size(), h->stream);
   h->tc_b1.upload(b1.data(), b1.size(), h->stream);
   h->tc_b2.upload(b2.data(), b2.size(), h->stream);
   h->tc_b3.upload(b3.data(), b3.size(), h->stream);

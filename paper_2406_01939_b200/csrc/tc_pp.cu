@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
   // ---------------------------------------------------------------- setup
   {
-    const uint4* src = (const uint4*)a.wimg;
+    const uint4* src = (const uint4*)a.wimg2;
     uint4* dst = (uint4*)sW;
     for (int i = tid; i < kWImgBytes / 16; i += kBlock) dst[i] = src[i];
     uint4* da = (uint4*)(smem + Layout::a);
@@ -421,10 +421,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   }
 
   const uint32_t aBase = smem_u32(sAh);
-  const uint32_t w1h = smem_u32(sW), w1l = w1h + kW1Bytes;
-  const uint32_t w2h = w1l + kW1Bytes, w2l = w2h + kW2Bytes;
-  const uint32_t w3h = w2l + kW2Bytes, w3l = w3h + kW3Bytes;
-  const uint32_t id64 = idesc_f16(64, 64), id112 = idesc_f16(64, kTcN3);
+  // per layer one [hi; lo] operand of 2N rows (engine.cu prepare_tc, img2)
+  const uint32_t w1 = smem_u32(sW), w2 = w1 + 2 * kW1Bytes, w3 = w2 + 2 * kW2Bytes;
+  const uint32_t id64 = idesc_f16(64, 64), id128 = idesc_f16(64, 128);
+  const uint32_t id112 = idesc_f16(64, kTcN3), id224 = idesc_f16(64, 2 * kTcN3);
   uint32_t phase = 0;
   const float invT = S.model.horizon > 0 ? (float)(1.0 / (double)S.model.horizon) : 0.f;
   uint32_t xb = 0;  // x > 0 bits of the thread's nodes (bit 8i + k: node 8(g + 4i) + k), persistent
@@ -436,18 +436,18 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   const bool prof_on = PROF && blockIdx.x == 0 && tid == 0;
 #define PMARK(k) do { if (PROF && prof_on) { const long long now_ = clock64(); pacc[k] += now_ - plast; plast = now_; } } while (0)
 
-  // the half's MMAs of one layer: K16 k-steps, three products into (acc, acc+off)
-  auto issue_layer = [&](uint32_t acc, uint32_t off, uint32_t wh, uint32_t wl, uint32_t wlbo, int ksteps,
-                         uint32_t id) {
+  // the half's MMAs of one layer (N outputs), K16 k-steps: A_hi . [W_hi; W_lo]
+  // (one N = 2N MMA: hi.hi into acc, hi.lo into acc + N), then A_lo . W_hi
+  // accumulated into acc + N
+  auto issue_layer = [&](uint32_t acc, uint32_t N, uint32_t wb, int ksteps, uint32_t idfull, uint32_t idhalf) {
     tc_fence_after();
     const uint64_t dA = umma_desc(aBase, kHalfRows * 16, 128), dAl = umma_desc(aBase + kAH, kHalfRows * 16, 128);
-    const uint64_t dW = umma_desc(wh, wlbo, 128), dWl = umma_desc(wl, wlbo, 128);
+    const uint64_t dW = umma_desc(wb, 2 * N * 16, 128);
     for (int s = 0; s < ksteps; ++s) {
       const uint64_t ah = dA + s * ((2 * kChunkB) >> 4), al = dAl + s * ((2 * kChunkB) >> 4);
-      const uint64_t bh = dW + s * ((2 * wlbo) >> 4), bl = dWl + s * ((2 * wlbo) >> 4);
-      mma_f16(tD + acc, ah, bh, id, s > 0);
-      mma_f16(tD + acc + off, ah, bl, id, s > 0);
-      mma_f16(tD + acc + off, al, bh, id, 1);
+      const uint64_t b = dW + s * ((4 * N * 16) >> 4);
+      mma_f16(tD + acc, ah, b, idfull, s > 0);
+      mma_f16(tD + acc + N, al, b, idhalf, 1);
     }
     mma_commit(bar);
   };
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     if (PROF && prof_on) pacc[10] += 1;
 
     // ============================ layer 1: z1 = F . W1^T (three products)
-    if (ht == 0) issue_layer(0, 64, w1h, w1l, kTcH * 16, kTcK1 / 16, id64);
+    if (ht == 0) issue_layer(0, kTcH, w1, kTcK1 / 16, id128, id64);
     if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
     bar_half(h);
     PMARK(1);
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     PMARK(2);
 
     // ============================ layer 2
-    if (ht == 0) issue_layer(128, 64, w2h, w2l, kTcH * 16, kTcH / 16, id64);
+    if (ht == 0) issue_layer(128, kTcH, w2, kTcH / 16, id128, id64);
     if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
     bar_half(h);
     PMARK(3);
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     PMARK(4);
 
     // ============================ layer 3: q = h2 . W3'^T (N = 112)
-    if (ht == 0) issue_layer(0, kTcN3, w3h, w3l, kTcN3 * 16, kTcH / 16, id112);
+    if (ht == 0) issue_layer(0, kTcN3, w3, kTcH / 16, id224, id112);
     // this thread's reward loads while layer 3 runs
     uint32_t rwv[kMaxCI][8];
     {
