@@ -1,3 +1,10 @@
+"""C3 on the exact FP64 SIMT engines (not a test): the run-partition sweep
+(engine=product_fp64) and the general closed form (engine=general) on the
+product-chunk plan, same trajectory as the tensor-core sweep. One JSON line
+per engine (profiles/r01_fp64_engines_c3.jsonl).
+
+  python tools/fp64_engines_probe.py
+"""
 import sys, json
 sys.path.insert(0, ".")
 import paper_2406_01939_b200 as P
