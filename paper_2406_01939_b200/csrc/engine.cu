@@ -979,10 +979,12 @@ static double tc_scaled_guard(const pcd_policy* pol, const pcd_instance* in, con
   if (wmax > 3.0e4) return 0.0;
   // largest feature: c / c0, x / x0 (states never exceed the instance's), t / T
   double fmax = 1.0, rmax = 0.0;
-  for (int j = 0; j < J; ++j)
-    if (pcap[j] > 0) fmax = std::max(fmax, (double)in->capacity[j] / pcap[j]);
-  for (size_t i = 0; i < (size_t)in->products * J; ++i)
-    if (pinv[i] > 0) fmax = std::max(fmax, (double)in->inventory[i] / pinv[i]);
+  if (pcap != in->capacity)  // the instance's own normalisers give ratios <= 1
+    for (int j = 0; j < J; ++j)
+      if (pcap[j] > 0) fmax = std::max(fmax, (double)in->capacity[j] / pcap[j]);
+  if (pinv != in->inventory)
+    for (size_t i = 0; i < (size_t)in->products * J; ++i)
+      if (pinv[i] > 0) fmax = std::max(fmax, (double)in->inventory[i] / pinv[i]);
   if (horizon > 0) {
     double tmax = (double)std::max<int64_t>(in->horizon - 1, 0);
     if (in->order_t)
@@ -1071,18 +1073,21 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
     for (int k = 0; k < kTcH; ++k)
       put(w3base, kW3Bytes, kTcN3, r, k,
           r < J ? pol->w3[(size_t)r * kTcH + k] + pol->w3[(size_t)(J + r) * kTcH + k] : 0.0);
-  std::vector<float> b1(kTcH), b2(kTcH), b3(kTcN3, 0.f), ic0(J), ix0((size_t)I * J);
+  std::vector<float> b1(kTcH), b2(kTcH), b3(kTcN3, 0.f), ic0(J);
   for (int r = 0; r < kTcH; ++r) { b1[r] = (float)pol->b1[r]; b2[r] = (float)pol->b2[r]; }
   for (int j = 0; j < J; ++j) b3[j] = (float)(pol->b3[j] + pol->b3[J + j]);
   for (int j = 0; j < J; ++j) ic0[j] = pcap[j] > 0 ? (float)(1.0 / pcap[j]) : 0.f;
-  for (size_t i = 0; i < (size_t)I * J; ++i) ix0[i] = pinv[i] > 0 ? (float)(1.0 / pinv[i]) : 0.f;
   h->tc_wimg.upload(img.data(), img.size(), h->stream);
   h->tc_wimg2.upload(img2.data(), img2.size(), h->stream);
   h->tc_b1.upload(b1.data(), b1.size(), h->stream);
   h->tc_b2.upload(b2.data(), b2.size(), h->stream);
   h->tc_b3.upload(b3.data(), b3.size(), h->stream);
   h->tc_ic0.upload(ic0.data(), ic0.size(), h->stream);
-  h->tc_ix0.upload(ix0.data(), ix0.size(), h->stream);
+  // 1/x0 of the policy's inventory normalisers, on the device (pinv0 is resident)
+  h->tc_ix0.alloc(std::max<size_t>(1, (size_t)I * J));
+  if ((size_t)I * J > 0)
+    k_inv_f32<<<grid_for((long long)I * J, 256), 256, 0, h->stream>>>(h->pinv0.p, (long long)I * J, h->tc_ix0.p);
+  CK(cudaGetLastError());
   const int RJ = (J + 7) & ~7;  // 32-byte rows for the 256-bit loads of the score phase
   std::vector<float> rtf((size_t)h->R * RJ, 0.f);
   for (int64_t rr = 0; rr < h->R; ++rr)

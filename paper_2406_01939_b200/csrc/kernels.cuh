@@ -775,6 +775,12 @@ static __global__ void k_first_out_of_range(const int* __restrict__ a, long long
     if (a[t] < lo || a[t] >= hi) atomicMin(first, (unsigned long long)t);
 }
 
+// out[i] = 1 / x[i] rounded to float (0 where x[i] <= 0): feature scales of the tensor-core sweep
+static __global__ void k_inv_f32(const int* __restrict__ x, long long n, float* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = x[i] > 0 ? (float)(1.0 / (double)x[i]) : 0.f;
+}
+
 static __global__ void k_iota(int* p, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = (int)i;
 }
