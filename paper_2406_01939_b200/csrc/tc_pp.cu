@@ -439,17 +439,18 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   // the half's MMAs of one layer (N outputs), K16 k-steps: A_hi . [W_hi; W_lo]
   // (one N = 2N MMA: hi.hi into acc, hi.lo into acc + N), then A_lo . W_hi
   // accumulated into acc + N
-  auto issue_layer = [&](uint32_t acc, uint32_t N, uint32_t wb, int ksteps, uint32_t idfull, uint32_t idhalf) {
+  auto issue_layer = [&](uint32_t acc, uint32_t N, uint32_t wb, int ksteps, uint32_t idfull, uint32_t idhalf,
+                         int s0 = 0, bool commit = true) {
     tc_fence_after();
     const uint64_t dA = umma_desc(aBase, kHalfRows * 16, 128), dAl = umma_desc(aBase + kAH, kHalfRows * 16, 128);
     const uint64_t dW = umma_desc(wb, 2 * N * 16, 128);
-    for (int s = 0; s < ksteps; ++s) {
+    for (int s = s0; s < ksteps; ++s) {
       const uint64_t ah = dA + s * ((2 * kChunkB) >> 4), al = dAl + s * ((2 * kChunkB) >> 4);
       const uint64_t b = dW + s * ((4 * N * 16) >> 4);
       mma_f16(tD + acc, ah, b, idfull, s > 0);
       mma_f16(tD + acc + N, al, b, idhalf, 1);
     }
-    mma_commit(bar);
+    if (commit) mma_commit(bar);
   };
 
   for (;;) {
@@ -648,48 +649,52 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
     // ============================ hidden epilogues (z -> tanh -> fp16 hi/lo)
     const bool qact = ctl[CT_QACT + q] != 0;  // warp-uniform: skip idle row quarters
-    auto hidden_epilogue = [&](uint32_t col_hh, uint32_t col_x, const float* bias) {
+    // one 8-unit chunk (i = 0: units 0-31 of the layer = the next layer's
+    // k-steps 0-1; i = 1: units 32-63 = k-steps 2-3), so the next layer's
+    // first k-steps run while the second chunk is computed
+    auto hidden_part = [&](uint32_t col_hh, uint32_t col_x, const float* bias, int i) {
       if (!qact) return;
-      uint32_t vh[2][8], vx[2][8];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        ld8s(tmem + tl + col_hh + 16 * p2 + 32 * i, vh[i]);
-        ld8s(tmem + tl + col_x + 16 * p2 + 32 * i, vx[i]);
-      }
+      uint32_t vh[8], vx[8];
+      ld8s(tmem + tl + col_hh + 16 * p2 + 32 * i, vh);
+      ld8s(tmem + tl + col_x + 16 * p2 + 32 * i, vx);
       tmem_wait_ld();
+      const int u0 = 8 * (g + 4 * i);
+      uint32_t ph[4], pl[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int u0 = 8 * (g + 4 * i);
-        uint32_t ph[4], pl[4];
-#pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-          const float z0 = fmaf(__uint_as_float(vx[i][k]), kLoInv, __uint_as_float(vh[i][k])) + bias[u0 + k];
-          const float z1 =
-              fmaf(__uint_as_float(vx[i][k + 1]), kLoInv, __uint_as_float(vh[i][k + 1])) + bias[u0 + k + 1];
-          split2(tanh_mufu(z0), tanh_mufu(z1), ph[k / 2], pl[k / 2]);
-        }
-        const int off = rowo + kc64(u0);
-        *(uint4*)(sAh + off) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-        *(uint4*)(sAh + kAH + off) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+      for (int k = 0; k < 8; k += 2) {
+        const float z0 = fmaf(__uint_as_float(vx[k]), kLoInv, __uint_as_float(vh[k])) + bias[u0 + k];
+        const float z1 = fmaf(__uint_as_float(vx[k + 1]), kLoInv, __uint_as_float(vh[k + 1])) + bias[u0 + k + 1];
+        split2(tanh_mufu(z0), tanh_mufu(z1), ph[k / 2], pl[k / 2]);
       }
+      const int off = rowo + kc64(u0);
+      *(uint4*)(sAh + off) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+      *(uint4*)(sAh + kAH + off) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
     };
-    hidden_epilogue(0, 64, sB1);
-    tc_fence_before();
-    fence_async_smem();
-    bar_half(h);
+    auto publish_operand = [&]() {
+      tc_fence_before();
+      fence_async_smem();
+      bar_half(h);
+    };
+    hidden_part(0, 64, sB1, 0);
+    publish_operand();
+    if (ht == 0) issue_layer(128, kTcH, w2, 2, id128, id64, 0, false);  // layer 2, k-steps 0-1
+    tc_fence_after();
+    hidden_part(0, 64, sB1, 1);
+    publish_operand();
     PMARK(2);
 
-    // ============================ layer 2
-    if (ht == 0) issue_layer(128, kTcH, w2, kTcH / 16, id128, id64);
+    // ============================ layer 2 (k-steps 2-3)
+    if (ht == 0) issue_layer(128, kTcH, w2, kTcH / 16, id128, id64, 2, true);
     if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
     bar_half(h);
     PMARK(3);
     phase ^= 1;
     tc_fence_after();
-    hidden_epilogue(128, 192, sB2);  // h2 overwrites h1 (layer 2 has completed)
-    tc_fence_before();
-    fence_async_smem();
-    bar_half(h);
+    // h2 overwrites h1 (layer 2 has completed); no early layer-3 k-steps here:
+    // layer 3's accumulators (columns 0..2 N3) overlap layer 2's (128..255)
+    hidden_part(128, 192, sB2, 0);
+    hidden_part(128, 192, sB2, 1);
+    publish_operand();
     PMARK(4);
 
     // ============================ layer 3: q = h2 . W3'^T (N = 112)
