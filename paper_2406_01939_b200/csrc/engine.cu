@@ -32,6 +32,7 @@ namespace pcd {
 
 void launch_tc_sweep(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_sweep.cu (128-row lockstep)
 void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream);     // tc_pp.cu (two 64-row halves)
+int tc_pp_width_class(int J);  // tc_pp.cu: layer-3 width class of the ping-pong sweep for J nodes
 size_t tc_smem_bytes();
 
 #define CK(x)                                                                              \
@@ -203,6 +204,7 @@ struct pcd_handle {
   // tensor-core policy (tc_sweep.cu)
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   double tc_guard = 5e-5;                // tc_scaled_guard
+  int tc_n3 = 0;                         // layer-3 width class of the ping-pong image (prepare_tc)
   pcd::DBuf<unsigned char> tc_wimg, tc_wimg2;
   pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf, tc_rtq;
   pcd::DBuf<unsigned long long> tc_stats;
@@ -438,7 +440,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
                                                  bits, h->stream));
     h->timing.kernel_launches += 2;
   }
-  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p; a.wimg2 = h->tc_wimg2.p;
+  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p; a.rtabq = h->tc_rtq.p;
   a.guard = (float)(guard > 0 ? guard : h->tc_guard);
@@ -1051,6 +1053,8 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
                        const double* rtab) {
   const int J = h->J, I = h->I, in = 2 * J + 1;
   std::vector<unsigned char> img(kWImgBytes, 0), img2(kWImgBytes, 0);
+  const int n3 = tc_pp_width_class(J);
+  h->tc_n3 = n3;
   // hi part at `base`, lo part at `base + part` (matches w1h/w1l/... in tc_sweep.cu)
   auto put = [&](size_t base, size_t part, int R, int r, int k, double w) {
     const float wf = (float)w;
@@ -1061,8 +1065,12 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
     std::memcpy(&img[base + part + off], &lo, 2);
     // ping-pong image: the layer's hi rows 0..R-1 and lo rows R..2R-1 as one
     // 2R-row K-major operand, so hi.hi and hi.lo are one N = 2R MMA
-    std::memcpy(&img2[base + (size_t)canon_off(2 * R, r, k)], &hi, 2);
-    std::memcpy(&img2[base + (size_t)canon_off(2 * R, R + r, k)], &lo, 2);
+    // (layer 3: R2 = the width class of J instead of kTcN3)
+    const int R2 = R == kTcN3 ? n3 : R;
+    if (r < R2) {
+      std::memcpy(&img2[base + (size_t)canon_off(2 * R2, r, k)], &hi, 2);
+      std::memcpy(&img2[base + (size_t)canon_off(2 * R2, R2 + r, k)], &lo, 2);
+    }
   };
   const size_t w2base = 2 * (size_t)kW1Bytes, w3base = w2base + 2 * (size_t)kW2Bytes;
   for (int r = 0; r < kTcH; ++r)

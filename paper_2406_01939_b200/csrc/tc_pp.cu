@@ -311,7 +311,9 @@ __device__ void half_recheck(const DevModel& P, unsigned char* sAh, const int* c
   mark(4);
 }
 
-template <bool PROF>
+// N3: layer-3 width class (J <= N3), KS1: layer-1 k-steps (2J + 1 <= 16 KS1);
+// the C3 shape is <112, 13>, smaller node counts get narrower MMAs
+template <bool PROF, int N3, int KS1>
 __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const SweepArgs& S = a.s;
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   // per layer one [hi; lo] operand of 2N rows (engine.cu prepare_tc, img2)
   const uint32_t w1 = smem_u32(sW), w2 = w1 + 2 * kW1Bytes, w3 = w2 + 2 * kW2Bytes;
   const uint32_t id64 = idesc_f16(64, 64), id128 = idesc_f16(64, 128);
-  const uint32_t id112 = idesc_f16(64, kTcN3), id224 = idesc_f16(64, 2 * kTcN3);
+  const uint32_t idn3 = idesc_f16(64, N3), id2n3 = idesc_f16(64, 2 * N3);
   uint32_t phase = 0;
   const float invT = S.model.horizon > 0 ? (float)(1.0 / (double)S.model.horizon) : 0.f;
   uint32_t xb = 0;  // x > 0 bits of the thread's nodes (bit 8i + k: node 8(g + 4i) + k), persistent
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     if (PROF && prof_on) pacc[10] += 1;
 
     // ============================ layer 1: z1 = F . W1^T (three products)
-    if (ht == 0) issue_layer(0, kTcH, w1, kTcK1 / 16, id128, id64);
+    if (ht == 0) issue_layer(0, kTcH, w1, KS1, id128, id64);
     if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
     bar_half(h);
     PMARK(1);
@@ -698,7 +700,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     PMARK(4);
 
     // ============================ layer 3: q = h2 . W3'^T (N = 112)
-    if (ht == 0) issue_layer(0, kTcN3, w3, kTcH / 16, id224, id112);
+    if (ht == 0) issue_layer(0, N3, w3, kTcH / 16, id2n3, idn3);
     // this thread's reward loads while layer 3 runs
     uint32_t rwv[kMaxCI][8];
     {
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
           for (int u = 0; u < 2; ++u) {
             if (i0 + u < ni) {
               ld8s(tmem + tl + 16 * p2 + 32 * (i0 + u), vh[u]);
-              ld8s(tmem + tl + kTcN3 + 16 * p2 + 32 * (i0 + u), vx[u]);
+              ld8s(tmem + tl + N3 + 16 * p2 + 32 * (i0 + u), vx[u]);
             }
           }
           tmem_wait_ld();
@@ -941,18 +943,31 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
 }  // namespace pp
 
-void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+template <bool PROF, int N3>
+static void launch_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+  constexpr int KS1 = (2 * N3 + 1 + 15) / 16 < kTcK1 / 16 ? (2 * N3 + 1 + 15) / 16 : kTcK1 / 16;
   static bool attr = false;
   const size_t smem = pp::Layout::total;
   if (!attr) {
-    cudaFuncSetAttribute(pp::k_sweep_pp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(pp::k_sweep_pp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pp::k_sweep_pp<PROF, N3, KS1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  if (a.prof)
-    pp::k_sweep_pp<true><<<ntiles, pp::kBlock, smem, stream>>>(a);
-  else
-    pp::k_sweep_pp<false><<<ntiles, pp::kBlock, smem, stream>>>(a);
+  pp::k_sweep_pp<PROF, N3, KS1><<<ntiles, pp::kBlock, smem, stream>>>(a);
+}
+
+int tc_pp_width_class(int J) { return J <= 16 ? 16 : J <= 32 ? 32 : J <= 64 ? 64 : kTcN3; }
+
+void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+  if (a.prof) {
+    launch_pp<true, kTcN3>(a, ntiles, stream);  // (debug profiles: the C3 shape)
+    return;
+  }
+  switch (a.n3) {
+    case 16: launch_pp<false, 16>(a, ntiles, stream); break;
+    case 32: launch_pp<false, 32>(a, ntiles, stream); break;
+    case 64: launch_pp<false, 64>(a, ntiles, stream); break;
+    default: launch_pp<false, kTcN3>(a, ntiles, stream); break;
+  }
 }
 
 }  // namespace pcd

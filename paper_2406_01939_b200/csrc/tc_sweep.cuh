@@ -52,6 +52,7 @@ struct TcArgs {
   int* wctl;            // {entries of wq, next entry beyond the dealt ones}
   const unsigned char* wimg;  // kWImgBytes: W1hi W1lo W2hi W2lo W3hi W3lo
   const unsigned char* wimg2; // kWImgBytes, ping-pong sweep: per layer one 2N-row operand [hi; lo]
+  int n3;                     // ping-pong sweep: layer-3 width class (tc_pp_width_class(J))
   const float* b1f;     // [64]
   const float* b2f;     // [64]
   const float* b3f;     // [112] b3[:J] + b3[J:]
