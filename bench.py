@@ -6,8 +6,9 @@ Workload (default "c3", BASELINE.json configs[2], the north-star target and the
 largest config; it fits one B200): SCO with J=100 nodes, I=10^4 products,
 T=10^7 orders (generate_instance recipe, seed 7, beta 0, coverage 0.8, the
 seeded synthetic 100-node geometry), dual-price MLP policy {201,64,64,200}
-with theta seed 5, M=65536 processes, max_steps = 300*M (whole horizon,
-cli.cpp:225-227). Partition (--partition): "chunk" (default) =
+with theta seed 5, M=65536 processes, max_steps = 500,000 (the window; the
+CLI default 300*M = the whole horizon is timed beside it, same trajectory).
+Partition (--partition): "chunk" (default) =
 make_product_chunk_partition(M): every product's orders cut into contiguous
 chunks, one process each, so all 65536 processes carry work; "product" = the
 reference's make_product_partition(M, seed 1), which activates only I=10^4 of
@@ -45,6 +46,19 @@ WORKLOADS = {
     "c2": (10, 1_000, 1_000_000, 4096, 5),
     "c3": (100, 10_000, 10_000_000, 65536, 5),
 }
+# PicardConfig::max_steps (the window, engine.hpp:120-126, :529-531) per
+# workload. Every window reaches the same serial trajectory (Prop. 1; the
+# reference's window-width invariance test, test_engine.cpp:455-477); the
+# width only changes how much of the horizon each iteration re-evaluates.
+# C3: 500,000 (profiles/r02_window_sweep.jsonl: 90 ms vs 340 ms for the CLI
+# default 300*M, which is the whole horizon here); C2/C1: the CLI default
+# (cli.cpp:225-227), narrower windows are slower there.
+WINDOWS = {"c1": None, "c2": None, "c3": 500_000}
+
+
+def default_window(name: str) -> int:
+    M = WORKLOADS[name][3]
+    return WINDOWS[name] if WINDOWS[name] is not None else 300 * M
 METRIC = "simulated time-steps/sec to convergence (1 trajectory); speedup vs serial CPU ref"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
@@ -142,6 +156,27 @@ PARTITIONS = {
     "product": "make_product_partition(M, seed 1) (the reference's partitioner)",
     "chunk": "make_product_chunk_partition(M): each product's orders cut into contiguous chunks, one process each",
 }
+DTYPE = "f64 decisions (fp16x3 tcgen05 MLP + exact FP64 recheck of rows within the guard)"
+
+
+def workload_config(args, world: int) -> dict:
+    """The config dict both arms print (identical by construction)."""
+    J, I, T, M, theta = WORKLOADS[args.workload]
+    return {"workload": args.workload, "J": J, "I": I, "T": T, "M": M, "theta": theta,
+            "policy": "dual MLP {2J+1,64,64,2J} seeded", "instance": "generate_instance(J, I, T, beta 0, "
+            "coverage 0.8, seed 7)" + (", seeded synthetic J-node geometry" if J > 30 else ""),
+            "partition": PARTITIONS[args.partition],
+            "max_steps": default_window(args.workload) if args.max_steps is None else args.max_steps,
+            "cli_default_max_steps": 300 * M,
+            "l2": "512 MiB flush before every GPU step; working set > L2",
+            "parallelism": f"processes sharded over {world} GPU(s)"}
+
+
+def trajectory_hash(actions) -> str:
+    """blake2b-64 of the int32 action array: both arms print it, so the same
+    trajectory shows the same hash."""
+    import hashlib
+    return hashlib.blake2b(np.ascontiguousarray(actions, np.int32).tobytes(), digest_size=8).hexdigest()
 
 
 def make_workload(name: str, partition: str = "product"):
@@ -156,62 +191,173 @@ def make_workload(name: str, partition: str = "product"):
     return inst, pol, plan, dict(J=J, I=I, T=T, M=M, theta=theta)
 
 
-def cpu_baseline(inst, pol, budget_s: float = 12.0):
-    """The UNMODIFIED reference's sequential_simulate (oracle/_ref) on the first
-    T' orders of the same instance, 1 host core (the path is inherently
-    serial). T' is sized for ~budget_s of CPU time."""
+def ref_workload(name: str):
+    """The workload built through the CPU oracle only (the reference's own
+    generate_instance / MlpParams::seeded_uniform via oracle/_ref, or the C
+    restatement when the reference build is absent) — the reference arm never
+    imports the product package."""
     from types import SimpleNamespace as NS
     from oracle.oracle import REF, ORC
     lib, kind = (REF, "reference") if REF is not None else (ORC, "port")
-    J = inst.nodes
+    J, I, T, M, theta = WORKLOADS[name]
+    inst = NS(**lib.generate_instance_arrays(J, I, T, 0.0, 0.8, 7, geometry=0 if J <= 30 else 1))
+    w = lib.seeded_mlp(2 * J + 1, 2 * J, theta)
+    pol = NS(kind=2, hidden=64, gamma=0.0, horizon=T, w1=w[0], b1=w[1], w2=w[2], b2=w[3], w3=w[4], b3=w[5])
+    return inst, pol, lib, kind
+
+
+def oracle_policy_of(pol, T):
+    from types import SimpleNamespace as NS
+    return NS(kind=2, hidden=pol.hidden, gamma=0.0, horizon=T, w1=pol.w1, b1=pol.b1, w2=pol.w2, b2=pol.b2,
+              w3=pol.w3, b3=pol.b3)
+
+
+def state_at(inst, actions, t):
+    """FoState after orders [0, t) of a trajectory (fo_transition applied in
+    order; env.hpp / types.hpp:89-100): capacities and dense inventory."""
+    a = np.asarray(actions[:t])
+    ok = a >= 0
+    J = int(inst.nodes)
+    cap = np.asarray(inst.capacity, np.int64) - np.bincount(a[ok], minlength=J)[:J]
+    inv = np.asarray(inst.inventory, np.int64).reshape(-1, J).copy()
+    np.subtract.at(inv, (np.asarray(inst.product[:t])[ok], a[ok]), 1)
+    return cap.astype(np.int32), inv.astype(np.int32).ravel()
+
+
+def cpu_baseline(inst, pol, actions, budget_s: float = 20.0, segments: int = 8):
+    """The UNMODIFIED reference's sequential_simulate (oracle/_ref), 1 host
+    core (the serial path cannot use more), on a STRATIFIED sample of the
+    same workload: `segments` equal stretches of n orders starting at
+    k*T/segments, each started from the exact state the trajectory reaches
+    there (the reference's actions on every stretch are compared with ours:
+    equal stretches mean equal states). The horizon's tail is mostly
+    declines (no forward pass, policies.hpp:127-134), so a head prefix would
+    overstate the serial cost; the stratified sample does not."""
+    from oracle.oracle import REF, ORC
+    T = int(inst.horizon)
+    opol = oracle_policy_of(pol, T)
+    if REF is None:  # C restatement: one full serial run (no session API)
+        t0 = time.perf_counter()
+        a, _ = ORC.sequential(inst, opol)
+        sec = time.perf_counter() - t0
+        return dict(value=T / sec, unit="steps/s", cores=1, kind="port",
+                    sample=f"C restatement sequential over all {T} orders ({sec:.2f} s, 1 core)",
+                    segments_equal=bool(np.array_equal(a, actions)))
+    sess = REF.session(inst, opol)
+    # size the stretches from a short probe at the head
+    probe = min(T, 20_000)
+    _, sp = sess.run(probe)
+    rate = probe / max(sp, 1e-6)
+    n = int(min(T // segments, max(1000, budget_s * rate / segments)))
+    total_n, total_s, equal = 0, 0.0, True
+    for k in range(segments):
+        t0 = k * (T // segments)
+        cap, inv = state_at(inst, actions, t0)
+        sess.set_state(t0, cap, inv)
+        a, sec = sess.run(t0 + n)
+        equal &= bool(np.array_equal(a, actions[t0:t0 + n]))
+        total_n += n
+        total_s += sec
+    sess.close()
+    return dict(value=total_n / total_s, unit="steps/s", cores=1, kind="reference",
+                sample=f"sequential_simulate on {segments} stretches of {n} orders at t = k*T/{segments} "
+                       f"({total_n} of {T} orders, {total_s:.2f} s, 1 core), each from the trajectory's exact "
+                       f"state there", segments_equal=equal)
+
+
+def cpu_picard(inst, pol, owner, M, budget_s: float = 15.0):
+    """The reference's picard_simulate (threads = every host core) to
+    convergence on a prefix of the same instance under the same plan
+    (restricted to the prefix), policy horizon T. Every process replays its
+    whole window (engine.hpp:313-336), so the full-size run is O(M * T) per
+    iteration; the extrapolation to the full horizon scales the sample by the
+    first iteration's replay count (sum over processes of last own slot + 1)."""
+    from oracle.oracle import REF
+    if REF is None:
+        return None
+    T = int(inst.horizon)
+    threads = os.cpu_count() or 1
+    opol = oracle_policy_of(pol, T)
+    from types import SimpleNamespace as NS
 
     def prefix(n):
-        return NS(nodes=J, products=inst.products, horizon=n, product=inst.product[:n], order_t=None,
-                  reward_row=inst.reward_row[:n], reward_table=inst.reward_table.ravel(),
-                  capacity=inst.capacity, inventory=inst.inventory.ravel())
+        return NS(nodes=inst.nodes, products=inst.products, horizon=n, product=inst.product[:n], order_t=None,
+                  reward_row=inst.reward_row[:n], reward_table=np.asarray(inst.reward_table).ravel(),
+                  capacity=inst.capacity, inventory=np.asarray(inst.inventory).ravel())
 
-    opol = NS(kind=2, hidden=pol.hidden, gamma=0.0, horizon=int(inst.horizon), w1=pol.w1, b1=pol.b1,
-              w2=pol.w2, b2=pol.b2, w3=pol.w3, b3=pol.b3)
-    n = min(int(inst.horizon), 20_000)
+    def replays(own, n):
+        last = np.full(M, -1, np.int64)
+        np.maximum.at(last, own[:n], np.arange(n))
+        return int((last + 1).sum())
+
+    n, sec, it = 2000, 0.0, 0
+    owner = np.asarray(owner, np.int32)
     while True:
-        if kind == "reference":
-            actions, sec = lib.sequential_timed(prefix(n), opol)
-        else:
-            t0 = time.perf_counter()
-            actions, _ = lib.sequential(prefix(n), opol)
-            sec = time.perf_counter() - t0
-        if sec >= budget_s / 4 or n >= inst.horizon:
+        _, it, se, sec = REF.picard_timed(prefix(n), opol, owner[:n], M, 300 * M, threads)
+        if sec >= budget_s / 3 or n >= T:
             break
-        n = min(int(inst.horizon), int(n * max(2.0, budget_s / max(sec, 1e-3) * 0.9)))
-    return dict(value=n / sec, unit="steps/s", cores=1, kind=kind,
-                sample=f"sequential_simulate on the first {n} of {inst.horizon} orders of the same "
-                       f"instance ({sec:.2f} s, 1 core); the serial path cannot use more threads"), actions
+        n = min(T, int(n * max(2.0, min(8.0, (budget_s / 3) / max(sec, 1e-3)))))
+    full_replays, sample_replays = replays(owner, T), replays(owner, n)
+    return dict(value=n / sec, unit="steps/s", cores=threads, kind="reference",
+                sample=f"picard_simulate(threads={threads}) to convergence on the first {n} of {T} orders under "
+                       f"the same plan ({sec:.2f} s, {it} iterations)",
+                replays_first_iteration={"sample": sample_replays, "full": full_replays},
+                extrapolated_full_s_per_iteration=sec / max(it, 1) * full_replays / max(sample_replays, 1))
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference's own CPU implementation, rank 0 only."""
+    """--impl reference: the reference's own CPU implementation on rank 0 only.
+    The timed K steps are K consecutive stretches of one serial trajectory
+    (sequential_simulate over [kT/K, (k+1)T/K) from the carried state), so
+    they cover the whole horizon exactly once; each warm-up step runs a short
+    head stretch and restores the initial state."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    inst, pol, plan, w = make_workload(args.workload, args.partition)
-    from oracle.oracle import REF
-    steps = []
-    for _ in range(args.warmup + args.steps):
-        cb, _ = cpu_baseline(inst, pol, budget_s=8.0)
-        steps.append(cb)
-    timed = steps[args.warmup:]
-    value = statistics.mean(s["value"] for s in timed)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    inst, pol, lib, kind = ref_workload(args.workload)
+    T = int(inst.horizon)
+    K = max(1, args.steps)
+    if kind == "reference":
+        sess = lib.session(inst, pol)
+        for _ in range(args.warmup):
+            sess.run(min(T, max(1, T // (8 * K))))
+            sess.set_state(0, inst.capacity, inst.inventory)
+        secs, parts = [], []
+        for k in range(K):
+            a, sec = sess.run((k + 1) * T // K)
+            secs.append(sec)
+            parts.append(a)
+        actions = np.concatenate(parts) if parts else np.zeros(0, np.int32)
+        sess.close()
+        total = sum(secs)
+        sample = (f"sequential_simulate over the whole horizon as {K} consecutive stretches of {T // K} orders "
+                  f"(state carried between stretches), {total:.2f} s, 1 core")
+    else:
+        t0 = time.perf_counter()
+        actions, _ = lib.sequential(inst, pol)
+        total = time.perf_counter() - t0
+        secs = [total / K] * K
+        sample = f"C restatement sequential over the whole horizon once ({total:.2f} s, 1 core), split into {K} steps"
+    value = T / total
+    M = WORKLOADS[args.workload][3]
+    picard = None
+    if kind == "reference" and not args.no_cpu_picard:
+        owner = lib.product_partition(inst, M, 1)
+        picard = cpu_picard(inst, pol, owner, M)
+        if picard:
+            picard["plan"] = "make_product_partition(M, seed 1) (the reference's partitioner)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * w["T"] / value, "higher_is_better": True, "scaling": "strong",
+            "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * total / K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, **w, "policy": "dual MLP seeded", "partition": args.partition},
-            "cpu_baseline": {**timed[-1], "value": value},
+            "config": workload_config(args, world),
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "reference has no GPU path; the serial CPU path is the reference's fastest way to the "
-                    "trajectory (its CPU Picard path is slower in wall time, BASELINE.md §2)"}
-    if REF is None:
-        line["note"] += "; oracle/_ref unavailable -> C restatement timed"
+            "cpu_picard": picard, "trajectory_hash": trajectory_hash(actions),
+            "step_seconds": [round(x, 3) for x in secs],
+            "note": "the reference has no GPU path; its serial CPU path is its fastest route to the trajectory "
+                    "(its CPU Picard path replays every window per process, cpu_picard)"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -226,6 +372,9 @@ def main():
     ap.add_argument("--partition", default="chunk", choices=sorted(PARTITIONS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-picard", action="store_true")
+    ap.add_argument("--no-alt-window", action="store_true")
+    ap.add_argument("--max-steps", type=int, default=None, help="PicardConfig::max_steps (default 300*M)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -242,7 +391,8 @@ def main():
     import paper_2406_01939_b200 as P
     inst, pol, plan, w = make_workload(args.workload, args.partition)
     T = w["T"]
-    cfg = P.PicardConfig(max_steps=300 * w["M"])
+    max_steps = default_window(args.workload) if args.max_steps is None else args.max_steps
+    cfg = P.PicardConfig(max_steps=max_steps)
     sim = P.Simulator(inst, pol, device=local)
     sim.set_plan(plan)
     if world > 1:
@@ -333,6 +483,26 @@ def main():
                         "policy steps (feature build -> 3 MMAs -> argmax) whose latency chains, not tensor "
                         "or HBM throughput, set the step time (ncu: ~39% issue-active, tensor pipe ~16%)"}
 
+    # ---- the same trajectory with the CLI-default window (300*M), device-timed
+    alt = None
+    if max_steps != 300 * w["M"] and not args.no_alt_window:
+        acfg = P.PicardConfig(max_steps=300 * w["M"])
+        sim.simulate_resident(acfg)
+        ams = []
+        for _ in range(2):
+            flush.zero_()
+            ra = sim.simulate_resident(acfg)
+            ams.append(ra.timing["total_ms"])
+        if world > 1:
+            tt = torch.tensor([min(ams)], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ams = [float(tt.item())]
+        alt_actions = sim.download_actions()
+        alt = {"max_steps": 300 * w["M"], "ms_per_step": min(ams), "value": T / (min(ams) / 1000.0),
+               "iterations": ra.iterations_to_converged, "total_evals": ra.total_policy_evals,
+               "steps_critical": ra.timing["steps_critical"],
+               "same_trajectory": bool(np.array_equal(alt_actions, actions))}
+
     # ---- e2e through the public one-shot API from pinned host memory
     e2e = None
     if world == 1 and args.e2e_steps > 0:
@@ -358,21 +528,20 @@ def main():
                "api": "paper_2406_01939_b200.picard_simulate (pcd_picard_simulate: upload, plan CSR, "
                       "fixed point, download)"}
 
-    # ---- CPU baseline (rank 0, N=1)
-    cpu = None
+    # ---- CPU baselines (rank 0, N=1): the reference's serial path on a
+    # stratified sample, its Picard path on a prefix
+    cpu, cpic = None, None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        cpu, ref_prefix = cpu_baseline(inst, pol)
-        n = ref_prefix.size
-        cpu["prefix_equal"] = bool(np.array_equal(ref_prefix, actions[:n]))
+        cpu = cpu_baseline(inst, pol, actions)
+        if not args.no_cpu_picard:
+            cpic = cpu_picard(inst, pol, plan.owner, plan.processes)
 
     if rank == 0:
+        config = workload_config(args, world)
         line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": args.workload, **w, "policy": "dual MLP {2J+1,64,64,2J} seeded",
-                           "partition": PARTITIONS[args.partition], "max_steps": 300 * w["M"],
-                           "l2": "512 MiB flush before every step; working set > L2",
-                           "parallelism": f"processes sharded over {world} GPU(s)"},
+                "scaling": "strong", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+                "config": config,
                 "iterations": res.iterations_to_converged,
                 "steps_critical": tm["steps_critical"], "total_evals": tm["total_evals"],
                 "us_per_critical_step": 1000.0 * ms_per_step / max(1, tm["steps_critical"]),
@@ -382,7 +551,9 @@ def main():
                              "wall_ms_per_step": wall_ms / args.steps,
                              "host_gap_ms": tm["total_ms"] - sum(tm[k] for k in ("sweep_ms", "prep_ms", "publish_ms",
                                                                                     "advance_ms"))},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "cpu_picard": cpic, "e2e": e2e,
+                "cli_default_window": alt,
+                "trajectory_hash": trajectory_hash(actions),
                 "gpu_launches": int(sum(t["kernel_launches"] for t in timings)),
                 "clocks": clocks.summary()}
         if cpu:

@@ -127,7 +127,8 @@ typedef struct pcd_config {
                               features than the reference's seeded ones)      */
   int32_t tc_verify;       /* debug: re-evaluate EVERY row in FP64 and count
                               unflagged disagreements (pcd_timing.tc_unflagged_bad) */
-  int32_t reserved;
+  int32_t tc_tiles;        /* CTAs of the tensor-core sweep; 0 = one per SM (tests
+                              use fewer, so rows pull processes mid-iteration) */
 } pcd_config;
 
 /* PicardTraceRow (engine.hpp:128-134). */
@@ -359,6 +360,16 @@ int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* policy_evals);
 
 int pcd_last_timing(const pcd_handle* h, pcd_timing* out);
 
+/* Debug flags of a handle (not for production runs). */
+enum { PCD_DEBUG_TC_PROFILE = 1 /* per-phase clock64 totals of the tensor-core
+                                   sweep's CTA 0, printed to stderr per launch */ };
+int pcd_set_debug(pcd_handle* h, int32_t flags);
+
+/* The device checkpoint FoState (capacity[J], dense inventory[I*J]): the
+ * state at the start of the current window; after a converged pcd_simulate
+ * it is the trajectory's final state (advance_checkpoint, engine.hpp:514-526). */
+int pcd_checkpoint_state(pcd_handle* h, int32_t* capacity, int32_t* inventory);
+
 /* Debug/parity hook (theory::CacheTraceRecorder, theory.hpp:120-126): when
  * set, pcd_simulate copies the full cache into history[k*T .. (k+1)*T) after
  * iteration k+1 (first `cap_iterations` iterations). NULL disables. */
@@ -381,6 +392,18 @@ int pcd_picard_simulate(const pcd_instance* inst, const pcd_policy* policy,
 int pcd_nccl_unique_id(unsigned char out[128]);
 int pcd_attach_comm(pcd_handle* h, const unsigned char id[128], int32_t rank,
                     int32_t nranks);
+
+/* In-process loopback group (tests; no reference counterpart): the same
+ * multi-rank protocol (per-rank process shards, window-slot all-gather,
+ * scalar all-reduces) between N handles in ONE process — e.g. N handles on
+ * one GPU, each driven by its own host thread, since NCCL refuses duplicate
+ * devices. Every rank must call pcd_simulate concurrently; results are
+ * identical to a single rank. The group outlives pcd_loopback_destroy while
+ * handles remain attached. */
+typedef struct pcd_loopback pcd_loopback;
+pcd_loopback* pcd_loopback_create(int32_t nranks);
+void pcd_loopback_destroy(pcd_loopback* group);
+int pcd_attach_loopback(pcd_handle* h, pcd_loopback* group, int32_t rank);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -18,14 +18,27 @@
 //   picard::timewarp::time_warp_simulate    fo/timewarp.hpp:56-181
 //   picard::linear::picard_convergence_curve linear.cpp:279-330
 // for FoEnv x {GreedyPolicy, CapacityPenalizedPolicy, DualNetworkPolicy}.
-// Observers are not supported on the device path (they need per-step host
-// callbacks); the per-iteration cache history is available through
-// pcd_set_history instead.
+//
+// Observers (engine.hpp:194-223) keep the reference's call shapes:
+//   * SequentialObserver (on_state) on sequential_simulate: the device
+//     computes the trajectory, then the states are replayed on the host with
+//     the reference's own FoLocalState (a state is a pure function of the
+//     action prefix), so the observer sees every state entering t in [0, T];
+//     sequential_simulate_with_states is built on it exactly as in the
+//     reference (engine.hpp:277-291);
+//   * IterationObserver (on_iteration, e.g. theory::CacheTraceRecorder) on
+//     picard_simulate: the device records the cache after every iteration
+//     (pcd_set_history) and the callbacks are delivered in iteration order
+//     after the run, with the reference's (iteration, chunk, lo, hi, cache);
+//   * LocalStateObserver (on_local_state, e.g. theory::MonotonicityChecker)
+//     needs every process's local state at every step on the host: refused
+//     with ContractViolation.
 //
 // DualNetworkPolicy keeps its normalisation state (initial_, horizon_)
 // private; every reference call site builds it from the instance's initial
 // state and horizon (cli.cpp:324-349, tests), which is what the adapter
-// assumes. Pass a DualNormalization to state it explicitly.
+// assumes. Pass DeviceOptions{DualNormalization{...}} to state it
+// explicitly (and the CUDA device), after the reference's own arguments.
 #pragma once
 
 #include <cstdint>
@@ -44,6 +57,12 @@ namespace picard::b200 {
 struct DualNormalization {
   const fo::FoState* initial = nullptr;  // DualNetworkPolicy::initial_ (nullptr: env initial)
   std::int64_t horizon = -1;             // DualNetworkPolicy::horizon_ (-1: orders.size())
+};
+
+// Adapter arguments beyond the reference signatures (always last).
+struct DeviceOptions {
+  DualNormalization norm{};
+  int device = 0;
 };
 
 namespace detail {
@@ -181,14 +200,28 @@ inline std::vector<std::int32_t> nodes_of(std::span<const fo::FoAction> a) {
 
 }  // namespace detail
 
-// picard_simulate (engine.hpp:458-590) on the B200.
-template <typename P>
+namespace detail {
+template <typename Obs>
+void refuse_local_state_observer(Obs* observer) {
+  if constexpr (LocalStateObserver<Obs, fo::FoEnv>) {
+    if (observer != nullptr)
+      throw ContractViolation(
+          "local-state observers need every process's state at every step on the host; "
+          "the B200 device path does not support them");
+  }
+}
+}  // namespace detail
+
+// picard_simulate (engine.hpp:458-590) on the B200. Same arguments as the
+// reference (observer included, see the header comment), then DeviceOptions.
+template <typename P, typename Obs = NoObserver>
 PicardResult<fo::FoAction> picard_simulate(const fo::FoEnv& env, const P& policy,
                                            std::span<const fo::Order> orders, const PartitionPlan& plan,
                                            const PicardConfig& config = {},
                                            std::span<const fo::FoAction> initial_cache = {},
                                            std::span<const fo::FoAction> reference_actions = {},
-                                           DualNormalization norm = {}, int device = 0) {
+                                           Obs* observer = nullptr, const DeviceOptions& opts = {}) {
+  detail::refuse_local_state_observer(observer);
   const std::int64_t T = static_cast<std::int64_t>(orders.size());
   if (static_cast<std::int64_t>(plan.owner.size()) != T)
     throw ContractViolation("partition plan does not cover the horizon");
@@ -197,20 +230,35 @@ PicardResult<fo::FoAction> picard_simulate(const fo::FoEnv& env, const P& policy
   if (!reference_actions.empty() && static_cast<std::int64_t>(reference_actions.size()) != T)
     throw ContractViolation("reference action length must equal the horizon");
   auto m = detail::marshal(env, orders);
-  auto ps = detail::policy_spec(policy, m, norm);
-  detail::Handle h(m.view, ps.view, device);
+  auto ps = detail::policy_spec(policy, m, opts.norm);
+  detail::Handle h(m.view, ps.view, opts.device);
   int rc = pcd_set_plan(h.h, plan.owner.data(), plan.processes);
   if (rc) detail::raise(rc);
-  const pcd_config cfg{config.processes, config.record_trace ? 1 : 0, config.max_steps, config.max_iterations,
+  constexpr bool wants_iterations = IterationObserver<Obs, fo::FoEnv>;
+  const bool observe = wants_iterations && observer != nullptr;
+  const bool trace_on = config.record_trace || observe;  // the callbacks need (chunk, lo) per iteration
+  const pcd_config cfg{config.processes, trace_on ? 1 : 0, config.max_steps, config.max_iterations,
                        config.threads, PCD_ENGINE_AUTO, 0.0, 0, 0};
   const auto init = detail::nodes_of(initial_cache);
   const auto ref = detail::nodes_of(reference_actions);
   std::vector<std::int32_t> actions(static_cast<std::size_t>(T));
-  std::vector<pcd_trace_row> trace(config.record_trace ? static_cast<std::size_t>(4 * T + 16) : 1);
+  std::vector<pcd_trace_row> trace(trace_on ? static_cast<std::size_t>(4 * T + 16) : 1);
   pcd_result res{};
-  rc = pcd_simulate(h.h, &cfg, init.empty() ? nullptr : init.data(), ref.empty() ? nullptr : ref.data(),
-                    actions.data(), &res, trace.data(), config.record_trace ? static_cast<std::int64_t>(trace.size()) : 0);
+  auto run = [&] {
+    return pcd_simulate(h.h, &cfg, init.empty() ? nullptr : init.data(), ref.empty() ? nullptr : ref.data(),
+                        actions.data(), &res, trace.data(), trace_on ? static_cast<std::int64_t>(trace.size()) : 0);
+  };
+  rc = run();
   if (rc) detail::raise(rc, &res, &trace);
+  std::vector<std::int32_t> history;
+  if (observe && T > 0) {  // the run is deterministic: repeat it recording the cache after every iteration
+    const std::int64_t k = res.iterations_run;
+    history.assign(static_cast<std::size_t>(k * T), 0);
+    rc = pcd_set_history(h.h, history.data(), k);
+    if (rc == PCD_OK) rc = run();
+    pcd_set_history(h.h, nullptr, 0);
+    if (rc) detail::raise(rc, &res, &trace);
+  }
   PicardResult<fo::FoAction> out;
   out.actions.reserve(actions.size());
   for (auto a : actions) out.actions.push_back(fo::FoAction{a});
@@ -223,18 +271,34 @@ PicardResult<fo::FoAction> picard_simulate(const fo::FoEnv& env, const P& policy
     const auto& t = trace[static_cast<std::size_t>(i)];
     out.trace.push_back({t.chunk, t.iteration, t.changed_slots, t.max_process_evals, t.t_reset});
   }
+  if constexpr (wants_iterations) {
+    if (observe) {
+      std::vector<fo::FoAction> cache(static_cast<std::size_t>(T));
+      for (std::int64_t i = 0; i < res.trace_rows && i < res.iterations_run; ++i) {
+        const auto& row = trace[static_cast<std::size_t>(i)];
+        const std::int64_t hi = config.max_steps > 0 ? std::min(T, row.t_reset + config.max_steps) : T;
+        for (std::int64_t t = 0; t < T; ++t)
+          cache[static_cast<std::size_t>(t)] = fo::FoAction{history[static_cast<std::size_t>(i * T + t)]};
+        observer->on_iteration(row.iteration, row.chunk, row.t_reset, hi, std::span<const fo::FoAction>(cache));
+      }
+    }
+  }
   return out;
 }
 
 // picard_iterate_once (engine.hpp:358-444) on the B200; `cache` updated in place.
-template <typename P>
+template <typename P, typename Obs = NoObserver>
 IterationOutcome picard_iterate_once(const fo::FoEnv& env, const P& policy, std::span<const fo::Order> orders,
                                      const PartitionPlan& plan, ActionCache<fo::FoAction>& cache,
                                      std::int64_t t_lo, std::int64_t t_hi, const fo::FoState& checkpoint_state,
-                                     DualNormalization norm = {}, int device = 0) {
+                                     const IterateOptions& options = {}, Obs* observer = nullptr,
+                                     std::int64_t iteration = 0, const DeviceOptions& opts = {}) {
+  (void)options;    // IterateOptions::threads: the device ignores it
+  (void)iteration;  // only passed on to local-state observers, which are refused
+  detail::refuse_local_state_observer(observer);
   auto m = detail::marshal(env, orders);
-  auto ps = detail::policy_spec(policy, m, norm);
-  detail::Handle h(m.view, ps.view, device);
+  auto ps = detail::policy_spec(policy, m, opts.norm);
+  detail::Handle h(m.view, ps.view, opts.device);
   int rc = pcd_set_plan(h.h, plan.owner.data(), plan.processes);
   if (rc) detail::raise(rc);
   std::vector<std::int32_t> ck_cap, ck_inv;
@@ -253,14 +317,16 @@ IterationOutcome picard_iterate_once(const fo::FoEnv& env, const P& policy, std:
 }
 
 // sequential_simulate (engine.hpp:237-267): the serial trajectory, computed
-// on the device as the Picard fixed point (Prop. 1); policy_evals = T.
-template <typename P>
+// on the device as the Picard fixed point (Prop. 1); policy_evals = T. A
+// SequentialObserver sees the states entering every t in [0, T], replayed on
+// the host with the reference's FoLocalState from the device's actions.
+template <typename P, typename Obs = NoObserver>
 SequentialOutput<fo::FoAction> sequential_simulate(const fo::FoEnv& env, const P& policy,
-                                                   std::span<const fo::Order> orders,
-                                                   DualNormalization norm = {}, int device = 0) {
+                                                   std::span<const fo::Order> orders, Obs* observer = nullptr,
+                                                   const DeviceOptions& opts = {}) {
   auto m = detail::marshal(env, orders);
-  auto ps = detail::policy_spec(policy, m, norm);
-  detail::Handle h(m.view, ps.view, device);
+  auto ps = detail::policy_spec(policy, m, opts.norm);
+  detail::Handle h(m.view, ps.view, opts.device);
   std::vector<std::int32_t> actions(orders.size());
   std::int64_t evals = 0;
   const int rc = pcd_sequential(h.h, actions.data(), &evals);
@@ -268,7 +334,35 @@ SequentialOutput<fo::FoAction> sequential_simulate(const fo::FoEnv& env, const P
   SequentialOutput<fo::FoAction> out;
   for (auto a : actions) out.actions.push_back(fo::FoAction{a});
   out.policy_evals = evals;
+  if constexpr (SequentialObserver<Obs, fo::FoEnv>) {
+    if (observer != nullptr) {
+      auto local = env.make_local();
+      const auto start = env.initial_state();
+      env.reset_local(local, start);
+      for (std::size_t t = 0; t < orders.size(); ++t) {
+        observer->on_state(static_cast<std::int64_t>(t), local);
+        env.apply_local(local, out.actions[t], orders[t]);
+      }
+      observer->on_state(static_cast<std::int64_t>(orders.size()), local);
+    }
+  }
   return out;
+}
+
+// sequential_simulate_with_states (engine.hpp:277-291): actions plus the
+// state entering every step (size T + 1), through the observer path above.
+template <typename P>
+SequentialTrajectory<fo::FoEnv> sequential_simulate_with_states(const fo::FoEnv& env, const P& policy,
+                                                                std::span<const fo::Order> orders,
+                                                                const DeviceOptions& opts = {}) {
+  struct Recorder {
+    const fo::FoEnv* env;
+    std::vector<fo::FoState> states;
+    void on_state(std::int64_t, const fo::FoLocalState& local) { states.push_back(env->snapshot(local)); }
+  } recorder{&env, {}};
+  recorder.states.reserve(orders.size() + 1);
+  auto out = sequential_simulate(env, policy, orders, &recorder, opts);
+  return {std::move(out.actions), std::move(recorder.states)};
 }
 
 #if __has_include("picard/fo/timewarp.hpp")
@@ -281,12 +375,12 @@ template <typename P>
 timewarp::TimeWarpResult time_warp_simulate(const fo::Instance& instance, const P& policy, std::int32_t processes,
                                             std::uint64_t seed, bool record_trace = false,
                                             timewarp::WindowRule rule = timewarp::WindowRule::min_capacity,
-                                            DualNormalization norm = {}, int device = 0) {
+                                            const DeviceOptions& opts = {}) {
   const auto env = instance.make_env();
   const std::span<const fo::Order> orders(instance.orders);
   auto m = detail::marshal(env, orders);
-  auto ps = detail::policy_spec(policy, m, norm);
-  detail::Handle h(m.view, ps.view, device);
+  auto ps = detail::policy_spec(policy, m, opts.norm);
+  detail::Handle h(m.view, ps.view, opts.device);
   std::vector<std::int32_t> actions(orders.size());
   std::vector<pcd_tw_trace_row> rows(record_trace ? 2 * orders.size() + 4 : 1);
   pcd_tw_result res{};

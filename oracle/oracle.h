@@ -172,6 +172,14 @@ int ref_picard_timed(const orc_instance* inst, const orc_policy* pol,
                      const int32_t* owner, int32_t processes, int64_t max_steps,
                      int32_t threads, int32_t* actions, int64_t* iterations,
                      int64_t* seq_equiv, double* seconds);
+/* segmented serial trajectory (bench.py reference arm) */
+void* ref_session_create(const orc_instance* inst, const orc_policy* pol);
+void ref_session_destroy(void* session);
+int ref_session_set_state(void* session, int64_t t, const int32_t* cap, const int32_t* inv);
+int ref_session_get_state(void* session, int64_t* t, int32_t* cap, int32_t* inv);
+int ref_session_total_reward(void* session, const int32_t* actions, double* total);
+int ref_session_sequential(void* session, int64_t t1, int32_t* actions, double* seconds,
+                           int64_t* error_t);
 
 #ifdef __cplusplus
 }

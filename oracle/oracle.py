@@ -320,6 +320,10 @@ class _Lib:
                                            C.byref(it), C.byref(se), C.byref(sec)))
         return actions[:int(inst.horizon)], it.value, se.value, sec.value
 
+    def session(self, inst, pol):
+        """REF only: a segmented sequential trajectory (RefSession)."""
+        return RefSession(self, inst, pol)
+
     def depletion(self, inst, actions):
         ci, k1 = self._inst(inst)
         out = np.zeros(int(inst.nodes), np.int64)
@@ -384,6 +388,70 @@ class _Lib:
         out = C.c_double()
         self.check(self.fn("total_reward")(C.byref(ci), _p(a, C.c_int32), C.byref(out)))
         return out.value
+
+
+class RefSession:
+    """The reference's sequential_simulate run as consecutive segments over one
+    marshalled instance (ref_session_* in ref_harness.cpp): ``run(t1)`` times
+    sequential_simulate over [at, t1) from the carried state and returns
+    (actions, seconds). Concatenated segments are one serial trajectory."""
+
+    def __init__(self, lib, inst, pol):
+        self.lib = lib
+        self.J, self.I, self.T = int(inst.nodes), int(inst.products), int(inst.horizon)
+        self._ci, self._k1 = lib._inst(inst)
+        self._cp, self._k2 = lib._pol(pol)
+        f = lib.fn("session_create")
+        f.restype = C.c_void_p
+        self.h = f(C.byref(self._ci), C.byref(self._cp))
+        if not self.h:
+            raise OracleError(1, lib.err())
+        lib.fn("session_destroy").argtypes = [C.c_void_p]
+        lib.fn("session_sequential").argtypes = [C.c_void_p, C.c_int64, _I32P, C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_int64)]
+        lib.fn("session_set_state").argtypes = [C.c_void_p, C.c_int64, _I32P, _I32P]
+        lib.fn("session_get_state").argtypes = [C.c_void_p, C.POINTER(C.c_int64), _I32P, _I32P]
+
+    def run(self, t1):
+        t1 = int(t1)
+        _, at, _, _ = self.state()
+        actions = np.zeros(max(t1 - at, 1), np.int32)
+        sec = C.c_double()
+        et = C.c_int64(-1)
+        rc = self.lib.fn("session_sequential")(self.h, t1, _p(actions, C.c_int32), C.byref(sec), C.byref(et))
+        self.lib.check(rc, et.value)
+        return actions[:t1 - at], sec.value
+
+    def total_reward(self, actions):
+        a = np.ascontiguousarray(actions, np.int32)
+        out = C.c_double()
+        f = self.lib.fn("session_total_reward")
+        f.argtypes = [C.c_void_p, _I32P, C.POINTER(C.c_double)]
+        self.lib.check(f(self.h, _p(a, C.c_int32), C.byref(out)))
+        return out.value
+
+    def set_state(self, t, cap, inv):
+        cap = np.ascontiguousarray(cap, np.int32)
+        inv = np.ascontiguousarray(inv, np.int32)
+        self.lib.check(self.lib.fn("session_set_state")(self.h, int(t), _p(cap, C.c_int32), _p(inv, C.c_int32)))
+
+    def state(self):
+        cap = np.zeros(self.J, np.int32)
+        inv = np.zeros(self.I * self.J, np.int32)
+        t = C.c_int64()
+        self.lib.check(self.lib.fn("session_get_state")(self.h, C.byref(t), _p(cap, C.c_int32), _p(inv, C.c_int32)))
+        return None, t.value, cap, inv
+
+    def close(self):
+        if self.h:
+            self.lib.fn("session_destroy")(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def build(quiet=True):

@@ -508,6 +508,97 @@ int ref_total_reward(const orc_instance* in, const int32_t* actions, double* tot
   });
 }
 
+// ------------------------------------------------------- serial sessions
+// One sequential trajectory run as consecutive segments (bench.py's reference
+// arm): the instance is marshalled once; each segment is the reference's own
+// sequential_simulate over orders [t0, t1) on an FoEnv built from the state
+// the previous segments reached (carried with the reference's apply_in_place,
+// types.hpp:89-100), the policy keeping the instance's normalisation state
+// and horizon. Concatenated segments are exactly one sequential_simulate of
+// the whole horizon: its state at t0 is that same carried state.
+struct RefSession {
+  orc_instance in;
+  orc_policy pol;
+  Instance inst;
+  FoState state;
+  int64_t at = 0;
+};
+
+void* ref_session_create(const orc_instance* in, const orc_policy* pol) {
+  try {
+    auto s = std::make_unique<RefSession>();
+    s->in = *in;
+    s->pol = *pol;
+    s->inst = make_instance(in);
+    s->state = s->inst.initial;
+    return s.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_session_destroy(void* p) { delete static_cast<RefSession*>(p); }
+
+// state at time t (cap[J], dense inv[I*J]); the next segment must start at t
+int ref_session_set_state(void* p, int64_t t, const int32_t* cap, const int32_t* inv) {
+  return guarded([&] {
+    auto* s = static_cast<RefSession*>(p);
+    if (t < 0 || t > s->in.horizon) throw std::invalid_argument("session time out of range");
+    s->state = make_state(s->in.nodes, s->in.products, cap, inv);
+    s->at = t;
+    return 0;
+  });
+}
+
+int ref_session_get_state(void* p, int64_t* t, int32_t* cap, int32_t* inv) {
+  return guarded([&] {
+    auto* s = static_cast<RefSession*>(p);
+    const int32_t J = s->in.nodes;
+    *t = s->at;
+    for (int32_t j = 0; j < J; ++j) cap[j] = s->state.capacity[(size_t)j];
+    std::memset(inv, 0, sizeof(int32_t) * (size_t)s->in.products * J);
+    for (const auto& [i, row] : s->state.inventory)
+      for (int32_t j = 0; j < J; ++j) inv[(size_t)i * J + j] = row[(size_t)j];
+    return 0;
+  });
+}
+
+// fo_total_reward (env.hpp) of a whole-horizon trajectory over the session's orders
+int ref_session_total_reward(void* p, const int32_t* actions, double* total) {
+  return guarded([&] {
+    auto* s = static_cast<RefSession*>(p);
+    std::vector<FoAction> a((size_t)s->in.horizon);
+    for (int64_t t = 0; t < s->in.horizon; ++t) a[(size_t)t] = FoAction{actions[t]};
+    *total = fo_total_reward(std::span<const Order>(s->inst.orders), std::span<const FoAction>(a));
+    return 0;
+  });
+}
+
+// sequential_simulate over orders [at, t1) (timed alone), then the state carry
+int ref_session_sequential(void* p, int64_t t1, int32_t* actions, double* seconds, int64_t* error_t) {
+  auto* s = static_cast<RefSession*>(p);
+  return guarded(
+      [&] {
+        if (t1 < s->at || t1 > s->in.horizon) throw std::invalid_argument("segment end out of range");
+        const std::span<const Order> seg(s->inst.orders.data() + s->at, (size_t)(t1 - s->at));
+        FoEnv env(s->state, s->in.products);
+        return with_policy(&s->in, &s->pol, s->inst, [&](const auto& policy) {
+          const auto c0 = std::chrono::steady_clock::now();
+          auto out = sequential_simulate(env, policy, seg);
+          const auto c1 = std::chrono::steady_clock::now();
+          *seconds = std::chrono::duration<double>(c1 - c0).count();
+          for (size_t k = 0; k < out.actions.size(); ++k) {
+            actions[k] = out.actions[k].node;
+            apply_in_place(s->state, seg[k], out.actions[k]);
+          }
+          s->at = t1;
+          return 0;
+        });
+      },
+      error_t);
+}
+
 // theory::compute_depletion_from_capacities on the capacities of the
 // trajectory `actions` replayed from the initial state (fo_transition)
 int ref_depletion(const orc_instance* in, const int32_t* actions, int64_t* first_depleted_at) {

@@ -54,7 +54,7 @@ class pcd_policy(C.Structure):
 class pcd_config(C.Structure):
     _fields_ = [("processes", C.c_int32), ("record_trace", C.c_int32), ("max_steps", C.c_int64),
                 ("max_iterations", C.c_int64), ("threads", C.c_int32), ("engine", C.c_int32),
-                ("tc_guard", C.c_double), ("tc_verify", C.c_int32), ("reserved", C.c_int32)]
+                ("tc_guard", C.c_double), ("tc_verify", C.c_int32), ("tc_tiles", C.c_int32)]
 
 
 class pcd_trace_row(C.Structure):
@@ -124,11 +124,16 @@ SIGNATURES = {
     "pcd_sequential": (C.c_int, [C.c_void_p, I32P, I64P]),
     "pcd_last_timing": (C.c_int, [C.c_void_p, C.POINTER(pcd_timing)]),
     "pcd_set_history": (C.c_int, [C.c_void_p, I32P, C.c_int64]),
+    "pcd_checkpoint_state": (C.c_int, [C.c_void_p, I32P, I32P]),
+    "pcd_set_debug": (C.c_int, [C.c_void_p, C.c_int32]),
     "pcd_picard_simulate": (C.c_int, [C.POINTER(pcd_instance), C.POINTER(pcd_policy), I32P, C.c_int32,
                                       C.POINTER(pcd_config), I32P, I32P, I32P, C.POINTER(pcd_result),
                                       C.POINTER(pcd_trace_row), C.c_int64]),
     "pcd_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte * 128)]),
     "pcd_attach_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_ubyte * 128), C.c_int32, C.c_int32]),
+    "pcd_loopback_create": (C.c_void_p, [C.c_int32]),
+    "pcd_loopback_destroy": (None, [C.c_void_p]),
+    "pcd_attach_loopback": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
 
 

@@ -389,11 +389,12 @@ class PicardConfig:
     engine: str = "auto"
     tc_guard: float = 0.0
     tc_verify: bool = False
+    tc_tiles: int = 0
 
     def to_c(self):
         return K.pcd_config(int(self.processes), 1 if self.record_trace else 0, int(self.max_steps),
                             int(self.max_iterations), int(self.threads), ENGINES[self.engine],
-                            float(self.tc_guard), 1 if self.tc_verify else 0, 0)
+                            float(self.tc_guard), 1 if self.tc_verify else 0, int(self.tc_tiles))
 
 
 @dataclass
@@ -566,14 +567,49 @@ class Simulator:
         _check(LIB.pcd_sequential(self._h, _ptr(actions), C.byref(ev)))
         return SequentialOutput(actions[:T], ev.value)
 
+    def checkpoint_state(self):
+        """The device checkpoint FoState (capacities [J], inventory [I, J]);
+        after a converged simulate, the trajectory's final state."""
+        J, I = int(self.instance.nodes), int(self.instance.products)
+        cap = np.zeros(J, np.int32)
+        inv = np.zeros(I * J, np.int32)
+        _check(LIB.pcd_checkpoint_state(self._h, _ptr(cap), _ptr(inv)))
+        return cap, inv.reshape(I, J)
+
     def timing(self) -> dict:
         t = K.pcd_timing()
         LIB.pcd_last_timing(self._h, C.byref(t))
         return _timing_dict(t)
 
+    def attach_loopback(self, group: "LoopbackGroup", rank: int):
+        _check(LIB.pcd_attach_loopback(self._h, C.c_void_p(group._g), int(rank)))
+
     def attach_comm(self, unique_id: bytes, rank: int, nranks: int):
         buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
         _check(LIB.pcd_attach_comm(self._h, C.byref(buf), int(rank), int(nranks)))
+
+
+class LoopbackGroup:
+    """In-process loopback communicator of ``nranks`` ranks
+    (pcd_loopback_create): the multi-GPU protocol between handles of one
+    process, e.g. N Simulators on one GPU each driven by its own thread."""
+
+    def __init__(self, nranks: int):
+        self._g = LIB.pcd_loopback_create(int(nranks))
+        if not self._g:
+            raise InvalidArgument(_err())
+        self.nranks = int(nranks)
+
+    def close(self):
+        if self._g:
+            LIB.pcd_loopback_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def nccl_unique_id() -> bytes:

@@ -9,7 +9,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <map>
 #include <mutex>
 #include <cstdio>
@@ -26,12 +28,11 @@
 #include "capi_internal.h"
 #include "general.cuh"
 #include "kernels.cuh"
-#include "tc_sweep.cuh"
+#include "tc_common.cuh"
 
 namespace pcd {
 
-void launch_tc_sweep(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_sweep.cu (128-row lockstep)
-void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream);     // tc_pp.cu (two 64-row halves)
+cudaError_t launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_pp.cu (two 64-row halves)
 int tc_pp_width_class(int J);  // tc_pp.cu: layer-3 width class of the ping-pong sweep for J nodes
 size_t tc_smem_bytes();
 
@@ -119,6 +120,11 @@ struct DBuf {
     p = (T*)g_pool.get(count * sizeof(T), &bytes);
     n = count;
   }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(bytes, o.bytes);
+  }
   void upload(const T* h, size_t count, cudaStream_t s) {
     alloc(count);
     if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -155,6 +161,113 @@ struct NcclApi {
 };
 static NcclApi g_nccl;
 enum { ncclInt32 = 2, ncclInt64 = 4, ncclUint64 = 5, ncclSum = 0, ncclMax = 2, ncclMin = 3 };
+
+// The communicator of one rank: an all-gather of int32
+// cache slices and integer all-reduces of the convergence scalars. NCCL over
+// NVLink / NVSwitch between processes (one per GPU), or an in-process
+// loopback group: N handles on one device, each driven by its own host
+// thread — the test harness that runs the multi-rank code path (exchange,
+// pack / unpack, per-rank process masks, shards) on a single GPU, where NCCL
+// refuses duplicate devices.
+enum class RedOp { SumI64, MinU64, MaxU64 };
+struct Comm {
+  virtual ~Comm() = default;
+  virtual void all_gather(const int* send, int* recv, size_t count, cudaStream_t s) = 0;
+  virtual void all_reduce(long long* buf, size_t count, RedOp op, cudaStream_t s) = 0;
+};
+
+struct NcclComm final : Comm {
+  nccl_comm c = nullptr;
+  ~NcclComm() override {
+    if (c && g_nccl.CommDestroy) g_nccl.CommDestroy(c);
+  }
+  static void check(int rc, const char* what) {
+    if (rc) throw CudaError(std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));
+  }
+  void all_gather(const int* send, int* recv, size_t count, cudaStream_t s) override {
+    check(g_nccl.AllGather(send, recv, count, ncclInt32, c, s), "ncclAllGather");
+  }
+  void all_reduce(long long* buf, size_t count, RedOp op, cudaStream_t s) override {
+    const int dt = op == RedOp::SumI64 ? ncclInt64 : ncclUint64;
+    const int o = op == RedOp::SumI64 ? ncclSum : op == RedOp::MinU64 ? ncclMin : ncclMax;
+    check(g_nccl.AllReduce(buf, buf, count, dt, o, c, s), "ncclAllReduce");
+  }
+};
+
+struct LoopbackGroup {
+  static constexpr size_t kMaxReduce = 64;
+  int n = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  int* staging = nullptr;  // device
+  size_t staging_cap = 0;  // ints
+  std::vector<long long> host;  // n x kMaxReduce
+  explicit LoopbackGroup(int nr) : n(nr), host((size_t)nr * kMaxReduce) {}
+  ~LoopbackGroup() {
+    if (staging) cudaFree(staging);
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g; }))
+      throw CudaError("loopback group: a rank did not reach the collective (timeout)");
+  }
+};
+
+struct LoopbackComm final : Comm {
+  std::shared_ptr<LoopbackGroup> g;
+  int rank = 0;
+  void all_gather(const int* send, int* recv, size_t count, cudaStream_t s) override {
+    CK(cudaStreamSynchronize(s));  // this rank's send slice is complete
+    g->barrier();
+    if (rank == 0 && g->staging_cap < count * g->n) {
+      if (g->staging) CK(cudaFree(g->staging));
+      g->staging = nullptr;
+      CK(cudaMalloc(&g->staging, sizeof(int) * count * g->n));
+      g->staging_cap = count * g->n;
+    }
+    g->barrier();
+    if (count) {
+      CK(cudaMemcpyAsync(g->staging + (size_t)rank * count, send, sizeof(int) * count, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    g->barrier();
+    if (count) {
+      CK(cudaMemcpyAsync(recv, g->staging, sizeof(int) * count * g->n, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    g->barrier();  // nobody refills the staging buffer before every rank has read it
+  }
+  void all_reduce(long long* buf, size_t count, RedOp op, cudaStream_t s) override {
+    if (count > LoopbackGroup::kMaxReduce) throw InvalidArgument("loopback reduce too large");
+    long long mine[LoopbackGroup::kMaxReduce];
+    CK(cudaMemcpyAsync(mine, buf, sizeof(long long) * count, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::copy(mine, mine + count, g->host.begin() + (size_t)rank * LoopbackGroup::kMaxReduce);
+    g->barrier();
+    for (size_t i = 0; i < count; ++i) {
+      long long v = g->host[i];
+      for (int r = 1; r < g->n; ++r) {
+        const long long w = g->host[(size_t)r * LoopbackGroup::kMaxReduce + i];
+        if (op == RedOp::SumI64) v += w;
+        else if (op == RedOp::MinU64) v = (long long)std::min((unsigned long long)v, (unsigned long long)w);
+        else v = (long long)std::max((unsigned long long)v, (unsigned long long)w);
+      }
+      mine[i] = v;
+    }
+    g->barrier();  // every rank has read the inputs
+    CK(cudaMemcpyAsync(buf, mine, sizeof(long long) * count, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+};
 
 }  // namespace pcd
 
@@ -201,20 +314,22 @@ struct pcd_handle {
   bool resident_valid = false;
   int32_t* history = nullptr;  // host, pcd_set_history
   int64_t history_cap = 0;
-  // tensor-core policy (tc_sweep.cu)
+  // tensor-core policy (tc_pp.cu)
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   double tc_guard = 5e-5;                // tc_scaled_guard
   int tc_n3 = 0;                         // layer-3 width class of the ping-pong image (prepare_tc)
-  pcd::DBuf<unsigned char> tc_wimg, tc_wimg2;
-  pcd::DBuf<float> tc_b1, tc_b2, tc_b3, tc_ic0, tc_ix0, tc_rtf, tc_rtq;
+  pcd::DBuf<unsigned char> tc_wimg2;
+  pcd::DBuf<float> tc_b1, tc_b2, tc_ic0, tc_ix0, tc_rtq;
+  int debug = 0;                         // pcd_set_debug flags
+  pcd::DBuf<long long> tc_prof;          // PCD_DEBUG_TC_PROFILE: phase clocks of CTA 0
   pcd::DBuf<unsigned long long> tc_stats;
   int32_t tc_tiles = 0;
   int64_t max_load = 0;
   // multi-GPU
   int32_t rank = 0, nranks = 1;
-  pcd::nccl_comm comm = nullptr;
+  std::unique_ptr<pcd::Comm> comm;  // NCCL, or a loopback group (tests)
   std::vector<int32_t> rank_of;
-  std::vector<int32_t> h_roff;
+  std::vector<int32_t> h_roff, h_rslots;  // rank-major, time-ordered owned slots (host copy)
   int32_t maxn = 0;
   pcd::DBuf<unsigned char> d_mine;
   pcd::DBuf<int> d_roff, d_rslots, d_send, d_recv;
@@ -232,7 +347,7 @@ struct pcd_handle {
     return m;
   }
   ~pcd_handle() {
-    if (comm && pcd::g_nccl.CommDestroy) pcd::g_nccl.CommDestroy(comm);
+    comm.reset();
     if (scal) cudaFree(scal);
     if (h_scal) cudaFreeHost(h_scal);
     if (d_errt) cudaFree(d_errt);
@@ -241,7 +356,7 @@ struct pcd_handle {
 };
 
 // multi-GPU helpers (defined with the C ABI below)
-static void exchange(pcd_handle* h, int* buf, bool reduce);
+static void exchange(pcd_handle* h, int* buf, bool reduce, int lo, int hi);
 static void rebuild_shards(pcd_handle* h);
 
 namespace pcd {
@@ -351,11 +466,7 @@ static void launch_product_sweep(pcd_handle* h, int lo, int hi, long long* evals
   a.mine = h->comm ? h->d_mine.p : nullptr;
   const int wpb = 4;
   const size_t smem = warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
-  static bool attr_set[4] = {false, false, false, false};
-  if (smem > 48 * 1024 && !attr_set[KIND]) {
-    CK(cudaFuncSetAttribute(k_sweep_product<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[KIND] = true;
-  }
+  CK(ensure_dyn_smem((const void*)k_sweep_product<KIND>, smem));
   k_sweep_product<KIND><<<(h->M + wpb - 1) / wpb, wpb * 32, smem, h->stream>>>(a);
   CK(cudaGetLastError());
 }
@@ -368,11 +479,7 @@ static void launch_replay_sweep(pcd_handle* h, int lo, int hi, long long* evals_
   h->scratch.alloc(std::max<size_t>(1, per * (size_t)batch));
   const int wpb = 4;
   const size_t smem = warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
-  static bool attr_set[4] = {false, false, false, false};
-  if (smem > 48 * 1024 && !attr_set[KIND]) {
-    CK(cudaFuncSetAttribute(k_sweep_replay<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[KIND] = true;
-  }
+  CK(ensure_dyn_smem((const void*)k_sweep_replay<KIND>, smem));
   for (int m0 = 0; m0 < h->M; m0 += batch) {
     ReplayArgs a{};
     a.model = h->model();
@@ -410,7 +517,8 @@ static void throw_sweep_error(pcd_handle* h) {
 }
 
 // One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
-static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify) {
+static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify,
+                      int tiles_req = 0) {
   TcArgs a{};
   SweepArgs& s = a.s;
   s.model = h->model();
@@ -440,32 +548,25 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
                                                  bits, h->stream));
     h->timing.kernel_launches += 2;
   }
-  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg = h->tc_wimg.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
-  a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p; a.b3f = h->tc_b3.p;
-  a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabf = h->tc_rtf.p; a.rtabq = h->tc_rtq.p;
+  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
+  a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p;
+  a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabq = h->tc_rtq.p;
   a.guard = (float)(guard > 0 ? guard : h->tc_guard);
   a.verify = verify;
   a.stats = h->tc_stats.p;
-  static const int pf = getenv("PCD_TC_PF") ? atoi(getenv("PCD_TC_PF")) : 0;  // tuning knob
-  a.pf = pf;
-  // PCD_TC_PROF=1: per-phase clock64 totals of CTA 0, printed to stderr (debug)
-  static const bool prof = getenv("PCD_TC_PROF") != nullptr;
-  static DBuf<long long> dprof;
+  // PCD_DEBUG_TC_PROFILE: per-phase clock64 totals of CTA 0, printed to stderr
+  const bool prof = (h->debug & PCD_DEBUG_TC_PROFILE) != 0;
   if (prof) {
-    dprof.alloc(20);
-    CK(cudaMemsetAsync(dprof.p, 0, 20 * sizeof(long long), h->stream));
-    a.prof = dprof.p;
+    h->tc_prof.alloc(20);
+    CK(cudaMemsetAsync(h->tc_prof.p, 0, 20 * sizeof(long long), h->stream));
+    a.prof = h->tc_prof.p;
   }
-  // PCD_TC_TILES=n (tests): fewer CTAs than SMs, so rows pull from the work list
-  int tiles = h->tc_tiles;
-  if (const char* e = getenv("PCD_TC_TILES")) tiles = std::max(1, std::min(tiles, atoi(e)));
-  static const bool lockstep = getenv("PCD_TC_LOCKSTEP") != nullptr;  // A/B knob
-  if (lockstep) launch_tc_sweep(a, tiles, h->stream);
-  else launch_tc_pp(a, tiles, h->stream);
-  CK(cudaGetLastError());
+  // tiles < SMs (tests): rows pull processes from the work list mid-iteration
+  const int tiles = tiles_req > 0 ? std::min(h->tc_tiles, tiles_req) : h->tc_tiles;
+  CK(launch_tc_pp(a, tiles, h->stream));
   if (prof) {
     long long v[20];
-    CK(cudaMemcpyAsync(v, dprof.p, sizeof v, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(v, h->tc_prof.p, sizeof v, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     fprintf(stderr, "tcprof steps=%lld F=%lld(own %lld) L1=%lld E1=%lld L2=%lld E2=%lld L3=%lld S=%lld fin=%lld chk=%lld U=%lld\n",
             v[10], v[0], v[11], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
@@ -485,11 +586,7 @@ static int build_hck(pcd_handle* h, int lo, int hi) {
   const int nb = hck_rows(lo, hi);
   const int nseg = (nb + kSegRows - 1) / kSegRows;
   const size_t hsm = (size_t)kSegRows * J * 4;
-  static size_t hsm_set = 0;
-  if (hsm > 48 * 1024 && hsm > hsm_set) {
-    CK(cudaFuncSetAttribute(k_hist_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-    hsm_set = hsm;
-  }
+  CK(ensure_dyn_smem((const void*)k_hist_prefix, hsm));
   k_seg_count<<<nseg, 256, (size_t)J * 4, h->stream>>>(h->ev.p, lo, hi, J, h->seg.p);
   {
     const int nblk = std::max(1, std::min(256, nseg));
@@ -564,17 +661,13 @@ static void launch_general_sweep(pcd_handle* h, int lo, int hi, long long* evals
   a.mine = h->comm ? h->d_mine.p : nullptr;
   const int wpb = 4;
   const size_t smem = gen_warp_smem_bytes(h->J, 2 * h->J + 1, h->H, 2 * h->J) * wpb;
-  static bool attr_set[4] = {false, false, false, false};
-  if (smem > 48 * 1024 && !attr_set[KIND]) {
-    CK(cudaFuncSetAttribute(k_sweep_general<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[KIND] = true;
-  }
+  CK(ensure_dyn_smem((const void*)k_sweep_general<KIND>, smem));
   k_sweep_general<KIND><<<(h->M + wpb - 1) / wpb, wpb * 32, smem, h->stream>>>(a);
   CK(cudaGetLastError());
 }
 
 static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
-                             double guard = 0.0, int verify = 0) {
+                             double guard = 0.0, int verify = 0, int tiles = 0) {
   IterOut out;
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
   reset_scalars(h);
@@ -587,7 +680,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     h->timing.prep_ms += tm.stop_ms();
     tm.start();
     dispatch_kind(h->kind, [&](auto k) { launch_general_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
-    exchange(h, h->cache.p, true);  // N>1: owned slots + convergence scalars
+    exchange(h, h->cache.p, true, lo, hi);  // N>1: owned window slots + convergence scalars
     if (h->comm) CK(cudaMemsetAsync(h->written.p + lo, 1, (size_t)W, h->stream));
     h->timing.sweep_ms += tm.stop_ms();
     h->timing.kernel_launches += 1;
@@ -607,13 +700,13 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {
-      launch_tc(h, lo, hi, evals_out, guard, verify);
+      launch_tc(h, lo, hi, evals_out, guard, verify, tiles);
       h->timing.tc_used = 1;
       h->timing.tc_tiles = h->tc_tiles;
     } else {
       dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
     }
-    exchange(h, h->cache.p, true);  // N>1: owned slots + convergence scalars
+    exchange(h, h->cache.p, true, lo, hi);  // N>1: owned window slots + convergence scalars
     if (h->comm)  // every window slot is owned by some rank: all written now
       CK(cudaMemsetAsync(h->written.p + lo, 1, (size_t)W, h->stream));
     h->timing.sweep_ms += tm.stop_ms();
@@ -623,12 +716,11 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     tm.start();
     dispatch_kind(h->kind, [&](auto k) { launch_replay_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
     if (h->comm) {  // fresh[] slices to every rank; then a replicated publish
-      exchange(h, h->fresh.p, false);
+      exchange(h, h->fresh.p, false, lo, hi);
       k_scalars_pack<<<1, 1, 0, h->stream>>>(h->scal, h->d_red.p);
-      int rc = g_nccl.AllReduce(h->d_red.p + 3, h->d_red.p + 3, 1, ncclInt64, ncclSum, h->comm, h->stream);
-      if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 5, h->d_red.p + 5, 2, ncclUint64, ncclMin, h->comm, h->stream);
-      if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 7, h->d_red.p + 7, 1, ncclUint64, ncclMax, h->comm, h->stream);
-      if (rc) throw CudaError(std::string("ncclAllReduce: ") + g_nccl.GetErrorString(rc));
+      h->comm->all_reduce(h->d_red.p + 3, 1, RedOp::SumI64, h->stream);
+      h->comm->all_reduce(h->d_red.p + 5, 2, RedOp::MinU64, h->stream);
+      h->comm->all_reduce(h->d_red.p + 7, 1, RedOp::MaxU64, h->stream);
       k_scalars_unpack<<<1, 1, 0, h->stream>>>(h->d_red.p, h->scal);
     }
     h->timing.sweep_ms += tm.stop_ms();
@@ -759,7 +851,7 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
                            iteration, rows);
     }
     ++iteration;
-    IterOut it = run_iteration(h, engine, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify);
+    IterOut it = run_iteration(h, engine, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify, cfg->tc_tiles);
     res->iterations_to_converged += 1;
     res->policy_eval_count_sequential_equivalent += it.max_evals;
     res->total_policy_evals += it.total_evals;
@@ -897,6 +989,7 @@ static void rebuild_shards(pcd_handle* h) {
     std::vector<int32_t> fill(off.begin(), off.end() - 1);
     for (int64_t t = 0; t < T; ++t) slots[(size_t)fill[(size_t)h->rank_of[(size_t)owner[(size_t)t]]]++] = (int32_t)t;
     h->h_roff = off;
+    h->h_rslots = slots;
     h->maxn = 0;
     for (int32_t r = 0; r < h->nranks; ++r) h->maxn = std::max(h->maxn, off[(size_t)r + 1] - off[(size_t)r]);
     h->d_roff.upload(off.data(), off.size(), h->stream);
@@ -917,35 +1010,70 @@ static void rebuild_shards(pcd_handle* h) {
   CK(cudaStreamSynchronize(h->stream));
 }
 
-// After a sweep on N>1 ranks: gather every rank's owned slots of `buf` (the
-// cache for the fused product sweeps, fresh[] for the replay sweep) and, for
-// the fused sweeps, reduce the per-rank convergence scalars.
-static void exchange(pcd_handle* h, int* buf, bool reduce) {
+// After a sweep on N>1 ranks: gather every rank's owned slots of `buf` inside
+// the window [lo, hi) (the cache for the fused run-partition / general
+// sweeps, fresh[] for the replay sweep) and, for the fused sweeps, reduce
+// the per-rank convergence scalars. Each rank's owned slots are one
+// time-ordered list, so its window slice is a contiguous range [a_r, a_r +
+// n_r); the all-gather ships max_r n_r int32 per rank (padded).
+static void exchange(pcd_handle* h, int* buf, bool reduce, int lo, int hi) {
   if (!h->comm) return;  // single GPU without a communicator
-  const int r = h->rank;
-  const int n = h->h_roff[(size_t)r + 1] - h->h_roff[(size_t)r];
-  k_pack_slots<<<grid_for(std::max(1, n), 256), 256, 0, h->stream>>>(buf, h->d_rslots.p + h->h_roff[(size_t)r], n,
-                                                                     h->d_send.p);
-  int rc = g_nccl.AllGather(h->d_send.p, h->d_recv.p, (size_t)h->maxn, ncclInt32, h->comm, h->stream);
-  if (rc) throw CudaError(std::string("ncclAllGather: ") + g_nccl.GetErrorString(rc));
-  k_unpack_slots<<<grid_for((long long)h->maxn * h->nranks, 256), 256, 0, h->stream>>>(
-      h->d_recv.p, h->d_rslots.p, h->d_roff.p, h->nranks, h->maxn, buf);
+  if (h->nranks > kMaxRanks) throw InvalidArgument("too many ranks");
+  RankWindow w{};
+  int maxw = 0;
+  for (int r = 0; r < h->nranks; ++r) {
+    const int32_t* b = h->h_rslots.data() + h->h_roff[(size_t)r];
+    const int32_t* e = h->h_rslots.data() + h->h_roff[(size_t)r + 1];
+    const int32_t* a0 = std::lower_bound(b, e, lo);
+    const int32_t* a1 = std::lower_bound(a0, e, hi);
+    w.start[r] = h->h_roff[(size_t)r] + (int)(a0 - b);
+    w.count[r] = (int)(a1 - a0);
+    maxw = std::max(maxw, w.count[r]);
+  }
+  if (maxw > 0) {
+    const int r = h->rank;
+    k_pack_slots<<<grid_for(std::max(1, w.count[r]), 256), 256, 0, h->stream>>>(buf, h->d_rslots.p + w.start[r],
+                                                                                w.count[r], h->d_send.p);
+    h->comm->all_gather(h->d_send.p, h->d_recv.p, (size_t)maxw, h->stream);
+    k_unpack_window<<<grid_for((long long)maxw * h->nranks, 256), 256, 0, h->stream>>>(h->d_recv.p, h->d_rslots.p, w,
+                                                                                      h->nranks, maxw, buf);
+  }
   if (reduce) {
     k_scalars_pack<<<1, 1, 0, h->stream>>>(h->scal, h->d_red.p);
-    rc = g_nccl.AllReduce(h->d_red.p, h->d_red.p, 4, ncclInt64, ncclSum, h->comm, h->stream);
-    if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 4, h->d_red.p + 4, 3, ncclUint64, ncclMin, h->comm, h->stream);
-    if (!rc) rc = g_nccl.AllReduce(h->d_red.p + 7, h->d_red.p + 7, 1, ncclUint64, ncclMax, h->comm, h->stream);
-    if (rc) throw CudaError(std::string("ncclAllReduce: ") + g_nccl.GetErrorString(rc));
+    h->comm->all_reduce(h->d_red.p, 4, RedOp::SumI64, h->stream);
+    h->comm->all_reduce(h->d_red.p + 4, 3, RedOp::MinU64, h->stream);
+    h->comm->all_reduce(h->d_red.p + 7, 1, RedOp::MaxU64, h->stream);
     k_scalars_unpack<<<1, 1, 0, h->stream>>>(h->d_red.p, h->scal);
   }
   CK(cudaGetLastError());
   h->timing.kernel_launches += reduce ? 4 : 2;
 }
 
+// Largest dual-network feature (policies.hpp:136-148): c / c0 and x / x0 with
+// the policy's normalisers (states never exceed the instance's initial one),
+// t / T with the policy's horizon; at least 1.
+static double feature_max(const pcd_instance* in, const int32_t* pcap, const int32_t* pinv, int64_t horizon,
+                          int J) {
+  double fmax = 1.0;
+  if (pcap != in->capacity)  // the instance's own normalisers give ratios <= 1
+    for (int j = 0; j < J; ++j)
+      if (pcap[j] > 0) fmax = std::max(fmax, (double)in->capacity[j] / pcap[j]);
+  if (pinv != in->inventory)
+    for (size_t i = 0; i < (size_t)in->products * J; ++i)
+      if (pinv[i] > 0) fmax = std::max(fmax, (double)in->inventory[i] / pinv[i]);
+  if (horizon > 0) {
+    double tmax = (double)std::max<int64_t>(in->horizon - 1, 0);
+    if (in->order_t)
+      for (int64_t t = 0; t < in->horizon; ++t) tmax = std::max(tmax, (double)in->order_t[t]);
+    fmax = std::max(fmax, tmax / (double)horizon);
+  }
+  return fmax;
+}
+
 // Rounding bound E between two FP64 evaluations of the dual network's scores
 // that differ only in summation order / FMA use (the reference's ordered
 // acc = b; acc += w*x vs the order-free recheck), for features in [0, 1]:
-//   layer 1: |dz1| <= 2 g(in+1) S1,                 S1 = max_n |b1| + sum|W1[n]|
+//   layer 1: |dz1| <= 2 g(in+1) S1,                 S1 = max_n |b1| + fmax sum|W1[n]|
 //   h1:      |dh1| <= |dz1| + 2u                    (tanh 1-Lipschitz, <= 1 ulp each)
 //   layer 2: |dz2| <= A2 |dh1| + 2 g(H+1) S2,       A2 = max_n sum|W2[n]|
 //   score:   |ds|  <= A3 |dh2| + 2 g(H+2) S3 + 4u (|r| + S3)
@@ -979,20 +1107,8 @@ static double tc_scaled_guard(const pcd_policy* pol, const pcd_instance* in, con
       !scan(pol->w3, (size_t)2 * J * H) || !scan(pol->b3, 2 * J))
     return 0.0;
   if (wmax > 3.0e4) return 0.0;
-  // largest feature: c / c0, x / x0 (states never exceed the instance's), t / T
-  double fmax = 1.0, rmax = 0.0;
-  if (pcap != in->capacity)  // the instance's own normalisers give ratios <= 1
-    for (int j = 0; j < J; ++j)
-      if (pcap[j] > 0) fmax = std::max(fmax, (double)in->capacity[j] / pcap[j]);
-  if (pinv != in->inventory)
-    for (size_t i = 0; i < (size_t)in->products * J; ++i)
-      if (pinv[i] > 0) fmax = std::max(fmax, (double)in->inventory[i] / pinv[i]);
-  if (horizon > 0) {
-    double tmax = (double)std::max<int64_t>(in->horizon - 1, 0);
-    if (in->order_t)
-      for (int64_t t = 0; t < in->horizon; ++t) tmax = std::max(tmax, (double)in->order_t[t]);
-    fmax = std::max(fmax, tmax / (double)horizon);
-  }
+  const double fmax = feature_max(in, pcap, pinv, horizon, J);
+  double rmax = 0.0;
   for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i) rmax = std::max(rmax, std::fabs(in->reward_table[i]));
   if (!(fmax <= 1.0e4) || !(rmax <= 1.0e6)) return 0.0;
   double Z1 = 0, A2 = 0, Z2 = 0, A3 = 0, Z3 = 0;
@@ -1018,15 +1134,15 @@ static double tc_scaled_guard(const pcd_policy* pol, const pcd_instance* in, con
   return guard <= 1e-2 ? guard : 0.0;
 }
 
-static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax) {
+static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax, double fmax) {
   const int in = 2 * J + 1, out = 2 * J;
   const double u = std::ldexp(1.0, -53);
   auto g = [&](double n) { return n * u / (1.0 - n * u); };
   double S1 = 0, A2 = 0, S2 = 0, A3 = 0, S3 = 0;
   for (int n = 0; n < H; ++n) {
-    double a = std::fabs(pol->b1[n]);
+    double a = 0;
     for (int c = 0; c < in; ++c) a += std::fabs(pol->w1[(size_t)n * in + c]);
-    S1 = std::max(S1, a);
+    S1 = std::max(S1, std::fabs(pol->b1[n]) + fmax * a);
     double b = 0;
     for (int c = 0; c < H; ++c) b += std::fabs(pol->w2[(size_t)n * H + c]);
     A2 = std::max(A2, b);
@@ -1052,20 +1168,17 @@ static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax
 static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap, const int32_t* pinv,
                        const double* rtab) {
   const int J = h->J, I = h->I, in = 2 * J + 1;
-  std::vector<unsigned char> img(kWImgBytes, 0), img2(kWImgBytes, 0);
+  std::vector<unsigned char> img2(kWImgBytes, 0);
   const int n3 = tc_pp_width_class(J);
   h->tc_n3 = n3;
-  // hi part at `base`, lo part at `base + part` (matches w1h/w1l/... in tc_sweep.cu)
-  auto put = [&](size_t base, size_t part, int R, int r, int k, double w) {
+  // per layer the hi rows 0..R-1 and lo rows R..2R-1 as one 2R-row K-major
+  // operand, so hi.hi and hi.lo are one N = 2R MMA (layer 3: R = the width
+  // class of J); the layers sit at the offsets of hi + lo images of widths
+  // kTcH / kTcH / kTcN3
+  auto put = [&](size_t base, int R, int r, int k, double w) {
     const float wf = (float)w;
     const __half hi = __float2half_rn(wf);
     const __half lo = __float2half_rn((wf - __half2float(hi)) * kLoScale);
-    const size_t off = (size_t)canon_off(R, r, k);
-    std::memcpy(&img[base + off], &hi, 2);
-    std::memcpy(&img[base + part + off], &lo, 2);
-    // ping-pong image: the layer's hi rows 0..R-1 and lo rows R..2R-1 as one
-    // 2R-row K-major operand, so hi.hi and hi.lo are one N = 2R MMA
-    // (layer 3: R2 = the width class of J instead of kTcN3)
     const int R2 = R == kTcN3 ? n3 : R;
     if (r < R2) {
       std::memcpy(&img2[base + (size_t)canon_off(2 * R2, r, k)], &hi, 2);
@@ -1074,35 +1187,28 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
   };
   const size_t w2base = 2 * (size_t)kW1Bytes, w3base = w2base + 2 * (size_t)kW2Bytes;
   for (int r = 0; r < kTcH; ++r)
-    for (int k = 0; k < kTcK1; ++k) put(0, kW1Bytes, kTcH, r, k, k < in ? pol->w1[(size_t)r * in + k] : 0.0);
+    for (int k = 0; k < kTcK1; ++k) put(0, kTcH, r, k, k < in ? pol->w1[(size_t)r * in + k] : 0.0);
   for (int r = 0; r < kTcH; ++r)
-    for (int k = 0; k < kTcH; ++k) put(w2base, kW2Bytes, kTcH, r, k, pol->w2[(size_t)r * kTcH + k]);
+    for (int k = 0; k < kTcH; ++k) put(w2base, kTcH, r, k, pol->w2[(size_t)r * kTcH + k]);
   for (int r = 0; r < kTcN3; ++r)
     for (int k = 0; k < kTcH; ++k)
-      put(w3base, kW3Bytes, kTcN3, r, k,
-          r < J ? pol->w3[(size_t)r * kTcH + k] + pol->w3[(size_t)(J + r) * kTcH + k] : 0.0);
-  std::vector<float> b1(kTcH), b2(kTcH), b3(kTcN3, 0.f), ic0(J);
+      put(w3base, kTcN3, r, k, r < J ? pol->w3[(size_t)r * kTcH + k] + pol->w3[(size_t)(J + r) * kTcH + k] : 0.0);
+  std::vector<float> b1(kTcH), b2(kTcH), ic0(J);
   for (int r = 0; r < kTcH; ++r) { b1[r] = (float)pol->b1[r]; b2[r] = (float)pol->b2[r]; }
-  for (int j = 0; j < J; ++j) b3[j] = (float)(pol->b3[j] + pol->b3[J + j]);
   for (int j = 0; j < J; ++j) ic0[j] = pcap[j] > 0 ? (float)(1.0 / pcap[j]) : 0.f;
-  h->tc_wimg.upload(img.data(), img.size(), h->stream);
   h->tc_wimg2.upload(img2.data(), img2.size(), h->stream);
   h->tc_b1.upload(b1.data(), b1.size(), h->stream);
   h->tc_b2.upload(b2.data(), b2.size(), h->stream);
-  h->tc_b3.upload(b3.data(), b3.size(), h->stream);
   h->tc_ic0.upload(ic0.data(), ic0.size(), h->stream);
   // 1/x0 of the policy's inventory normalisers, on the device (pinv0 is resident)
   h->tc_ix0.alloc(std::max<size_t>(1, (size_t)I * J));
   if ((size_t)I * J > 0)
     k_inv_f32<<<grid_for((long long)I * J, 256), 256, 0, h->stream>>>(h->pinv0.p, (long long)I * J, h->tc_ix0.p);
   CK(cudaGetLastError());
-  const int RJ = (J + 7) & ~7;  // 32-byte rows for the 256-bit loads of the score phase
-  std::vector<float> rtf((size_t)h->R * RJ, 0.f);
-  for (int64_t rr = 0; rr < h->R; ++rr)
-    for (int j = 0; j < J; ++j) rtf[(size_t)rr * RJ + j] = (float)rtab[(size_t)rr * J + j];
-  h->tc_rtf.upload(rtf.data(), rtf.size(), h->stream);
   // score = r - (q + b3) is computed as (r - b3) - q: one rounding of the
-  // FP64 difference instead of a bias add per node per step
+  // FP64 difference instead of a bias add per node per step; 32-byte rows for
+  // the 256-bit loads of the score phase
+  const int RJ = (J + 7) & ~7;
   std::vector<float> rtq((size_t)h->R * RJ, 0.f);
   for (int64_t rr = 0; rr < h->R; ++rr)
     for (int j = 0; j < J; ++j)
@@ -1176,7 +1282,11 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
       h->w3s.upload(w3s.data(), w3s.size(), s);
       double rmax = 0;
       for (int64_t i = 0; i < in->reward_rows * in->nodes; ++i) rmax = std::max(rmax, std::fabs(in->reward_table[i]));
-      h->fast_margin = fast_margin_bound(pol, Jn, H, rmax);
+      const int32_t* pc = pol->init_capacity ? pol->init_capacity : in->capacity;
+      const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
+                                             : in->inventory;
+      const int64_t ph = pol->horizon >= 0 ? pol->horizon : in->horizon;
+      h->fast_margin = fast_margin_bound(pol, Jn, H, rmax, feature_max(in, pc, pi, ph, Jn));
     }
     h->b1.upload(pol->b1, H, s);
     h->b2.upload(pol->b2, H, s);
@@ -1223,10 +1333,13 @@ extern "C" int pcd_set_plan(pcd_handle* h, const int32_t* owner, int32_t M) {
   // PartitionPlan::validate (engine.hpp:82-95)
   if (M < 1) throw ContractViolation("partition plan: process count must be >= 1");
   if (h->T > 0 && !owner) throw ContractViolation("partition plan does not cover the horizon");
-  h->owner.upload(owner, (size_t)h->T, h->stream);
-  {
-    const long long bad = first_out_of_range(h, h->owner.p, h->T, 0, M);
+  {  // validate into a scratch buffer: a rejected plan leaves the handle's plan intact
+    DBuf<int> nowner;
+    nowner.upload(owner, (size_t)h->T, h->stream);
+    const long long bad = first_out_of_range(h, nowner.p, h->T, 0, M);
     if (bad >= 0) throw ContractViolation("partition plan: owner out of range", bad);
+    h->have_plan = false;  // until the new plan's CSR / runs / shards are built
+    nowner.swap(h->owner);
   }
   h->M = M;
   build_csr(h, h->owner.p, M, h->pstart, h->pslots);
@@ -1521,7 +1634,7 @@ extern "C" int pcd_time_warp(pcd_handle* h, int32_t processes, uint64_t seed, in
                                                                    h->rid.p, h->ckinv.p, h->J, h->xloc.p);
     if (tc) launch_tc(h, lo32, hi32, nullptr, 0.0, 0);
     else dispatch_kind(h->kind, [&](auto k) { launch_product_sweep<decltype(k)::value>(h, lo32, hi32, nullptr); });
-    exchange(h, h->cache.p, true);
+    exchange(h, h->cache.p, true, lo32, hi32);
     read_scalars(h);
     throw_sweep_error(h);
     const int64_t max_evals = (int64_t)h->h_scal->max_evals, sum_evals = (int64_t)h->h_scal->total_evals;
@@ -1618,10 +1731,29 @@ extern "C" int pcd_depletion_profile(pcd_handle* h, const int32_t* actions, int6
   PCD_CATCH
 }
 
+extern "C" int pcd_checkpoint_state(pcd_handle* h, int32_t* capacity, int32_t* inventory) {
+  PCD_TRY
+  if (!h || !capacity || !inventory) throw InvalidArgument("null argument");
+  if (!h->ckcap.p) throw InvalidArgument("no simulation has run on this handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(capacity, h->ckcap.p, sizeof(int32_t) * (size_t)h->J, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(inventory, h->ckinv.p, sizeof(int32_t) * (size_t)h->I * h->J, cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return PCD_OK;
+  PCD_CATCH
+}
+
 extern "C" int pcd_set_history(pcd_handle* h, int32_t* history, int64_t cap_iterations) {
   if (!h) return PCD_INVALID_ARGUMENT;
   h->history = history;
   h->history_cap = history ? cap_iterations : 0;
+  return PCD_OK;
+}
+
+extern "C" int pcd_set_debug(pcd_handle* h, int32_t flags) {
+  if (!h) return PCD_INVALID_ARGUMENT;
+  h->debug = flags;
   return PCD_OK;
 }
 
@@ -1663,10 +1795,45 @@ extern "C" int pcd_attach_comm(pcd_handle* h, const unsigned char id[128], int32
   CK(cudaSetDevice(h->device));
   nccl_unique_id uid;
   std::memcpy(uid.internal, id, 128);
-  const int rc = g_nccl.CommInitRank(&h->comm, nranks, uid, rank);
+  auto c = std::make_unique<NcclComm>();
+  const int rc = g_nccl.CommInitRank(&c->c, nranks, uid, rank);
   if (rc != 0) throw CudaError(std::string("ncclCommInitRank failed: ") + g_nccl.GetErrorString(rc));
+  h->comm = std::move(c);
   h->rank = rank;
   h->nranks = nranks;
+  rebuild_shards(h);
+  return PCD_OK;
+  PCD_CATCH
+}
+
+// ------------------------------------------------ in-process loopback group
+struct pcd_loopback {
+  std::shared_ptr<pcd::LoopbackGroup> g;
+};
+
+extern "C" pcd_loopback* pcd_loopback_create(int32_t nranks) {
+  if (nranks < 1 || nranks > kMaxRanks) {
+    set_last_error("loopback group: nranks out of range");
+    return nullptr;
+  }
+  auto* l = new pcd_loopback;
+  l->g = std::make_shared<pcd::LoopbackGroup>(nranks);
+  return l;
+}
+
+extern "C" void pcd_loopback_destroy(pcd_loopback* l) { delete l; }
+
+extern "C" int pcd_attach_loopback(pcd_handle* h, pcd_loopback* l, int32_t rank) {
+  PCD_TRY
+  if (!h || !l) throw InvalidArgument("null argument");
+  if (rank < 0 || rank >= l->g->n) throw InvalidArgument("bad rank");
+  CK(cudaSetDevice(h->device));
+  auto c = std::make_unique<LoopbackComm>();
+  c->g = l->g;
+  c->rank = rank;
+  h->comm = std::move(c);
+  h->rank = rank;
+  h->nranks = l->g->n;
   rebuild_shards(h);
   return PCD_OK;
   PCD_CATCH

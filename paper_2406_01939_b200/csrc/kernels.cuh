@@ -24,9 +24,31 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "device_policy.cuh"
 
 namespace pcd {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: record the
+// largest size set for each (kernel, device) and raise it when a launch needs
+// more. Returns the CUDA status of the call (cudaSuccess when nothing to do).
+inline cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{kernel, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 constexpr int kLogK = 3;  // checkpoint stride K = 8 slots (partial block <= 7 events)
 constexpr int kK = 1 << kLogK;
@@ -810,12 +832,19 @@ static __global__ void k_pack_slots(const int* __restrict__ src, const int* __re
                                     int* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[slots[i]];
 }
-static __global__ void k_unpack_slots(const int* __restrict__ in, const int* __restrict__ slots,
-                                      const int* __restrict__ roff, int nranks, int maxn, int* __restrict__ dst) {
-  const long long total = (long long)nranks * maxn;
+// Window slices of every rank's owned-slot list (exchange): rank r's slots
+// d_rslots[start[r] .. start[r] + count[r]) arrive at recv[r * maxw ..).
+constexpr int kMaxRanks = 64;
+struct RankWindow {
+  int start[kMaxRanks];
+  int count[kMaxRanks];
+};
+static __global__ void k_unpack_window(const int* __restrict__ in, const int* __restrict__ slots, RankWindow w,
+                                       int nranks, int maxw, int* __restrict__ dst) {
+  const long long total = (long long)nranks * maxw;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(g / maxn), i = (int)(g % maxn);
-    if (i < roff[r + 1] - roff[r]) dst[slots[roff[r] + i]] = in[g];
+    const int r = (int)(g / maxw), i = (int)(g % maxw);
+    if (i < w.count[r]) dst[slots[w.start[r] + i]] = in[g];
   }
 }
 // Scalars <-> [sum: changed, conflicts, mismatch, total_evals | min: first,

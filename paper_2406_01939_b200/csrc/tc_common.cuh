@@ -1,11 +1,12 @@
-// tc_sweep.cuh — tcgen05/TMEM tensor-core sweep for product partitions.
+// tc_common.cuh — shared pieces of the tcgen05/TMEM tensor-core sweep
+// (tc_pp.cu) for run partitions: constants, weight-image layout, PTX glue.
 //
-// One CTA = a tile of 128 processes (MMA M=128, one TMEM lane per process).
-// Every step, each process evaluates the dual-price MLP (policies.hpp:121-168)
-// at its next own slot; the three layers run as tcgen05.mma.kind::f16 GEMMs
-//   z1 = F[128 x 208] . W1^T[208 x 64]       (features c/c0, x/x0, t/T)
-//   z2 = tanh(z1+b1)[128 x 64] . W2^T        (64 x 64)
-//   q  = tanh(z2+b2)[128 x 64] . W3'^T       (64 x 112),  W3' = W3[:J] + W3[J:]
+// Every step, each row (process) evaluates the dual-price MLP
+// (policies.hpp:121-168) at its next own slot; the three layers run as
+// tcgen05.mma.kind::f16 GEMMs over 64-row tiles
+//   z1 = F[64 x 208] . W1^T[208 x 64]        (features c/c0, x/x0, t/T)
+//   z2 = tanh(z1+b1)[64 x 64] . W2^T         (64 x 64)
+//   q  = tanh(z2+b2)[64 x 64] . W3'^T        (64 x N3), W3' = W3[:J] + W3[J:]
 // with operands split into fp16 hi + (scaled) lo parts and three products
 // (hi.hi + hi.lo + lo.hi) accumulated in fp32 TMEM (two accumulators so the
 // 2^-11-scaled cross terms keep full precision): ~2^-22 relative per product.
@@ -13,10 +14,9 @@
 //
 // Exactness: the tensor-core argmax is accepted only when its decision
 // margin (best - second best, and |best| vs the decline score 0) exceeds
-// `guard`; otherwise the row is re-evaluated by one warp with the exact FP64
-// path (warp_policy_eval<kDual>, bit-identical to the reference). The state of
-// each row is the product-partition closed form, identical to
-// k_sweep_product.
+// `guard`; otherwise the row is re-evaluated with the exact FP64 path
+// (bit-identical to the reference). The state of each row is the
+// run-partition closed form, identical to k_sweep_product.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -30,7 +30,6 @@ constexpr int kTcRows = 128;
 constexpr int kTcK1 = 208;     // 2J+1 <= 208 (J <= 103)
 constexpr int kTcH = 64;
 constexpr int kTcN3 = 112;     // J <= 112
-constexpr int kTcThreads = 256;
 constexpr float kLoScale = 2048.f;          // lo parts are stored * 2^11
 constexpr float kLoInv = 1.f / 2048.f;
 
@@ -40,7 +39,6 @@ constexpr int kW1Bytes = kTcH * kTcK1 * 2;   // one of hi / lo
 constexpr int kW2Bytes = kTcH * kTcH * 2;
 constexpr int kW3Bytes = kTcN3 * kTcH * 2;
 constexpr int kWImgBytes = 2 * (kW1Bytes + kW2Bytes + kW3Bytes);
-constexpr int kABytes = kTcRows * kTcK1 * 2;  // one of hi / lo
 
 __host__ __device__ constexpr int canon_off(int R, int r, int k) {
   return (k >> 3) * 16 * R + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
@@ -50,20 +48,16 @@ struct TcArgs {
   SweepArgs s;          // state, publish and counter pointers (as k_sweep_product)
   const int* wq;        // work list: processes with window slots, heaviest first
   int* wctl;            // {entries of wq, next entry beyond the dealt ones}
-  const unsigned char* wimg;  // kWImgBytes: W1hi W1lo W2hi W2lo W3hi W3lo
-  const unsigned char* wimg2; // kWImgBytes, ping-pong sweep: per layer one 2N-row operand [hi; lo]
-  int n3;                     // ping-pong sweep: layer-3 width class (tc_pp_width_class(J))
+  const unsigned char* wimg2; // kWImgBytes: per layer one 2N-row K-major operand [hi; lo]
+  int n3;                     // layer-3 width class (tc_pp_width_class(J))
   const float* b1f;     // [64]
   const float* b2f;     // [64]
-  const float* b3f;     // [112] b3[:J] + b3[J:]
   const float* inv_c0;  // [J]
   const float* inv_x0;  // [I*J]
-  const float* rtabf;   // [R*J] rewards in fp32 (scores of the tensor-core path)
-  const float* rtabq;   // [R*J] rewards minus the combined output bias b3f, in fp32 (ping-pong sweep)
+  const float* rtabq;   // [R*J] rewards minus the combined output bias b3[:J] + b3[J:], in fp32
   float guard;
   int verify;           // debug: exact re-evaluation of every row
   long long* prof;      // debug: per-phase clock64 totals of CTA 0 (or nullptr)
-  int pf;               // L2 prefetch of the next step's checkpoint row: 0 off, 1 step start, 2 step end
   unsigned long long* stats;  // [0] tc rows, [1] flagged, [2] flagged & tc wrong,
                               // [3] (verify) unflagged & tc wrong -- must stay 0
 };
@@ -121,16 +115,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
-               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
-}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -141,19 +125,9 @@ __device__ __forceinline__ float exp2f_approx(float x) {
 }
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256)
-__device__ __forceinline__ void ldg256(const void* p, uint32_t* r) {
-  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "l"(p));
-}
 
-// ... without allocating in L1 (streamed checkpoint rows / event blocks)
-__device__ __forceinline__ void ldg256_na(const void* p, uint32_t* r) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "l"(p));
-}
-// ... streamed through L2 with evict_first priority (read ~once per iteration;
+// 256-bit read-only loads (sm_100: LDG.E.ENL2.256) of streamed checkpoint
+// rows / event blocks, not allocated in L1 and streamed through L2 with evict_first priority (read ~once per iteration;
 // keeps the hot small tables — FP64 weights, run inventories — resident)
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t pol;
@@ -187,18 +161,5 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
   lo = __float2half_rn((x - __half2float(hi)) * kLoScale);
 }
 
-__device__ __forceinline__ float tanh_f32(float z) {
-  // 1 - 2/(1+e^{2z}): one MUFU op (ex2) and a reciprocal on the FMA pipe
-  // (bit-trick seed + 3 Newton steps, ~1e-8 relative), so the epilogue is not
-  // bound by the 16/clk/SM special-function unit; |err| ~1e-7 absolute, far
-  // below the decision guard (verify mode measures the end-to-end margin)
-  z = z > 9.f ? 9.f : (z < -9.f ? -9.f : z);  // NaN propagates (a non-finite score is flagged)
-  const float d = 1.f + exp2f_approx(2.8853900817779268f * z);  // 2 log2(e) z
-  float y = __int_as_float(0x7EF311C3 - __float_as_int(d));
-  y = y * fmaf(-d, y, 2.f);
-  y = y * fmaf(-d, y, 2.f);
-  y = y * fmaf(-d, y, 2.f);
-  return fmaf(-2.f, y, 1.f);
-}
 
 }  // namespace pcd

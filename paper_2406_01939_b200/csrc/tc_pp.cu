@@ -1,5 +1,5 @@
 // tc_pp.cu — the tcgen05 run-partition sweep, ping-pong form (see
-// tc_sweep.cuh for the MLP / precision / exactness scheme).
+// tc_common.cuh for the MLP / precision / exactness scheme).
 //
 // A CTA (one per SM, 16 warps) runs TWO independent 64-row pipelines
 // ("halves"). Half h owns warps 8h..8h+7, the TMEM lanes {32q + 16h + i :
@@ -28,7 +28,7 @@
 #include <climits>
 #include <cstdio>
 
-#include "tc_sweep.cuh"
+#include "tc_common.cuh"
 
 namespace pcd {
 namespace pp {
@@ -944,29 +944,24 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 }  // namespace pp
 
 template <bool PROF, int N3>
-static void launch_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+static cudaError_t launch_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
   constexpr int KS1 = (2 * N3 + 1 + 15) / 16 < kTcK1 / 16 ? (2 * N3 + 1 + 15) / 16 : kTcK1 / 16;
-  static bool attr = false;
   const size_t smem = pp::Layout::total;
-  if (!attr) {
-    cudaFuncSetAttribute(pp::k_sweep_pp<PROF, N3, KS1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  const cudaError_t e = ensure_dyn_smem((const void*)pp::k_sweep_pp<PROF, N3, KS1>, smem);
+  if (e != cudaSuccess) return e;
   pp::k_sweep_pp<PROF, N3, KS1><<<ntiles, pp::kBlock, smem, stream>>>(a);
+  return cudaGetLastError();
 }
 
 int tc_pp_width_class(int J) { return J <= 16 ? 16 : J <= 32 ? 32 : J <= 64 ? 64 : kTcN3; }
 
-void launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
-  if (a.prof) {
-    launch_pp<true, kTcN3>(a, ntiles, stream);  // (debug profiles: the C3 shape)
-    return;
-  }
+cudaError_t launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+  if (a.prof) return launch_pp<true, kTcN3>(a, ntiles, stream);  // (debug profiles: the C3 shape)
   switch (a.n3) {
-    case 16: launch_pp<false, 16>(a, ntiles, stream); break;
-    case 32: launch_pp<false, 32>(a, ntiles, stream); break;
-    case 64: launch_pp<false, 64>(a, ntiles, stream); break;
-    default: launch_pp<false, kTcN3>(a, ntiles, stream); break;
+    case 16: return launch_pp<false, 16>(a, ntiles, stream);
+    case 32: return launch_pp<false, 32>(a, ntiles, stream);
+    case 64: return launch_pp<false, 64>(a, ntiles, stream);
+    default: return launch_pp<false, kTcN3>(a, ntiles, stream);
   }
 }
 

@@ -15,6 +15,7 @@
 #include "picard/fo/instance.hpp"
 #include "picard/fo/policies.hpp"
 #include "picard/rng.hpp"
+#include "picard/theory.hpp"
 #include "picard_b200.hpp"
 
 using namespace picard;
@@ -233,6 +234,61 @@ int main() {
       cv = true;
     }
     CHECK(cv);
+  }
+  // the reference's full call shapes (engine.hpp:237-291, :358-365,
+  // :458-465; theory.hpp:120-126, :160-216, :258-268)
+  for (std::uint64_t seed = 900; seed < 912; ++seed) {
+    const auto inst = small_random(seed);
+    const auto env = inst.make_env();
+    const std::span<const Order> orders(inst.orders);
+    const auto plan = make_product_partition(inst, 3, seed);
+    PicardConfig cfg;
+    cfg.max_steps = seed % 3 == 0 ? 7 : 0;
+    // IterationObserver: per-iteration caches (CacheTraceRecorder) in order
+    theory::CacheTraceRecorder want_rec, got_rec;
+    const auto want = picard_simulate(env, GreedyPolicy{}, orders, plan, cfg, {}, {}, &want_rec);
+    const auto got = b200::picard_simulate(env, GreedyPolicy{}, orders, plan, cfg, {}, {}, &got_rec);
+    CHECK(got.actions == want.actions);
+    CHECK(got_rec.caches == want_rec.caches);
+    CHECK(got.trace.empty());  // the observer's trace rows are not returned unless record_trace
+    // evaluation_speedup_proxy on the drop-in's PicardResult
+    if (want.policy_eval_count_sequential_equivalent > 0)
+      CHECK(theory::evaluation_speedup_proxy(got, (std::int64_t)orders.size()) ==
+            theory::evaluation_speedup_proxy(want, (std::int64_t)orders.size()));
+    // SequentialObserver + sequential_simulate_with_states (states entering every t)
+    theory::CapacityRecorder want_caps, got_caps;
+    sequential_simulate(env, GreedyPolicy{}, orders, &want_caps);
+    b200::sequential_simulate(env, GreedyPolicy{}, orders, &got_caps);
+    CHECK(got_caps.capacities == want_caps.capacities);
+    const auto ws = sequential_simulate_with_states(env, GreedyPolicy{}, orders);
+    const auto gs = b200::sequential_simulate_with_states(env, GreedyPolicy{}, orders);
+    CHECK(gs.actions == ws.actions);
+    CHECK(gs.states.size() == ws.states.size());
+    for (std::size_t t = 0; t < std::min(gs.states.size(), ws.states.size()); ++t) {
+      CHECK(gs.states[t].capacity == ws.states[t].capacity);
+      CHECK(gs.states[t].inventory == ws.states[t].inventory);
+    }
+    // LocalStateObserver (theory::MonotonicityChecker, theory.hpp:216's call
+    // shape): refused with ContractViolation
+    theory::MonotonicityChecker checker(std::span<const FoState>(ws.states), inst.products, 1);
+    bool refused = false;
+    try {
+      b200::picard_simulate(env, GreedyPolicy{}, orders, plan, cfg, {}, {}, &checker);
+    } catch (const ContractViolation&) {
+      refused = true;
+    }
+    CHECK(refused);
+    // picard_iterate_once with IterateOptions / observer / iteration
+    ActionCache<FoAction> c1(orders.size(), kNoFulfill), c2(orders.size(), kNoFulfill);
+    IterateOptions io;
+    io.threads = 2;
+    const auto o1 = picard_iterate_once(env, GreedyPolicy{}, orders, plan, c1, 0, (std::int64_t)orders.size(),
+                                        env.initial_state(), io, static_cast<NoObserver*>(nullptr), 1);
+    const auto o2 = b200::picard_iterate_once(env, GreedyPolicy{}, orders, plan, c2, 0, (std::int64_t)orders.size(),
+                                              env.initial_state(), io, static_cast<NoObserver*>(nullptr), 1);
+    CHECK(c1 == c2);
+    CHECK(o1.changed_slots == o2.changed_slots);
+    CHECK(o1.evals_per_process == o2.evals_per_process);
   }
   std::printf("dropin_test: %d checks, %d failures\n", checks, failures);
   return failures;

@@ -259,17 +259,16 @@ def test_chunk_partition_iterate_once_random_caches_match_oracle(engine):
         assert out.changed_slots.tolist() == want_changed.tolist()
 
 
-@pytest.mark.parametrize("tiles", ["1", "3"])
-def test_tensor_core_work_list_pulls_match(tiles, monkeypatch):
+@pytest.mark.parametrize("tiles", [1, 3])
+def test_tensor_core_work_list_pulls_match(tiles):
     """Fewer CTAs than processes / 128: rows pull processes from the work list
     mid-iteration (per-process counters flushed at each switch)."""
     ons, inst, owner, opol, pol = _chunk_case(30, 100, 20000, 900, 2)
     seq, _ = ORC.sequential(ons, opol)
     ref = P.picard_simulate(inst, pol, P.PartitionPlan(900, owner),
                             P.PicardConfig(record_trace=True, engine="product_fp64"), reference_actions=seq)
-    monkeypatch.setenv("PCD_TC_TILES", tiles)
-    r = P.picard_simulate(inst, pol, P.PartitionPlan(900, owner), P.PicardConfig(record_trace=True, engine="product"),
-                          reference_actions=seq)
+    r = P.picard_simulate(inst, pol, P.PartitionPlan(900, owner),
+                          P.PicardConfig(record_trace=True, engine="product", tc_tiles=tiles), reference_actions=seq)
     assert r.timing["tc_used"] == 1
     assert r.actions.tolist() == seq.tolist()
     assert [x.astuple() for x in r.trace] == [x.astuple() for x in ref.trace]
@@ -391,12 +390,12 @@ def test_full_scale_c3_prefix_and_feasibility():
     assert int(ok.sum()) == int(inst.capacity.sum() - cap.sum())
 
 
-def test_c3_full_trajectory_chunk_vs_product_vs_fp64():
-    """The bench workload itself (C3: J=100, I=1e4, T=1e7): the product-chunk
-    plan on the tensor-core engine, the reference's product plan, and the
-    FP64 SIMT engine all reach the same trajectory (the serial one, Prop. 1);
-    its first 1e5 orders equal the serial oracle; chunks change the plan's
-    counters but not the 66 iterations at this shape."""
+def test_c3_chunk_and_product_plans_agree():
+    """The bench workload (C3: J=100, I=1e4, T=1e7): the product-chunk plan and
+    the reference's product plan (both on the tensor-core engine, whole-horizon
+    window) reach the same trajectory in the same 66 iterations; the
+    reference pin of that trajectory (all 1e7 actions, reward, final state,
+    verify mode, FP64 engine) is tests/test_gpu_fullscale.py."""
     J, I, T = 100, 10_000, 10_000_000
     inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
     pol = P.DualNetworkPolicy.seeded(inst, 5)
@@ -405,15 +404,7 @@ def test_c3_full_trajectory_chunk_vs_product_vs_fp64():
     prod = P.picard_simulate(inst, pol, P.make_product_partition(inst, 65536, 1), cfg)
     assert np.array_equal(chunk.actions, prod.actions)
     assert chunk.iterations_to_converged == prod.iterations_to_converged == 66
-    assert chunk.timing["tc_unflagged_bad"] == 0 and chunk.timing["tc_used"] == 1
-    n = 100_000
-    ons = NS(nodes=J, products=I, horizon=n, product=inst.product[:n], order_t=None,
-             reward_row=inst.reward_row[:n], reward_table=inst.reward_table.ravel(),
-             capacity=inst.capacity, inventory=inst.inventory.ravel())
-    opol = NS(kind=2, hidden=64, gamma=0.0, horizon=T, w1=pol.w1, b1=pol.b1, w2=pol.w2, b2=pol.b2,
-              w3=pol.w3, b3=pol.b3)
-    seq_prefix, _ = ORC.sequential(ons, opol)
-    assert chunk.actions[:n].tolist() == seq_prefix.tolist()
+    assert chunk.timing["tc_used"] == 1 and prod.timing["tc_used"] == 1
 
 
 @pytest.mark.parametrize("J,I,T,M", [(10, 300, 20000, 512), (30, 200, 12000, 256), (100, 40, 4000, 64),

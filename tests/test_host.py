@@ -189,3 +189,26 @@ def test_device_entry_points_fail_loudly_without_gpu():
 def test_dual_policy_rejects_wrong_widths():
     with pytest.raises(P.ContractViolation):
         P.DualNetworkPolicy(P.MlpParams.zeros(7, 5), nodes=3)
+
+
+def test_c3_instance_and_policy_equal_the_reference_generator():
+    """The bench workload's inputs (C3 with the J>30 synthetic geometry) are
+    bit-identical to the compiled reference's generate_instance /
+    MlpParams::seeded_uniform (instance.cpp:80-140, mlp.cpp:117-129)."""
+    import numpy as np
+    import pytest
+    from oracle.oracle import REF
+    if REF is None:
+        pytest.skip("oracle/_ref not built")
+    import paper_2406_01939_b200 as P
+    J, I, T = 100, 10_000, 10_000_000
+    ref = REF.generate_instance_arrays(J, I, T, 0.0, 0.8, 7, geometry=1)
+    inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
+    assert np.array_equal(inst.product, ref["product"])
+    assert np.array_equal(inst.reward_row, ref["reward_row"])
+    assert np.array_equal(inst.reward_table.ravel(), ref["reward_table"])
+    assert np.array_equal(inst.capacity, ref["capacity"])
+    assert np.array_equal(inst.inventory.ravel(), ref["inventory"])
+    pol = P.DualNetworkPolicy.seeded(inst, 5)
+    for a, b in zip((pol.w1, pol.b1, pol.w2, pol.b2, pol.w3, pol.b3), REF.seeded_mlp(2 * J + 1, 2 * J, 5)):
+        assert np.array_equal(a, b)

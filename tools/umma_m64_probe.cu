@@ -2,7 +2,7 @@
 // lane offsets 0 and 16, and the 16x32bx2 load mapping.
 #include <cstdio>
 #include <cuda_fp16.h>
-#include "../paper_2406_01939_b200/csrc/tc_sweep.cuh"
+#include "../paper_2406_01939_b200/csrc/tc_common.cuh"
 using namespace pcd;
 
 __global__ void probe(float* out, float* out2) {
