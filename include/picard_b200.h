@@ -129,6 +129,9 @@ typedef struct pcd_config {
                               unflagged disagreements (pcd_timing.tc_unflagged_bad) */
   int32_t tc_tiles;        /* CTAs of the tensor-core sweep; 0 = one per SM (tests
                               use fewer, so rows pull processes mid-iteration) */
+  int32_t tc_kernel;       /* tensor-core sweep: 0 = auto (incremental layer 1 when
+                              it applies), 1 = fused layer 1 (tc_pp), 2 = incremental
+                              layer 1 (tc_inc; error when it does not apply)        */
 } pcd_config;
 
 /* PicardTraceRow (engine.hpp:128-134). */
@@ -173,6 +176,8 @@ typedef struct pcd_timing {
   int64_t tc_unflagged_bad; /* tc_verify only: unflagged rows that were wrong (must be 0) */
   int32_t tc_used;        /* the sweep ran on tensor cores */
   int32_t tc_tiles;       /* CTAs (128 processes each) */
+  int32_t tc_kernel;      /* sweep kernel of the last tensor-core iteration: 1 fused, 2 incremental */
+  int32_t tc_inc_iters;   /* iterations that ran the incremental-layer-1 sweep */
 } pcd_timing;
 
 typedef struct pcd_handle pcd_handle;
@@ -361,8 +366,11 @@ int pcd_sequential(pcd_handle* h, int32_t* actions_out, int64_t* policy_evals);
 int pcd_last_timing(const pcd_handle* h, pcd_timing* out);
 
 /* Debug flags of a handle (not for production runs). */
-enum { PCD_DEBUG_TC_PROFILE = 1 /* per-phase clock64 totals of the tensor-core
-                                   sweep's CTA 0, printed to stderr per launch */ };
+enum { PCD_DEBUG_TC_PROFILE = 1, /* per-phase clock64 totals of the tensor-core
+                                    sweep's CTA 0, printed to stderr per launch */
+       PCD_DEBUG_TC_FUSED = 2,    /* entry points without a pcd_config (pcd_iterate_once,
+                                    pcd_sequential) use the fused-layer-1 sweep ... */
+       PCD_DEBUG_TC_INC = 4 };    /* ... or the incremental-layer-1 sweep (tests) */
 int pcd_set_debug(pcd_handle* h, int32_t flags);
 
 /* The device checkpoint FoState (capacity[J], dense inventory[I*J]): the

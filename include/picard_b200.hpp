@@ -238,7 +238,7 @@ PicardResult<fo::FoAction> picard_simulate(const fo::FoEnv& env, const P& policy
   const bool observe = wants_iterations && observer != nullptr;
   const bool trace_on = config.record_trace || observe;  // the callbacks need (chunk, lo) per iteration
   const pcd_config cfg{config.processes, trace_on ? 1 : 0, config.max_steps, config.max_iterations,
-                       config.threads, PCD_ENGINE_AUTO, 0.0, 0, 0};
+                       config.threads, PCD_ENGINE_AUTO, 0.0, 0, 0, 0};
   const auto init = detail::nodes_of(initial_cache);
   const auto ref = detail::nodes_of(reference_actions);
   std::vector<std::int32_t> actions(static_cast<std::size_t>(T));

@@ -54,7 +54,8 @@ class pcd_policy(C.Structure):
 class pcd_config(C.Structure):
     _fields_ = [("processes", C.c_int32), ("record_trace", C.c_int32), ("max_steps", C.c_int64),
                 ("max_iterations", C.c_int64), ("threads", C.c_int32), ("engine", C.c_int32),
-                ("tc_guard", C.c_double), ("tc_verify", C.c_int32), ("tc_tiles", C.c_int32)]
+                ("tc_guard", C.c_double), ("tc_verify", C.c_int32), ("tc_tiles", C.c_int32),
+                ("tc_kernel", C.c_int32)]
 
 
 class pcd_trace_row(C.Structure):
@@ -76,7 +77,8 @@ class pcd_timing(C.Structure):
                 ("steps_critical", C.c_int64), ("total_evals", C.c_int64),
                 ("engine_used", C.c_int32), ("device", C.c_int32), ("tc_rows", C.c_int64),
                 ("tc_flagged", C.c_int64), ("tc_disagree", C.c_int64), ("tc_unflagged_bad", C.c_int64),
-                ("tc_used", C.c_int32), ("tc_tiles", C.c_int32)]
+                ("tc_used", C.c_int32), ("tc_tiles", C.c_int32),
+                ("tc_kernel", C.c_int32), ("tc_inc_iters", C.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/picard_b200.h

@@ -45,6 +45,7 @@ LIB = K.LIB
 NO_FULFILL = -1
 ENGINES = {"auto": K.PCD_ENGINE_AUTO, "replay": K.PCD_ENGINE_REPLAY, "product": K.PCD_ENGINE_PRODUCT,
            "product_fp64": K.PCD_ENGINE_PRODUCT_FP64, "general": K.PCD_ENGINE_GENERAL}
+TC_KERNELS = {"auto": 0, "fused": 1, "incremental": 2}
 
 
 # ------------------------------------------------------------------ errors
@@ -390,11 +391,13 @@ class PicardConfig:
     tc_guard: float = 0.0
     tc_verify: bool = False
     tc_tiles: int = 0
+    tc_kernel: str = "auto"  # tensor-core sweep: "auto" / "fused" (tc_pp) / "incremental" (tc_inc)
 
     def to_c(self):
         return K.pcd_config(int(self.processes), 1 if self.record_trace else 0, int(self.max_steps),
                             int(self.max_iterations), int(self.threads), ENGINES[self.engine],
-                            float(self.tc_guard), 1 if self.tc_verify else 0, int(self.tc_tiles))
+                            float(self.tc_guard), 1 if self.tc_verify else 0, int(self.tc_tiles),
+                            TC_KERNELS[self.tc_kernel])
 
 
 @dataclass
@@ -546,9 +549,14 @@ class Simulator:
         _check(LIB.pcd_download_actions(self._h, _ptr(a)))
         return a[:int(self.instance.horizon)]
 
+    def set_debug(self, flags: int):
+        """pcd_set_debug: PCD_DEBUG_* flags (profiling, the sweep kernel of config-less calls)."""
+        _check(LIB.pcd_set_debug(self._h, int(flags)))
+
     def iterate_once(self, cache: np.ndarray, t_lo: int, t_hi: int, checkpoint_capacity=None,
-                     checkpoint_inventory=None, engine: str = "auto") -> IterationOutcome:
+                     checkpoint_inventory=None, engine: str = "auto", tc_kernel: str = "auto") -> IterationOutcome:
         eng = ENGINES[engine]
+        self.set_debug({"auto": 0, "fused": 2, "incremental": 4}[tc_kernel])
         assert cache.dtype == np.int32 and cache.flags.c_contiguous
         M = self.plan.processes
         evals = np.zeros(M, np.int64)
@@ -633,11 +641,11 @@ def picard_simulate(instance: Instance, policy: Policy, plan: PartitionPlan,
 
 def picard_iterate_once(instance: Instance, policy: Policy, plan: PartitionPlan, cache: np.ndarray,
                         t_lo: int, t_hi: int, checkpoint_capacity=None, checkpoint_inventory=None,
-                        engine: str = "auto", device: int = 0) -> IterationOutcome:
+                        engine: str = "auto", device: int = 0, tc_kernel: str = "auto") -> IterationOutcome:
     """picard_iterate_once (engine.hpp:358-444); ``cache`` is updated in place."""
     with Simulator(instance, policy, device) as sim:
         sim.set_plan(plan)
-        return sim.iterate_once(cache, t_lo, t_hi, checkpoint_capacity, checkpoint_inventory, engine)
+        return sim.iterate_once(cache, t_lo, t_hi, checkpoint_capacity, checkpoint_inventory, engine, tc_kernel)
 
 
 def sequential_simulate(instance: Instance, policy: Policy, device: int = 0) -> SequentialOutput:

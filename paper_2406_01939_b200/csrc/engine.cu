@@ -33,6 +33,8 @@
 namespace pcd {
 
 cudaError_t launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream);  // tc_pp.cu (two 64-row halves)
+cudaError_t launch_tc_inc(const IncArgs& a, const CUtensorMap& gmap, int ntiles, cudaStream_t stream);  // tc_inc.cu
+cudaError_t launch_inc_prep(const IncPrep& p, cudaStream_t stream);  // tc_inc.cu: G rows + node transitions
 int tc_pp_width_class(int J);  // tc_pp.cu: layer-3 width class of the ping-pong sweep for J nodes
 size_t tc_smem_bytes();
 
@@ -325,6 +327,14 @@ struct pcd_handle {
   pcd::DBuf<unsigned long long> tc_stats;
   int32_t tc_tiles = 0;
   int64_t max_load = 0;
+  // incremental-layer-1 sweep (tc_inc.cu): layer-1 tables, per-iteration G rows
+  bool inc_ok = false;                   // dual policy, J <= kIncMaxJ (prepare_tc)
+  int32_t tc_kernel_req = 0;             // pcd_config::tc_kernel of the running simulate
+  pcd::DBuf<float> inc_af, inc_wx, inc_wt, grow;
+  pcd::DBuf<double> inc_a64, inc_b1;
+  pcd::DBuf<int> inc_bA, inc_bD;
+  CUtensorMap gmap{};                    // TMA map over grow ([rows][64] fp32, one-row boxes)
+  size_t gmap_rows = 0;
   // multi-GPU
   int32_t rank = 0, nranks = 1;
   std::unique_ptr<pcd::Comm> comm;  // NCCL, or a loopback group (tests)
@@ -516,6 +526,38 @@ static void throw_sweep_error(pcd_handle* h) {
   throw ContractViolation("policy returned an infeasible action at t=" + std::to_string(t), t);
 }
 
+// AUTO's choice between the two tensor-core sweeps when the incremental one applies
+constexpr bool kIncDefault = false;
+
+// G-row buffer of the incremental sweep and its TMA map (2-D: 64 fp32 per
+// row, one-row boxes), grown to the window's block count.
+static void ensure_gmap(pcd_handle* h, size_t rows) {
+  rows = std::max<size_t>(rows, 1);
+  if (h->gmap_rows >= rows) return;
+  const size_t cap = std::max(rows, h->gmap_rows * 2);
+  h->grow.alloc(cap * kTcH);
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    encode = (EncodeFn)fn;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)kTcH, (cuuint64_t)cap};
+  const cuuint64_t strides[1] = {(cuuint64_t)kTcH * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)kTcH, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&h->gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, h->grow.p, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  h->gmap_rows = cap;
+}
+
 // One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
 static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify,
                       int tiles_req = 0) {
@@ -557,17 +599,60 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   // PCD_DEBUG_TC_PROFILE: per-phase clock64 totals of CTA 0, printed to stderr
   const bool prof = (h->debug & PCD_DEBUG_TC_PROFILE) != 0;
   if (prof) {
-    h->tc_prof.alloc(20);
-    CK(cudaMemsetAsync(h->tc_prof.p, 0, 20 * sizeof(long long), h->stream));
+    h->tc_prof.alloc(20 + 2 * 4096);  // phase totals + per-step (active rows, cycles) of CTA 0 half 0
+    CK(cudaMemsetAsync(h->tc_prof.p, 0, (20 + 2 * 4096) * sizeof(long long), h->stream));
     a.prof = h->tc_prof.p;
   }
   // tiles < SMs (tests): rows pull processes from the work list mid-iteration
   const int tiles = tiles_req > 0 ? std::min(h->tc_tiles, tiles_req) : h->tc_tiles;
-  CK(launch_tc_pp(a, tiles, h->stream));
+  // the incremental-layer-1 sweep needs the frozen-cache prefix counts (not
+  // Time Warp's nocache windows), J <= kIncMaxJ and |D| within int16
+  const int req = h->tc_kernel_req ? h->tc_kernel_req
+                  : (h->debug & PCD_DEBUG_TC_FUSED) ? 1 : (h->debug & PCD_DEBUG_TC_INC) ? 2 : 0;
+  const bool inc_fits = h->inc_ok && !h->nocache && std::min<int64_t>(h->max_load, (int64_t)hi - lo) < 32000;
+  if (req == 2 && !inc_fits)
+    throw InvalidArgument("tc_kernel=incremental does not apply (Time Warp window, J > 104 or window load >= 32000)");
+  if (inc_fits && req != 1 && (req == 2 || kIncDefault)) {
+    const int nb = hck_rows(lo, hi);
+    ensure_gmap(h, (size_t)nb);
+    IncPrep pr{};
+    pr.hck = h->hck.p; pr.ev = h->ev.p; pr.tau = h->tau.p; pr.ckcap = h->ckcap.p;
+    pr.a64 = h->inc_a64.p; pr.b1 = h->inc_b1.p; pr.wload_sorted = h->wload_s.p;
+    pr.lo = lo; pr.hi = hi; pr.J = h->J; pr.nb = nb;
+    pr.grow = h->grow.p; pr.bA = h->inc_bA.p; pr.bD = h->inc_bD.p;
+    CK(launch_inc_prep(pr, h->stream));
+    IncArgs x{};
+    x.t = a;
+    x.af = h->inc_af.p; x.wx = h->inc_wx.p; x.wt = h->inc_wt.p;
+    x.tau = h->tau.p; x.bA = h->inc_bA.p; x.bD = h->inc_bD.p;
+    CK(launch_tc_inc(x, h->gmap, tiles, h->stream));
+    h->timing.kernel_launches += 2;
+    h->timing.tc_kernel = 2;
+    h->timing.tc_inc_iters += 1;
+  } else {
+    CK(launch_tc_pp(a, tiles, h->stream));
+    h->timing.tc_kernel = 1;
+  }
   if (prof) {
     long long v[20];
     CK(cudaMemcpyAsync(v, h->tc_prof.p, sizeof v, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (h->timing.tc_kernel == 2) {
+      std::vector<long long> tr(2 * 4096);
+      CK(cudaMemcpy(tr.data(), h->tc_prof.p + 20, tr.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      const int edges[6] = {1, 3, 9, 17, 33, 65};
+      long long cyc[5] = {0, 0, 0, 0, 0}, cnt[5] = {0, 0, 0, 0, 0};
+      for (int k = 0; k < 4096 && tr[2 * k]; ++k)
+        for (int e = 0; e < 5; ++e)
+          if (tr[2 * k] >= edges[e] && tr[2 * k] < edges[e + 1]) { cyc[e] += tr[2 * k + 1]; cnt[e] += 1; }
+      fprintf(stderr, "incsteps active[1-2]=%lld@%lld [3-8]=%lld@%lld [9-16]=%lld@%lld [17-32]=%lld@%lld [33-64]=%lld@%lld (steps@cycles/step)\n",
+              cnt[0], cnt[0] ? cyc[0] / cnt[0] : 0, cnt[1], cnt[1] ? cyc[1] / cnt[1] : 0, cnt[2], cnt[2] ? cyc[2] / cnt[2] : 0,
+              cnt[3], cnt[3] ? cyc[3] / cnt[3] : 0, cnt[4], cnt[4] ? cyc[4] / cnt[4] : 0);
+    }
+    if (h->timing.tc_kernel == 2)
+      fprintf(stderr, "incprof steps=%lld exact_nodes=%lld pre=%lld dirty=%lld part/near=%lld zB1=%lld L2=%lld E2=%lld L3=%lld S=%lld UB4=%lld chk=%lld\n",
+              v[10], v[14], v[11], v[12], v[13], v[0], v[1], v[2], v[3], v[4], v[5], v[6]);
+    else
     fprintf(stderr, "tcprof steps=%lld F=%lld(own %lld) L1=%lld E1=%lld L2=%lld E2=%lld L3=%lld S=%lld fin=%lld chk=%lld U=%lld\n",
             v[10], v[0], v[11], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
     fprintf(stderr, "tcprof F: loads=%lld feat=%lld x=%lld | recheck feat=%lld L1=%lld L2=%lld L3=%lld score=%lld\n",
@@ -795,7 +880,7 @@ static void ensure_state_buffers(pcd_handle* h) {
   h->cache.alloc(T);
   h->fresh.alloc(T);
   h->ev.alloc(T + kK);  // + kK: the sweep reads whole K-slot blocks
-  h->written.alloc(T);
+  h->written.alloc(T + 4);  // + 4: the incremental sweep copies whole 4-byte words
   h->ckcap.alloc(std::max(1, h->J));
   h->ckinv.alloc(IJ);
   h->ckbak.alloc(IJ + h->J);
@@ -818,6 +903,8 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   if (cfg->max_steps < 0 || cfg->max_iterations < 0)
     throw ContractViolation("picard config values must be non-negative");
   const int engine = choose_engine(h, cfg->engine);
+  if (cfg->tc_kernel < 0 || cfg->tc_kernel > 2) throw InvalidArgument("tc_kernel must be 0, 1 or 2");
+  h->tc_kernel_req = cfg->tc_kernel;
   h->timing = pcd_timing{};
   h->timing.engine_used = engine;
   h->timing.device = h->device;
@@ -1201,7 +1288,7 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
   h->tc_b2.upload(b2.data(), b2.size(), h->stream);
   h->tc_ic0.upload(ic0.data(), ic0.size(), h->stream);
   // 1/x0 of the policy's inventory normalisers, on the device (pinv0 is resident)
-  h->tc_ix0.alloc(std::max<size_t>(1, (size_t)I * J));
+  h->tc_ix0.alloc((size_t)I * J + 4);  // + 4: the incremental sweep copies aligned 16-byte chunks
   if ((size_t)I * J > 0)
     k_inv_f32<<<grid_for((long long)I * J, 256), 256, 0, h->stream>>>(h->pinv0.p, (long long)I * J, h->tc_ix0.p);
   CK(cudaGetLastError());
@@ -1215,6 +1302,31 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
       rtq[(size_t)rr * RJ + j] = (float)(rtab[(size_t)rr * J + j] - (pol->b3[j] + pol->b3[J + j]));
   h->tc_rtq.upload(rtq.data(), rtq.size(), h->stream);
   h->tc_stats.alloc(4);
+  // incremental sweep (tc_inc.cu): A_j = W1[:, j] / c0_j (FP64 for the G rows,
+  // fp32 for the per-row updates), W1[:, J + j], W1[:, 2J], b1
+  h->inc_ok = J <= kIncMaxJ && h->H == kTcH;
+  if (h->inc_ok) {
+    std::vector<double> a64((size_t)J * kTcH), b1d(kTcH);
+    std::vector<float> af((size_t)J * kTcH), wx((size_t)J * kTcH), wt(kTcH);
+    for (int j = 0; j < J; ++j)
+      for (int u = 0; u < kTcH; ++u) {
+        const double w = pol->w1[(size_t)u * in + j];
+        a64[(size_t)j * kTcH + u] = pcap[j] > 0 ? w / (double)pcap[j] : 0.0;
+        af[(size_t)j * kTcH + u] = (float)a64[(size_t)j * kTcH + u];
+        wx[(size_t)j * kTcH + u] = (float)pol->w1[(size_t)u * in + J + j];
+      }
+    for (int u = 0; u < kTcH; ++u) {
+      wt[u] = (float)pol->w1[(size_t)u * in + 2 * J];
+      b1d[u] = pol->b1[u];
+    }
+    h->inc_a64.upload(a64.data(), a64.size(), h->stream);
+    h->inc_b1.upload(b1d.data(), b1d.size(), h->stream);
+    h->inc_af.upload(af.data(), af.size(), h->stream);
+    h->inc_wx.upload(wx.data(), wx.size(), h->stream);
+    h->inc_wt.upload(wt.data(), wt.size(), h->stream);
+    h->inc_bA.alloc(J);
+    h->inc_bD.alloc(J);
+  }
   CK(cudaStreamSynchronize(h->stream));
   h->tc_ok = true;
 }
@@ -1503,6 +1615,7 @@ extern "C" int pcd_iterate_once(pcd_handle* h, int32_t engine, int32_t* cache, i
   DBuf<int> saved_ref;  // iterate_once has no reference
   std::swap(saved_ref.p, h->ref.p);
   std::swap(saved_ref.n, h->ref.n);
+  h->tc_kernel_req = 0;
   try {
     run_iteration(h, eng, t_lo, t_hi, h->evals.p);
   } catch (...) {

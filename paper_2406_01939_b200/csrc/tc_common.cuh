@@ -19,6 +19,7 @@
 // run-partition closed form, identical to k_sweep_product.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
 
@@ -62,6 +63,31 @@ struct TcArgs {
                               // [3] (verify) unflagged & tc wrong -- must stay 0
 };
 
+// tc_inc.cu: the sweep with layer 1 off the tensor cores (nodes J <= kIncMaxJ)
+constexpr int kIncMaxJ = 104;
+struct IncArgs {
+  TcArgs t;           // everything the ping-pong sweep takes (its layer-2/3 weight image is reused)
+  const float* af;    // [J][64] A_j = W1[:, j] / c0_j (capacity weights over the normaliser)
+  const float* wx;    // [J][64] W1[:, J + j] (inventory weights)
+  const float* wt;    // [64]    W1[:, 2J] (time weight)
+  const int* tau;     // [J] death slot of every node under the frozen cache (k_tau)
+  const int* bA;      // [J] first block at which node j is no longer alive-far (k_trans)
+  const int* bD;      // [J] first block at which node j is dead-far (k_trans)
+};
+struct IncPrep {      // per-iteration G rows and node transition blocks
+  const int* hck;
+  const int* ev;
+  const int* tau;
+  const int* ckcap;
+  const double* a64;  // [J][64] A_j in FP64
+  const double* b1;   // [64]
+  const int* wload_sorted;  // [0] = the largest window load of this rank's processes
+  int lo, hi, J, nb;
+  float* grow;        // [nb][64]
+  int* bA;
+  int* bD;
+};
+
 // ---------------------------------------------------------------- PTX glue
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -78,6 +104,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity));
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// TMA: arm an mbarrier for `bytes` of transaction, then a 2-D tensor tile
+// (cp.async.bulk.tensor, SASS UTMALDG) or a plain bulk copy (UBLKCP) that
+// completes on it
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// 4-byte async global -> shared copy (LDGSTS), completed by this thread's wait
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// named barrier over `count` threads that also returns how many of them passed pred
+__device__ __forceinline__ int bar_red_popc(int id, int count, bool pred) {
+  int r;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\tbarrier.red.popc.u32 %0, %1, %2, p;\n\t}"
+               : "=r"(r)
+               : "r"(id), "r"(count), "r"((int)pred)
+               : "memory");
+  return r;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 

@@ -62,12 +62,14 @@ def c3():
     return NS(ref=ref, inst=inst, pol=pol, seq=seq, cap=cap, inv=inv, reward=reward, plan=plan)
 
 
-@pytest.mark.parametrize("window,engine", [(C3_WINDOW, "auto"), (300 * 65536, "auto"),
-                                           (300 * 65536, "product_fp64")])
-def test_c3_full_trajectory_equals_reference_serial(c3, window, engine):
+@pytest.mark.parametrize("window,engine,kernel", [(C3_WINDOW, "auto", "fused"), (C3_WINDOW, "auto", "incremental"),
+                                                  (300 * 65536, "auto", "fused"),
+                                                  (300 * 65536, "auto", "incremental"),
+                                                  (300 * 65536, "product_fp64", "auto")])
+def test_c3_full_trajectory_equals_reference_serial(c3, window, engine, kernel):
     with P.Simulator(c3.inst, c3.pol) as sim:
         sim.set_plan(c3.plan)
-        r = sim.simulate(P.PicardConfig(max_steps=window, engine=engine))
+        r = sim.simulate(P.PicardConfig(max_steps=window, engine=engine, tc_kernel=kernel))
         cap, inv = sim.checkpoint_state()
     assert r.timing["tc_used"] == (1 if engine == "auto" else 0)
     first = np.flatnonzero(r.actions != c3.seq)
@@ -76,24 +78,25 @@ def test_c3_full_trajectory_equals_reference_serial(c3, window, engine):
     assert np.array_equal(inv.ravel(), c3.inv)
     got = P.fo_total_reward(c3.inst, r.actions)
     rel = abs(got - c3.reward) / max(1.0, abs(c3.reward))
-    print(f"\nC3 window={window} engine={engine}: {r.iterations_to_converged} iterations, "
+    print(f"\nC3 window={window} engine={engine} kernel={kernel}: {r.iterations_to_converged} iterations, "
           f"total reward {got!r} vs reference {c3.reward!r} (rel. diff {rel:.3e})")
     assert rel <= 1e-4
 
 
-@pytest.mark.parametrize("window", [C3_WINDOW, 300 * 65536])
-def test_c3_verify_mode_every_row_rechecked(c3, window):
+@pytest.mark.parametrize("window,kernel", [(C3_WINDOW, "fused"), (C3_WINDOW, "incremental"),
+                                           (300 * 65536, "fused")])
+def test_c3_verify_mode_every_row_rechecked(c3, window, kernel):
     """tc_verify: every tensor-core row is also evaluated in exact FP64; no row
     outside the guard may disagree (tc_unflagged_bad == 0) and the trajectory
     is the reference's."""
     with P.Simulator(c3.inst, c3.pol) as sim:
         sim.set_plan(c3.plan)
-        r = sim.simulate(P.PicardConfig(max_steps=window, tc_verify=True))
+        r = sim.simulate(P.PicardConfig(max_steps=window, tc_verify=True, tc_kernel=kernel))
     t = r.timing
     assert t["tc_used"] == 1 and t["tc_rows"] > 3e7
     assert t["tc_unflagged_bad"] == 0
     assert np.array_equal(r.actions, c3.seq)
-    print(f"\nverify window={window}: {t['tc_rows']} rows, {t['tc_flagged']} flagged, "
+    print(f"\nverify window={window} kernel={kernel}: {t['tc_rows']} rows, {t['tc_flagged']} flagged, "
           f"{t['tc_disagree']} flagged rows where fp16x3 was wrong, 0 unflagged wrong")
 
 
