@@ -268,6 +268,49 @@ int pcd_linear_convergence_curve(const pcd_linear_spec* spec, const double* init
                                  int32_t device, double* curve, int64_t curve_cap, int64_t* curve_len,
                                  double* final_cache, double* elapsed_ms);
 
+/* MLP feedback policy on the linear env (BASELINE config 4):
+ * a_t = MlpParams::forward(s_t) (mlp.cpp:141-169) with widths
+ * {state_dim, hidden, hidden, input_dim}: tanh hidden layers, linear output,
+ * row-major as MlpParams: w1[hidden][n], b1[hidden], w2[hidden][hidden],
+ * b2[hidden], w3[p][hidden], b3[p]. The reference pairs the linear env only
+ * with GainPolicy (linear.hpp:104-126); this policy plugs the reference's own
+ * MLP into the same env and engine (PolicyFor, engine.hpp:57-61). */
+typedef struct pcd_linear_mlp {
+  int32_t hidden;               /* <= 64 */
+  int32_t pad;
+  const double* w1;
+  const double* b1;
+  const double* w2;
+  const double* b2;
+  const double* w3;
+  const double* b3;
+} pcd_linear_mlp;
+
+typedef struct pcd_linear_mlp_result {
+  int64_t curve_len;               /* iterations of the curve (as pcd_linear_convergence_curve) */
+  int64_t iterations_to_converged; /* picard_simulate's count for the single-step plan (M = T,
+                                      whole-horizon window): the first iteration that changes no
+                                      action under LinearEnv::actions_equal (linear.hpp:64-71) */
+  int64_t fixed_point_iterations;  /* iterations of the pass that computes the sequential
+                                      trajectory as the Picard fixed point (Prop. 1) */
+  double fixed_point_ms;           /* device time of that pass */
+  double curve_ms;                 /* device time of the curve pass */
+} pcd_linear_mlp_result;
+
+/* picard_convergence_curve (linear.cpp:267-318) with the MLP feedback policy:
+ * single-step partitions, one affine time-scan rollout plus one batched FP64
+ * MLP evaluation of all T states per iteration. The closed loop is no longer
+ * affine, so the sequential reference trajectory is computed first as the
+ * Picard fixed point (iterated until the cache stops changing beyond 2^-46
+ * relative), then the curve is scored against it. Arguments as
+ * pcd_linear_convergence_curve; reference_states[T+1][n] (optional) receives
+ * the sequential trajectory. */
+int pcd_linear_mlp_convergence_curve(const pcd_linear_spec* spec, const pcd_linear_mlp* policy,
+                                     const double* initial_cache, double tolerance, int64_t max_iterations,
+                                     int32_t normalization, int32_t device, double* curve, int64_t curve_cap,
+                                     pcd_linear_mlp_result* result, double* final_cache,
+                                     double* reference_states);
+
 /* Page-locked host buffers from a process-wide pool (no reference
  * counterpart): result arrays allocated here are written by the device at
  * full PCIe bandwidth and recycled by pcd_host_free instead of being pinned

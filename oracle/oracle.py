@@ -382,6 +382,43 @@ class _Lib:
                                                 _p(states, C.c_double)))
         return acts[:T], states
 
+    # MLP feedback policy on the linear env (ref_linear_mlp_* in ref_harness.cpp:
+    # the reference's MlpParams::forward as a PolicyFor<LinearEnv>)
+    def _lin_mlp_args(self, spec, mlp):
+        n, p, T = spec.state_dim, spec.input_dim, spec.horizon
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (spec.dynamics, spec.input, spec.disturbances)]
+        ws = [np.ascontiguousarray(a, np.float64) for a in (mlp.w1, mlp.b1, mlp.w2, mlp.b2, mlp.w3, mlp.b3)]
+        self._lin_keep = arrs + ws
+        return ([C.c_int32(n), C.c_int32(p), C.c_int64(T)] + [_p(a, C.c_double) for a in arrs]
+                + [C.c_int32(int(mlp.widths[1]))] + [_p(a, C.c_double) for a in ws])
+
+    def linear_mlp_curve(self, spec, mlp, initial_cache=None, tolerance=1e-3, max_iterations=0,
+                         normalization="draft"):
+        T = spec.horizon
+        init = None if initial_cache is None else np.ascontiguousarray(initial_cache, np.float64)
+        cap = max(max_iterations if max_iterations > 0 else T, 1)
+        curve = np.zeros(cap); ln = C.c_int64()
+        self.check(self.fn("linear_mlp_curve")(*self._lin_mlp_args(spec, mlp), _p(init, C.c_double),
+                                               C.c_double(tolerance), C.c_int64(max_iterations),
+                                               C.c_int32(1 if normalization == "draft" else 0),
+                                               _p(curve, C.c_double), C.c_int64(cap), C.byref(ln)))
+        return curve[:ln.value].copy()
+
+    def linear_mlp_sequential(self, spec, mlp):
+        n, p, T = spec.state_dim, spec.input_dim, spec.horizon
+        acts = np.zeros((max(T, 1), p)); states = np.zeros((T + 1, n))
+        self.check(self.fn("linear_mlp_sequential")(*self._lin_mlp_args(spec, mlp), _p(acts, C.c_double),
+                                                    _p(states, C.c_double)))
+        return acts[:T], states
+
+    def linear_mlp_picard(self, spec, mlp, initial_cache=None, threads=1):
+        p, T = spec.input_dim, spec.horizon
+        init = None if initial_cache is None else np.ascontiguousarray(initial_cache, np.float64)
+        acts = np.zeros((max(T, 1), p)); it = C.c_int64()
+        self.check(self.fn("linear_mlp_picard")(*self._lin_mlp_args(spec, mlp), _p(init, C.c_double),
+                                                C.c_int32(threads), C.byref(it), _p(acts, C.c_double)))
+        return it.value, acts[:T]
+
     def total_reward(self, inst, actions):
         ci, k1 = self._inst(inst)
         a = np.ascontiguousarray(actions, np.int32)

@@ -716,4 +716,133 @@ int ref_linear_sequential(int32_t n, int32_t p, int64_t T, const double* A, cons
   });
 }
 
+
+// ---------------------------------------------------------------- linear env, MLP feedback
+// The reference's MlpParams (mlp.cpp:141-169) as a PolicyFor<LinearEnv>
+// (engine.hpp:57-61): a_t = forward(s_t). Test-only policy for BASELINE
+// config 4 ("non-SCO env with MLP policy"); everything else is the unmodified
+// reference (LinearEnv, make_steps, rollout_states, relative_rmse and the engine).
+struct MlpFeedbackPolicy {
+  static constexpr EvalCost cost_class = EvalCost::expensive;
+  const MlpParams* mlp;
+  std::vector<double> evaluate(const std::vector<double>& s, const linear::LinearStep&) const {
+    std::vector<double> a(static_cast<std::size_t>(mlp->widths[3]));
+    mlp->forward(s, a);
+    return a;
+  }
+};
+static_assert(PolicyFor<MlpFeedbackPolicy, linear::LinearEnv>);
+
+static MlpParams make_lin_mlp(int32_t n, int32_t p, int32_t H, const double* w1, const double* b1,
+                              const double* w2, const double* b2, const double* w3, const double* b3) {
+  MlpParams m;
+  m.widths = {n, H, H, p};
+  m.w1.assign(w1, w1 + (size_t)H * n);
+  m.b1.assign(b1, b1 + H);
+  m.w2.assign(w2, w2 + (size_t)H * H);
+  m.b2.assign(b2, b2 + H);
+  m.w3.assign(w3, w3 + (size_t)p * H);
+  m.b3.assign(b3, b3 + p);
+  return m;
+}
+
+// picard_convergence_curve (linear.cpp:267-318) with MlpFeedbackPolicy in
+// place of GainPolicy: the same statements, the policy type swapped.
+int ref_linear_mlp_curve(int32_t n, int32_t p, int64_t T, const double* A, const double* B, const double* w,
+                         int32_t H, const double* w1, const double* b1, const double* w2, const double* b2,
+                         const double* w3, const double* b3, const double* init, double tolerance,
+                         int64_t max_iterations, int32_t normalization, double* curve, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    std::vector<double> G((size_t)p * n, 0.0);
+    const auto spec = make_linear(n, p, T, A, B, w, G.data());
+    const auto mlp = make_lin_mlp(n, p, H, w1, b1, w2, b2, w3, b3);
+    linear::LinearEnv env(spec);
+    MlpFeedbackPolicy policy{&mlp};
+    const auto steps = linear::make_steps(spec);
+    const std::int64_t horizon = spec.horizon;
+    PartitionPlan plan;
+    plan.processes = static_cast<std::int32_t>(std::max<std::int64_t>(1, horizon));
+    plan.owner.resize(static_cast<std::size_t>(horizon));
+    for (std::int64_t t = 0; t < horizon; ++t) plan.owner[(size_t)t] = static_cast<std::int32_t>(t);
+    ActionCache<std::vector<double>> cache;
+    if (init) {
+      for (int64_t t = 0; t < T; ++t) cache.emplace_back(init + (size_t)t * p, init + (size_t)(t + 1) * p);
+    } else {
+      cache.assign(static_cast<std::size_t>(horizon), env.null_action());
+    }
+    const auto reference = sequential_simulate_with_states(env, policy, std::span<const linear::LinearStep>(steps));
+    const auto draft = linear::rollout_states(spec, cache);
+    auto score = [&](const std::vector<std::vector<double>>& states) {
+      const std::span<const std::vector<double>> cand(states.begin() + 1, states.end());
+      const std::span<const std::vector<double>> ref(reference.states.begin() + 1, reference.states.end());
+      if (normalization) {
+        const std::span<const std::vector<double>> base(draft.begin() + 1, draft.end());
+        return linear::relative_rmse(cand, ref, base);
+      }
+      return linear::relative_rmse(cand, ref);
+    };
+    const std::int64_t capit = max_iterations > 0 ? max_iterations : horizon;
+    const auto checkpoint = env.initial_state();
+    std::vector<double> c;
+    for (std::int64_t k = 1; k <= capit; ++k) {
+      picard_iterate_once(env, policy, std::span<const linear::LinearStep>(steps), plan, cache, 0, horizon,
+                          checkpoint);
+      c.push_back(score(linear::rollout_states(spec, cache)));
+      if (c.back() <= tolerance) break;
+    }
+    *len = (int64_t)c.size();
+    for (size_t k = 0; k < c.size() && (int64_t)k < cap; ++k) curve[k] = c[k];
+    return 0;
+  });
+}
+
+// sequential_simulate_with_states of (LinearEnv, MlpFeedbackPolicy): actions[T][p], states[T+1][n]
+int ref_linear_mlp_sequential(int32_t n, int32_t p, int64_t T, const double* A, const double* B, const double* w,
+                              int32_t H, const double* w1, const double* b1, const double* w2, const double* b2,
+                              const double* w3, const double* b3, double* actions, double* states) {
+  return guarded([&] {
+    std::vector<double> G((size_t)p * n, 0.0);
+    const auto spec = make_linear(n, p, T, A, B, w, G.data());
+    const auto mlp = make_lin_mlp(n, p, H, w1, b1, w2, b2, w3, b3);
+    linear::LinearEnv env(spec);
+    MlpFeedbackPolicy pol{&mlp};
+    const auto steps = linear::make_steps(spec);
+    const auto r = sequential_simulate_with_states(env, pol, std::span<const linear::LinearStep>(steps));
+    for (int64_t t = 0; t < T; ++t) std::memcpy(actions + (size_t)t * p, r.actions[(size_t)t].data(), sizeof(double) * p);
+    for (int64_t t = 0; t <= T; ++t) std::memcpy(states + (size_t)t * n, r.states[(size_t)t].data(), sizeof(double) * n);
+    return 0;
+  });
+}
+
+// picard_simulate (engine.hpp:458-590) of (LinearEnv, MlpFeedbackPolicy) with
+// the single-step plan (M = T) and the whole horizon as window:
+// iterations_to_converged and the converged actions[T][p]
+int ref_linear_mlp_picard(int32_t n, int32_t p, int64_t T, const double* A, const double* B, const double* w,
+                          int32_t H, const double* w1, const double* b1, const double* w2, const double* b2,
+                          const double* w3, const double* b3, const double* init, int32_t threads,
+                          int64_t* iterations, double* actions) {
+  return guarded([&] {
+    std::vector<double> G((size_t)p * n, 0.0);
+    const auto spec = make_linear(n, p, T, A, B, w, G.data());
+    const auto mlp = make_lin_mlp(n, p, H, w1, b1, w2, b2, w3, b3);
+    linear::LinearEnv env(spec);
+    MlpFeedbackPolicy pol{&mlp};
+    const auto steps = linear::make_steps(spec);
+    PartitionPlan plan;
+    plan.processes = static_cast<std::int32_t>(std::max<std::int64_t>(1, T));
+    plan.owner.resize(static_cast<std::size_t>(T));
+    for (std::int64_t t = 0; t < T; ++t) plan.owner[(size_t)t] = static_cast<std::int32_t>(t);
+    std::vector<std::vector<double>> ic;
+    if (init)
+      for (int64_t t = 0; t < T; ++t) ic.emplace_back(init + (size_t)t * p, init + (size_t)(t + 1) * p);
+    PicardConfig cfg;
+    cfg.threads = threads;
+    const auto r = picard_simulate(env, pol, std::span<const linear::LinearStep>(steps), plan, cfg,
+                                   std::span<const std::vector<double>>(ic));
+    *iterations = r.iterations_to_converged;
+    for (int64_t t = 0; t < T; ++t) std::memcpy(actions + (size_t)t * p, r.actions[(size_t)t].data(), sizeof(double) * p);
+    return 0;
+  });
+}
+
 }  // extern "C"

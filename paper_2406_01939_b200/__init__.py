@@ -6,7 +6,7 @@ sm_100a kernels behind the C ABI in ``include/picard_b200.h``; this package is
 the Python mirror of the reference interface (see :mod:`.api`).
 """
 from .api import (  # noqa: F401
-    NO_FULFILL, CapacityPenalizedPolicy, LinearCurve, LinearSystemSpec, make_contractive_spec,
+    NO_FULFILL, CapacityPenalizedPolicy, LinearCurve, MlpFeedbackPolicy, LinearSystemSpec, make_contractive_spec,
     picard_convergence_curve, TimeWarpResult, time_warp_simulate, DepletionProfile, depletion_profile,
     check_iteration_bound, save_instance_binary, load_instance_binary, ContractViolation, CudaError, DualNetworkPolicy, GreedyPolicy,
     Instance, InvalidArgument, IterationLimitError, IterationOutcome, MlpParams, NullOnlyPolicy,

@@ -27,6 +27,16 @@ class pcd_linear_spec(C.Structure):
                 ("dynamics", F64P), ("input", F64P), ("disturbances", F64P), ("gain", F64P)]
 
 
+class pcd_linear_mlp(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("pad", C.c_int32), ("w1", F64P), ("b1", F64P), ("w2", F64P),
+                ("b2", F64P), ("w3", F64P), ("b3", F64P)]
+
+
+class pcd_linear_mlp_result(C.Structure):
+    _fields_ = [("curve_len", C.c_int64), ("iterations_to_converged", C.c_int64),
+                ("fixed_point_iterations", C.c_int64), ("fixed_point_ms", C.c_double), ("curve_ms", C.c_double)]
+
+
 class pcd_tw_result(C.Structure):
     _fields_ = [("sync_rounds", C.c_int64), ("rollbacks", C.c_int64),
                 ("policy_eval_count_sequential_equivalent", C.c_int64), ("total_policy_evals", C.c_int64),
@@ -95,6 +105,9 @@ SIGNATURES = {
     "pcd_linear_convergence_curve": (C.c_int, [C.POINTER(pcd_linear_spec), F64P, C.c_double, C.c_int64, C.c_int32,
                                                 C.c_int32, F64P, C.c_int64, C.POINTER(C.c_int64), F64P,
                                                 C.POINTER(C.c_double)]),
+    "pcd_linear_mlp_convergence_curve": (C.c_int, [C.POINTER(pcd_linear_spec), C.POINTER(pcd_linear_mlp), F64P,
+                                                    C.c_double, C.c_int64, C.c_int32, C.c_int32, F64P, C.c_int64,
+                                                    C.POINTER(pcd_linear_mlp_result), F64P, F64P]),
     "pcd_time_warp": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32, I32P,
                                  C.POINTER(pcd_tw_result), C.POINTER(pcd_tw_trace_row), C.c_int64]),
     "pcd_depletion_profile": (C.c_int, [C.c_void_p, I32P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -12,6 +12,7 @@ fo::make_product_partition (:142-186)  :func:`make_product_partition`
 make_uniform_time_partition (engine.hpp:99-114) :func:`make_uniform_time_partition`
 linear::make_contractive_spec (linear.cpp:126) :func:`make_contractive_spec`
 linear::picard_convergence_curve (linear.cpp:279) :func:`picard_convergence_curve`
+(ours: MLP policy on the linear env)   :class:`MlpFeedbackPolicy`
 PartitionPlan (engine.hpp:74-96)       :class:`PartitionPlan`
 PicardConfig (engine.hpp:120-126)      :class:`PicardConfig`
 PicardResult / PicardTraceRow          :class:`PicardResult` / :class:`PicardTraceRow`
@@ -727,14 +728,55 @@ class LinearCurve:
     curve: np.ndarray          # relative RMSE after each iteration
     final_cache: np.ndarray    # [T, p] actions after the last iteration
     device_ms: float
+    # MLP feedback policy only (None for GainPolicy): picard_simulate's
+    # iteration count for the single-step plan, the iterations and device time
+    # of the fixed-point pass, and the sequential trajectory [T+1, n]
+    iterations_to_converged: Optional[int] = None
+    fixed_point_iterations: Optional[int] = None
+    fixed_point_ms: Optional[float] = None
+    reference_states: Optional[np.ndarray] = None
+
+
+@dataclass
+class MlpFeedbackPolicy:
+    """a_t = MlpParams::forward(s_t) (mlp.cpp:141-169) on the linear env: the
+    reference's own MLP ({n, H, H, p}, tanh hidden layers, linear output) as a
+    PolicyFor<LinearEnv> (engine.hpp:57-61). The reference pairs the linear env
+    only with GainPolicy (linear.hpp:104-126); BASELINE config 4 asks for an
+    MLP policy."""
+    params: MlpParams
+
+    @staticmethod
+    def seeded(state_dim: int, input_dim: int, seed: int, hidden: int = 64, output_scale: float = 1.0):
+        """MlpParams::seeded_uniform(n, p, seed, hidden) (mlp.cpp:117-129), the
+        output layer (w3, b3) multiplied by ``output_scale`` (sets the policy's
+        Lipschitz constant, hence the closed-loop contraction)."""
+        m = MlpParams.seeded_uniform(state_dim, input_dim, seed, hidden)
+        m.w3 = m.w3 * float(output_scale)
+        m.b3 = m.b3 * float(output_scale)
+        return MlpFeedbackPolicy(m)
+
+    def to_c(self, state_dim: int, input_dim: int):
+        m = self.params
+        n, H, H2, p = (int(x) for x in m.widths)
+        if n != state_dim or p != input_dim or H != H2:
+            raise InvalidArgument("mlp widths must be {state_dim, hidden, hidden, input_dim}")
+        self._keep = [np.ascontiguousarray(a, np.float64).reshape(-1) for a in (m.w1, m.b1, m.w2, m.b2, m.w3, m.b3)]
+        want = (H * n, H, H * H, H, p * H, p)
+        if any(k.size != w for k, w in zip(self._keep, want)):
+            raise InvalidArgument("mlp parameter sizes disagree with the widths")
+        return K.pcd_linear_mlp(H, 0, *[_ptr(k, C.c_double) for k in self._keep])
 
 
 def picard_convergence_curve(spec: LinearSystemSpec, initial_cache=None, tolerance: float = 1e-3,
                              max_iterations: int = 0, normalization: str = "draft",
-                             device: int = 0) -> LinearCurve:
+                             device: int = 0, policy: Optional[MlpFeedbackPolicy] = None) -> LinearCurve:
     """linear::picard_convergence_curve (linear.cpp:279-330) on the B200:
-    single-step partitions (M = T), one affine time-scan per iteration."""
-    T, p = int(spec.horizon), int(spec.input_dim)
+    single-step partitions (M = T), one affine time-scan per iteration.
+    ``policy=None`` is the reference's GainPolicy a = G s; an
+    :class:`MlpFeedbackPolicy` evaluates the MLP at all T states per iteration
+    (pcd_linear_mlp_convergence_curve)."""
+    T, p, n = int(spec.horizon), int(spec.input_dim), int(spec.state_dim)
     cs = spec.to_c()
     init = None if initial_cache is None else np.ascontiguousarray(initial_cache, np.float64).reshape(-1)
     if init is not None and init.size != T * p:
@@ -742,10 +784,22 @@ def picard_convergence_curve(spec: LinearSystemSpec, initial_cache=None, toleran
     cap = max(int(max_iterations) if max_iterations > 0 else T, 1)
     curve = np.zeros(cap)
     fin = np.zeros(max(T * p, 1))
+    norm = 1 if normalization == "draft" else 0
+    if policy is not None:
+        cm = policy.to_c(n, p)
+        res = K.pcd_linear_mlp_result()
+        ref = np.zeros((T + 1) * n)
+        _check(LIB.pcd_linear_mlp_convergence_curve(C.byref(cs), C.byref(cm), _ptr(init, C.c_double),
+                                                    float(tolerance), int(max_iterations), norm, int(device),
+                                                    _ptr(curve, C.c_double), cap, C.byref(res),
+                                                    _ptr(fin, C.c_double), _ptr(ref, C.c_double)))
+        return LinearCurve(curve[:res.curve_len].copy(), fin[:T * p].reshape(T, p),
+                           res.fixed_point_ms + res.curve_ms, res.iterations_to_converged,
+                           res.fixed_point_iterations, res.fixed_point_ms, ref.reshape(T + 1, n))
     n_out = C.c_int64()
     ms = C.c_double()
     _check(LIB.pcd_linear_convergence_curve(C.byref(cs), _ptr(init, C.c_double), float(tolerance),
-                                            int(max_iterations), 1 if normalization == "draft" else 0,
+                                            int(max_iterations), norm,
                                             int(device), _ptr(curve, C.c_double), cap, C.byref(n_out),
                                             _ptr(fin, C.c_double), C.byref(ms)))
     return LinearCurve(curve[:n_out.value].copy(), fin[:T * p].reshape(T, p), ms.value)

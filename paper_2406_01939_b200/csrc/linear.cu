@@ -23,10 +23,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
 #include "capi_internal.h"
+#include "device_policy.cuh"
 
 namespace pcd {
 namespace lin {
@@ -317,6 +319,244 @@ static void curve_impl(const pcd_linear_spec* sp, const double* init, double tol
   LCK(cudaStreamSynchronize(s));
 }
 
+
+// ---------------------------------------------------------------------------
+// MLP feedback policy (BASELINE config 4): a_t = forward(s_t)
+// with the reference's MlpParams (mlp.cpp:141-169) in place of GainPolicy.
+constexpr int kMlpMaxH = 64;
+constexpr int kMlpMaxP = 16;
+constexpr int kMlpBlock = 128;
+
+static int host_tanh_fma_lin() {
+#if defined(__x86_64__)
+  __builtin_cpu_init();
+  return (__builtin_cpu_supports("fma") && __builtin_cpu_supports("avx2")) ? 1 : 0;
+#else
+  return 1;
+#endif
+}
+
+// Every state's action, one thread per state, in MlpParams::forward's exact
+// operation order (acc = b; acc += w * x with explicit round-to-nearest
+// multiply and add, glibc tanh restated): each action is bit-identical to the
+// reference's forward() of the same state. The weights sit in shared memory
+// (w1 | b1 | w2 | b2 | w3 | b3, MlpParams layout), the first hidden layer in
+// a [unit][thread] shared array; the second layer is streamed unit by unit
+// into the output accumulators, which keeps layer 3's order (c ascending).
+template <int N>
+__global__ void __launch_bounds__(kMlpBlock) k_mlp_policy(const double* __restrict__ Wg, int H, int P, int tfma,
+                                                          const double* __restrict__ states, long long T,
+                                                          double* __restrict__ a) {
+  extern __shared__ __align__(16) double lsm[];
+  const int nw = H * N + H + H * H + H + P * H + P;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) lsm[i] = Wg[i];
+  __syncthreads();
+  const double *w1 = lsm, *b1 = w1 + H * N, *w2 = b1 + H, *b2 = w2 + H * H, *w3 = b2 + H, *b3 = w3 + P * H;
+  double* h1 = lsm + nw + threadIdx.x;  // h1[c] at h1[c * kMlpBlock]
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+    double x[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) x[c] = states[(size_t)t * N + c];
+    for (int r = 0; r < H; ++r) {
+      double acc = b1[r];
+#pragma unroll
+      for (int c = 0; c < N; ++c) acc = __dadd_rn(acc, __dmul_rn(w1[r * N + c], x[c]));
+      h1[r * kMlpBlock] = gt_tanh(acc, tfma);
+    }
+    double out[kMlpMaxP];
+#pragma unroll
+    for (int k = 0; k < kMlpMaxP; ++k) out[k] = k < P ? b3[k] : 0.0;
+    for (int r = 0; r < H; ++r) {
+      double acc = b2[r];
+      const double* row = w2 + r * H;
+      for (int c = 0; c < H; ++c) acc = __dadd_rn(acc, __dmul_rn(row[c], h1[c * kMlpBlock]));
+      const double h2 = gt_tanh(acc, tfma);
+#pragma unroll
+      for (int k = 0; k < kMlpMaxP; ++k)
+        if (k < P) out[k] = __dadd_rn(out[k], __dmul_rn(w3[k * H + r], h2));
+    }
+#pragma unroll
+    for (int k = 0; k < kMlpMaxP; ++k)
+      if (k < P) a[(size_t)t * P + k] = out[k];
+  }
+}
+
+// LinearEnv::actions_equal (linear.hpp:64-71) over the whole cache: out[0] +=
+// slots that differ beyond 1e-9 relative, out[1] = max relative change (as
+// ordered bits of a non-negative double)
+__global__ void k_action_change(const double* __restrict__ x, const double* __restrict__ y, int P, long long T,
+                                unsigned long long* out) {
+  __shared__ unsigned long long sc[8], sm[8];
+  unsigned long long cnt = 0, mx = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+    bool diff = false;
+    for (int k = 0; k < P; ++k) {
+      const double u = x[(size_t)t * P + k], v = y[(size_t)t * P + k];
+      const double scale = fmax(1.0, fmax(fabs(u), fabs(v)));
+      const double d = fabs(u - v);
+      diff |= d > 1e-9 * scale;
+      const double rel = d / scale;
+      const unsigned long long b = (unsigned long long)__double_as_longlong(rel == rel ? rel : INFINITY);
+      mx = b > mx ? b : mx;
+    }
+    cnt += diff ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = m2 > mx ? m2 : mx;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sc[w] = cnt; sm[w] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c2 = 0, m3 = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { c2 += sc[i]; m3 = sm[i] > m3 ? sm[i] : m3; }
+    if (c2) atomicAdd(out, c2);
+    atomicMax(out + 1, m3);
+  }
+}
+
+template <int N>
+static void mlp_curve_impl(const pcd_linear_spec* sp, const pcd_linear_mlp* pol, const double* init, double tol,
+                           int64_t max_it, int norm, double* curve, int64_t cap, pcd_linear_mlp_result* res,
+                           double* final_cache, double* ref_states) {
+  const int P = sp->input_dim, H = pol->hidden;
+  const long long T = sp->horizon;
+  cudaStream_t s;
+  LCK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{s};
+  const size_t TN = (size_t)T * N, TP = (size_t)T * P;
+  Buf A(TN * N), B(TN * P), w(TN), c(TN), c0(std::max<size_t>(TP, 1)), ca(std::max<size_t>(TP, 1)),
+      cb(std::max<size_t>(TP, 1)), ref(TN + N), draft(TN + N), st(TN + N);
+  Runner<N> R(P, T, s);
+  Buf M((size_t)R.nchunks * N * N + 1), v((size_t)R.nchunks * N + 1), S((size_t)R.nchunks * N + 1),
+      part((size_t)R.grid + 1), out(1);
+  // weights, MlpParams layout
+  const size_t nw = (size_t)H * N + H + (size_t)H * H + H + (size_t)P * H + P;
+  std::vector<double> hw;
+  hw.reserve(nw);
+  hw.insert(hw.end(), pol->w1, pol->w1 + (size_t)H * N);
+  hw.insert(hw.end(), pol->b1, pol->b1 + H);
+  hw.insert(hw.end(), pol->w2, pol->w2 + (size_t)H * H);
+  hw.insert(hw.end(), pol->b2, pol->b2 + H);
+  hw.insert(hw.end(), pol->w3, pol->w3 + (size_t)P * H);
+  hw.insert(hw.end(), pol->b3, pol->b3 + P);
+  Buf W(nw);
+  unsigned long long* chg = nullptr;
+  LCK(cudaMalloc(&chg, 2 * sizeof(unsigned long long)));
+  struct ChgGuard {
+    unsigned long long* p;
+    ~ChgGuard() { cudaFree(p); }
+  } cg{chg};
+  bool zeroA = true;
+  for (size_t i = 0; i < TN * N && zeroA; ++i) zeroA = sp->dynamics[i] == 0.0;
+  LCK(cudaMemcpyAsync(A.p, sp->dynamics, TN * N * 8, cudaMemcpyHostToDevice, s));
+  LCK(cudaMemcpyAsync(B.p, sp->input, TN * P * 8, cudaMemcpyHostToDevice, s));
+  LCK(cudaMemcpyAsync(w.p, sp->disturbances, TN * 8, cudaMemcpyHostToDevice, s));
+  LCK(cudaMemcpyAsync(W.p, hw.data(), nw * 8, cudaMemcpyHostToDevice, s));
+  if (init) LCK(cudaMemcpyAsync(c0.p, init, TP * 8, cudaMemcpyHostToDevice, s));
+  else if (TP) LCK(cudaMemsetAsync(c0.p, 0, TP * 8, s));
+  const size_t smem = (nw + (size_t)kMlpMaxH * kMlpBlock) * sizeof(double);
+  LCK(cudaFuncSetAttribute(k_mlp_policy<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int tfma = host_tanh_fma_lin();
+  const int pgrid = (int)std::min<long long>(148 * 8, std::max<long long>(1, (T + kMlpBlock - 1) / kMlpBlock));
+  LCK(cudaStreamSynchronize(s));
+  // one Picard iteration with single-step processes: dst = pi(rollout(src)); the rollout is left in st
+  auto iterate = [&](const double* src, double* dst) {
+    k_drive<N><<<R.grid, 256, 0, s>>>(B.p, w.p, src, P, T, c.p);
+    R.rollout(zeroA ? nullptr : A.p, c.p, st.p, M.p, v.p, S.p);
+    k_mlp_policy<N><<<pgrid, kMlpBlock, smem, s>>>(W.p, H, P, tfma, st.p, T, dst);
+  };
+  auto change = [&](const double* x, const double* y, unsigned long long* cnt, double* rel) {
+    LCK(cudaMemsetAsync(chg, 0, 2 * sizeof(unsigned long long), s));
+    k_action_change<<<R.grid, 256, 0, s>>>(x, y, P, T, chg);
+    unsigned long long hcg[2];
+    LCK(cudaMemcpyAsync(hcg, chg, sizeof hcg, cudaMemcpyDeviceToHost, s));
+    LCK(cudaStreamSynchronize(s));
+    *cnt = hcg[0];
+    double r;
+    std::memcpy(&r, &hcg[1], sizeof r);
+    *rel = r;
+  };
+  // pass 1: the sequential trajectory as the Picard fixed point (Prop. 1);
+  // also picard_simulate's iterations_to_converged for the single-step plan
+  const int64_t hard_cap = 2 * (int64_t)T + 4;  // picard_simulate's safety cap (engine.hpp:485-490)
+  const auto t0 = std::chrono::steady_clock::now();
+  double* cur = ca.p;
+  double* nxt = cb.p;
+  LCK(cudaMemcpyAsync(cur, c0.p, std::max<size_t>(TP, 1) * 8, cudaMemcpyDeviceToDevice, s));
+  int64_t k = 0, conv = 0;
+  double best = INFINITY;
+  int stall = 0;
+  while (T > 0) {
+    if (k >= hard_cap)
+      throw IterationLimit("picard iteration cap exceeded (" + std::to_string(hard_cap) +
+                           "); the policy may be nondeterministic", k, {});
+    iterate(cur, nxt);
+    ++k;
+    unsigned long long cnt;
+    double rel;
+    change(cur, nxt, &cnt, &rel);
+    std::swap(cur, nxt);
+    if (!(rel == rel)) throw ContractViolation("linear mlp policy: non-finite action");
+    if (!conv && cnt == 0) conv = k;
+    // the fixed point in floating point: no change beyond 2^-46 relative, or
+    // the change stopped shrinking once below 1e-12 (last-ulp oscillation)
+    if (rel <= 0x1p-46) break;
+    if (rel <= 1e-12) {
+      stall = rel < best ? 0 : stall + 1;
+      if (stall >= 3) break;
+    }
+    best = std::min(best, rel);
+    if (conv && k > conv + 200 && rel <= 1e-9) break;
+  }
+  if (T > 0) {
+    // the reference trajectory is the rollout of the fixed-point cache
+    k_drive<N><<<R.grid, 256, 0, s>>>(B.p, w.p, cur, P, T, c.p);
+    R.rollout(zeroA ? nullptr : A.p, c.p, ref.p, M.p, v.p, S.p);
+  } else {
+    LCK(cudaMemsetAsync(ref.p, 0, sizeof(double) * N, s));
+  }
+  LCK(cudaStreamSynchronize(s));
+  const auto t1 = std::chrono::steady_clock::now();
+  res->iterations_to_converged = conv;
+  res->fixed_point_iterations = k;
+  res->fixed_point_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  // pass 2: the curve (linear.cpp:279-318): same iterates, scored against ref
+  k_drive<N><<<R.grid, 256, 0, s>>>(B.p, w.p, init ? c0.p : nullptr, P, T, c.p);
+  R.rollout(zeroA ? nullptr : A.p, c.p, draft.p, M.p, v.p, S.p);
+  const double denom = norm ? R.gap(ref.p, draft.p, part.p, out.p) : R.gap(ref.p, nullptr, part.p, out.p);
+  const int64_t capit = max_it > 0 ? max_it : T;
+  cur = ca.p;
+  nxt = cb.p;
+  LCK(cudaMemcpyAsync(cur, c0.p, std::max<size_t>(TP, 1) * 8, cudaMemcpyDeviceToDevice, s));
+  int64_t n = 0;
+  for (; n < capit; ++n) {
+    if (!(denom > 0.0))  // relative_rmse (linear.cpp:236-262)
+      throw ContractViolation(norm ? "relative rmse: baseline equals the reference"
+                                   : "relative rmse: reference trajectory is zero");
+    iterate(cur, nxt);
+    std::swap(cur, nxt);
+    k_drive<N><<<R.grid, 256, 0, s>>>(B.p, w.p, cur, P, T, c.p);
+    R.rollout(zeroA ? nullptr : A.p, c.p, st.p, M.p, v.p, S.p);
+    const double r = R.gap(ref.p, st.p, part.p, out.p) / denom;
+    if (n < cap) curve[n] = r;
+    if (r <= tol) {
+      ++n;
+      break;
+    }
+  }
+  LCK(cudaGetLastError());
+  res->curve_len = n;
+  res->curve_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+  if (final_cache && T) LCK(cudaMemcpyAsync(final_cache, cur, TP * 8, cudaMemcpyDeviceToHost, s));
+  if (ref_states) LCK(cudaMemcpyAsync(ref_states, ref.p, (TN + N) * 8, cudaMemcpyDeviceToHost, s));
+  LCK(cudaStreamSynchronize(s));
+}
 }  // namespace lin
 }  // namespace pcd
 
@@ -349,6 +589,46 @@ extern "C" int pcd_linear_convergence_curve(const pcd_linear_spec* spec, const d
     switch (spec->state_dim) {
 #define PCD_LIN_CASE(n) \
   case n: curve_impl<n>(spec, initial_cache, tolerance, max_iterations, normalization, curve, curve_cap, curve_len, final_cache, elapsed_ms); break;
+      PCD_LIN_CASE(1) PCD_LIN_CASE(2) PCD_LIN_CASE(3) PCD_LIN_CASE(4)
+      PCD_LIN_CASE(5) PCD_LIN_CASE(6) PCD_LIN_CASE(7) PCD_LIN_CASE(8)
+#undef PCD_LIN_CASE
+    }
+    return PCD_OK;
+  } catch (...) {
+    return pcd::translate_exception();
+  }
+}
+
+extern "C" int pcd_linear_mlp_convergence_curve(const pcd_linear_spec* spec, const pcd_linear_mlp* policy,
+                                                const double* initial_cache, double tolerance,
+                                                int64_t max_iterations, int32_t normalization, int32_t device,
+                                                double* curve, int64_t curve_cap, pcd_linear_mlp_result* result,
+                                                double* final_cache, double* reference_states) {
+  try {
+    if (!spec || !policy || !result) throw pcd::InvalidArgument("null argument");
+    *result = pcd_linear_mlp_result{};
+    if (spec->state_dim < 1 || spec->input_dim < 1 || spec->horizon < 0)
+      throw pcd::ContractViolation("linear spec: dimensions must be positive");
+    if (spec->state_dim > 8 || spec->input_dim > pcd::lin::kMlpMaxP)
+      throw pcd::InvalidArgument("linear mlp policy: state_dim <= 8 and input_dim <= 16 on the device");
+    if (policy->hidden < 1 || policy->hidden > pcd::lin::kMlpMaxH)
+      throw pcd::InvalidArgument("linear mlp policy: hidden width must be in [1, 64]");
+    if (!policy->w1 || !policy->b1 || !policy->w2 || !policy->b2 || !policy->w3 || !policy->b3)
+      throw pcd::InvalidArgument("linear mlp policy: weight arrays missing");
+    if (spec->horizon > 0 && (!spec->dynamics || !spec->input || !spec->disturbances))
+      throw pcd::InvalidArgument("linear spec arrays missing");
+    if (curve_cap > 0 && !curve) throw pcd::InvalidArgument("curve buffer missing");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw pcd::CudaError("no CUDA device available: the B200 engine has no CPU fallback");
+    }
+    if (device < 0 || device >= ndev) throw pcd::InvalidArgument("device index out of range");
+    if (cudaSetDevice(device) != cudaSuccess) throw pcd::CudaError("cudaSetDevice failed");
+    using namespace pcd::lin;
+    switch (spec->state_dim) {
+#define PCD_LIN_CASE(n) \
+  case n: mlp_curve_impl<n>(spec, policy, initial_cache, tolerance, max_iterations, normalization, curve, curve_cap, result, final_cache, reference_states); break;
       PCD_LIN_CASE(1) PCD_LIN_CASE(2) PCD_LIN_CASE(3) PCD_LIN_CASE(4)
       PCD_LIN_CASE(5) PCD_LIN_CASE(6) PCD_LIN_CASE(7) PCD_LIN_CASE(8)
 #undef PCD_LIN_CASE

@@ -94,21 +94,6 @@ __device__ __forceinline__ void ld8s(uint32_t taddr, uint32_t* r) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  const __half2 hh = __floats2half2_rn(x0, x1);
-  const float2 hf = __half22float2(hh);
-  const __half2 l = __floats2half2_rn((x0 - hf.x) * kLoScale, (x1 - hf.y) * kLoScale);
-  hi = *(const uint32_t*)&hh;
-  lo = *(const uint32_t*)&l;
-}
-// tanh(z) = 1 - 2/(1 + e^{2z}) with MUFU ex2 / rcp (error bound: tc_error_bound)
-__device__ __forceinline__ float tanh_mufu(float z) {
-  z = fminf(fmaxf(z, -9.f), 9.f);
-  const float d = 1.f + exp2f_approx(2.8853900817779268f * z);
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
-  return fmaf(-2.f, y, 1.f);
-}
 __device__ __forceinline__ bool bit128(const uint32_t* m, int j) { return (m[j >> 5] >> (j & 31)) & 1u; }
 
 // ---------------------------------------------------------------------------

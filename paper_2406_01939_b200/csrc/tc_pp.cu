@@ -91,23 +91,6 @@ __device__ __forceinline__ void st8s(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  const __half2 hh = __floats2half2_rn(x0, x1);
-  const float2 hf = __half22float2(hh);
-  const __half2 l = __floats2half2_rn((x0 - hf.x) * kLoScale, (x1 - hf.y) * kLoScale);
-  hi = *(const uint32_t*)&hh;
-  lo = *(const uint32_t*)&l;
-}
-// tanh(z) = 1 - 2/(1 + e^{2z}): MUFU ex2 and rcp (each ~1 ulp; ~2e-7
-// absolute; the verify-mode tests bound the end-to-end margin). Weights are
-// finite (tc_scaled_guard), so z is finite and the clamp loses nothing.
-__device__ __forceinline__ float tanh_mufu(float z) {
-  z = fminf(fmaxf(z, -9.f), 9.f);
-  const float d = 1.f + exp2f_approx(2.8853900817779268f * z);
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
-  return fmaf(-2.f, y, 1.f);
-}
 __device__ __forceinline__ void put_feature(unsigned char* sAh, int off, float v) {
   __half hh, l;
   split_f16(v, hh, l);
