@@ -13,7 +13,7 @@ from .api import (  # noqa: F401
     PartitionPlan, PicardConfig, PicardError, PicardResult, PicardTraceRow, Policy, SequentialOutput,
     Simulator, compare_to_oracle, device_count, fo_total_reward, generate_instance,
     make_product_chunk_partition, make_product_partition, make_uniform_time_partition, nccl_unique_id, picard_iterate_once,
-    LoopbackGroup,
+    LoopbackGroup, tc_error_bound,
     picard_simulate, sequential_simulate, shard_processes)
 
 __version__ = "0.1.0"

@@ -88,7 +88,8 @@ class pcd_timing(C.Structure):
                 ("engine_used", C.c_int32), ("device", C.c_int32), ("tc_rows", C.c_int64),
                 ("tc_flagged", C.c_int64), ("tc_disagree", C.c_int64), ("tc_unflagged_bad", C.c_int64),
                 ("tc_used", C.c_int32), ("tc_tiles", C.c_int32),
-                ("tc_kernel", C.c_int32), ("tc_inc_iters", C.c_int32)]
+                ("tc_kernel", C.c_int32), ("tc_inc_iters", C.c_int32),
+                ("tc_guard", C.c_double), ("tc_score_bound", C.c_double), ("tc_max_score_err", C.c_double)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/picard_b200.h
@@ -108,6 +109,8 @@ SIGNATURES = {
     "pcd_linear_mlp_convergence_curve": (C.c_int, [C.POINTER(pcd_linear_spec), C.POINTER(pcd_linear_mlp), F64P,
                                                     C.c_double, C.c_int64, C.c_int32, C.c_int32, F64P, C.c_int64,
                                                     C.POINTER(pcd_linear_mlp_result), F64P, F64P]),
+    "pcd_tc_error_bound": (C.c_int, [C.POINTER(pcd_instance), C.POINTER(pcd_policy), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]),
     "pcd_time_warp": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32, I32P,
                                  C.POINTER(pcd_tw_result), C.POINTER(pcd_tw_trace_row), C.c_int64]),
     "pcd_depletion_profile": (C.c_int, [C.c_void_p, I32P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -28,6 +28,7 @@
 namespace pcd {
 
 constexpr int kTcRows = 128;
+constexpr int kTcStats = 5;  // TcArgs::stats entries
 constexpr int kTcK1 = 208;     // 2J+1 <= 208 (J <= 103)
 constexpr int kTcH = 64;
 constexpr int kTcN3 = 112;     // J <= 112
@@ -40,6 +41,8 @@ constexpr int kW1Bytes = kTcH * kTcK1 * 2;   // one of hi / lo
 constexpr int kW2Bytes = kTcH * kTcH * 2;
 constexpr int kW3Bytes = kTcN3 * kTcH * 2;
 constexpr int kWImgBytes = 2 * (kW1Bytes + kW2Bytes + kW3Bytes);
+constexpr int kWImgRows = kWImgBytes / 256;  // TMA view of the image: [kWImgRows][128] fp16
+static_assert(kWImgBytes % 512 == 0 && kWImgRows / 2 <= 256, "two TMA boxes of <= 256 rows");
 
 __host__ __device__ constexpr int canon_off(int R, int r, int k) {
   return (k >> 3) * 16 * R + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
@@ -60,7 +63,9 @@ struct TcArgs {
   int verify;           // debug: exact re-evaluation of every row
   long long* prof;      // debug: per-phase clock64 totals of CTA 0 (or nullptr)
   unsigned long long* stats;  // [0] tc rows, [1] flagged, [2] flagged & tc wrong,
-                              // [3] (verify) unflagged & tc wrong -- must stay 0
+                              // [3] (verify) unflagged & tc wrong -- must stay 0,
+                              // [4] (verify) max |score_tc - score_exact| over
+                              //     feasible nodes of re-evaluated rows (float bits)
 };
 
 // tc_inc.cu: the sweep with layer 1 off the tensor cores (nodes J <= kIncMaxJ)
@@ -224,6 +229,12 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
   lo = __float2half_rn((x - __half2float(hi)) * kLoScale);
 }
 
+
+inline float __uint_as_float_host(uint32_t b) {
+  float f;
+  __builtin_memcpy(&f, &b, 4);
+  return f;
+}
 
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 hh = __floats2half2_rn(x0, x1);

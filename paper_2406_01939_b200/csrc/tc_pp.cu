@@ -52,7 +52,7 @@ enum {
 static_assert(RI_UXN < kInfo, "per-row state fits");
 enum { CN_CHANGED = 0, CN_CONFLICTS, CN_FIRST, CN_MISM, CN_NEV, CN_TC, CN_COUNT };
 // per-half control block: [0] active rows, [1] flagged rows, [2..66) flagged rows
-enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, kCtl = 80 };
+enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, CT_MAXERR = CT_QACT + 4, kCtl = 80 };
 
 struct Layout {
   static constexpr int w = 0;
@@ -64,8 +64,8 @@ struct Layout {
   static constexpr int cst = ctl + 2 * kCtl * 4;             // invc0[112] b1[64] b2[64] b3[112]
   static constexpr int cnt = cst + 352 * 4;                  // per-row counters
   static constexpr int prof = cnt + CN_COUNT * kTcRows * 4;  // debug phase clocks [20]
-  static constexpr int bar = prof + 20 * 8;                  // one mbarrier per half
-  static constexpr int tmem = bar + 16;
+  static constexpr int bar = prof + 20 * 8;                  // one mbarrier per half + the weight load's
+  static constexpr int tmem = bar + 32;
   static constexpr int total = tmem + 16;
 };
 static_assert(Layout::total <= 232448, "ping-pong sweep shared memory budget");
@@ -108,8 +108,8 @@ __device__ __forceinline__ void put_feature(unsigned char* sAh, int off, float v
 //   lo [0, ...)  f / h1 / h2 / pr (doubles)
 constexpr int kRcInts = 0;
 using rc::kRcVec;
-constexpr int kRcScratchHi = (kRcInts + (2 * kScrJ + 3) * 4 + 15) & ~15;
-constexpr int kRcScratchLo = (kRcVec * 8 + 15) & ~15;
+constexpr int kRcScratchHi = (kRcInts + (rc::kRcBatchInts + rc::kRcBatch) * 4 + 15) & ~15;
+constexpr int kRcScratchLo = ((rc::kRcBatch * rc::kRcRow > kRcVec ? rc::kRcBatch * rc::kRcRow : kRcVec) * 8 + 15) & ~15;
 static_assert(kRcScratchHi <= 12 * kChunkB && kRcScratchLo <= 12 * kChunkB, "recheck scratch in k-chunks 0..11");
 // operand columns the recheck scratch may overwrite (the x/x0 features persist
 // across steps only when they lie above these and above the hidden operands)
@@ -118,7 +118,7 @@ constexpr int kScratchCols = ((kRcScratchHi > kRcScratchLo ? kRcScratchHi : kRcS
 // N3: layer-3 width class (J <= N3), KS1: layer-1 k-steps (2J + 1 <= 16 KS1);
 // the C3 shape is <112, 13>, smaller node counts get narrower MMAs
 template <bool PROF, int N3, int KS1>
-__global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
+__global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_constant__ CUtensorMap wmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const SweepArgs& S = a.s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -154,9 +154,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 
   // ---------------------------------------------------------------- setup
   {
-    const uint4* src = (const uint4*)a.wimg2;
-    uint4* dst = (uint4*)sW;
-    for (int i = tid; i < kWImgBytes / 16; i += kBlock) dst[i] = src[i];
     uint4* da = (uint4*)(smem + Layout::a);
     for (int i = tid; i < 4 * kAH / 16; i += kBlock) da[i] = make_uint4(0, 0, 0, 0);
   }
@@ -208,7 +205,14 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   if (tid == 0) {
     mbar_init(sBar, 1);
     mbar_init(sBar + 1, 1);
+    mbar_init(sBar + 2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the B operands of every MMA (weight image, kWImgBytes) by TMA: two
+    // [kWImgRows/2][128] fp16 boxes; the MMA issuers wait on sBar[2] before
+    // their first layer, so the copy overlaps the first F phase
+    mbar_expect_tx(sBar + 2, kWImgBytes);
+    tma_load_2d(sW, &wmap, 0, 0, sBar + 2);
+    tma_load_2d(sW + kWImgBytes / 2, &wmap, 0, kWImgRows / 2, sBar + 2);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTmem)),
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
   const uint32_t id64 = idesc_f16(64, 64), id128 = idesc_f16(64, 128);
   const uint32_t idn3 = idesc_f16(64, N3), id2n3 = idesc_f16(64, 2 * N3);
   uint32_t phase = 0;
+  bool wready = false;  // (MMA issuers) the weight image's TMA load completed
   const float invT = S.model.horizon > 0 ? (float)(1.0 / (double)S.model.horizon) : 0.f;
   uint32_t xb = 0;  // x > 0 bits of the thread's nodes (bit 8i + k: node 8(g + 4i) + k), persistent
 
@@ -446,6 +451,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     if (PROF && prof_on) pacc[10] += 1;
 
     // ============================ layer 1: z1 = F . W1^T (three products)
+    if (ht == 0 && !wready) {
+      mbar_wait(sBar + 2, 0);  // the TMA weight image has landed
+      wready = true;
+    }
     if (ht == 0) issue_layer(0, kTcH, w1, KS1, id128, id64);
     if (ht == 0) mbar_wait(bar, phase);  // one waiter; the half sleeps on its named barrier
     bar_half(h);
@@ -605,51 +614,105 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
     PMARK(7);
 
     // ============================ exact FP64 re-evaluation of flagged rows
+    // in batches of rc::kRcBatch: one order-free FP64 pass certifies most
+    // rows (fast_margin), the rest take the reference's ordered chain
     const int nflag = ctl[1];
-    for (int f = 0; f < nflag; ++f) {
-      const int Rf = ctl[2 + f], rf = Rf - kHalfRows * h;
-      int* caps = (int*)(sAh + kRcInts);
-      int* xrow = caps + kScrJ;
-      int* res = xrow + kScrJ;
-      // the step's capacities (TMEM cap columns) from the row's four threads
-      if ((rf >> 4) == q) {  // warp-uniform
+    if (nflag > 0) {
+      int* rints = (int*)(sAh + kRcInts);
+      int* rres = rints + rc::kRcBatch * 2 * kScrJ;
+      int* rtb = rres + 4 * rc::kRcBatch;
+      double* rlo = (double*)(sAh + kAH);
+      // verify mode: the row's tensor-core scores (TMEM layer-3 columns) against
+      // the exact ones; ps2 == nullptr: ps holds summed prices
+      auto verify_row = [&](int b, const double* ps, const double* ps2) {
+        const int Rf = ctl[2 + b], rf = Rf - kHalfRows * h;
+        if ((rf >> 4) != q) return;  // warp-uniform
+        const int* caps = rints + (b % rc::kRcBatch) * 2 * kScrJ;
+        const int* xrow = caps + kScrJ;
+        const int* infF = sInfo + Rf * kInfo;
+        const double* rw = S.model.rtab + (size_t)S.model.rrow[infF[RI_T]] * J;
+        const float* rq = a.rtabq + (size_t)infF[RI_RR] * RJ;
+        float emax = 0.f;
         for (int i = 0; i < ni; ++i) {
-          uint32_t v[8];
-          ld8s(tmem + tl + kColCap + 16 * p2 + 32 * i, v);
+          uint32_t vh[8], vx[8];
+          ld8s(tmem + tl + 16 * p2 + 32 * i, vh);
+          ld8s(tmem + tl + N3 + 16 * p2 + 32 * i, vx);
           tmem_wait_ld();
           const int j0 = 8 * (g + 4 * i);
-          if (rr == rf && j0 < kScrJ)
+          if (rr != rf) continue;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) caps[j0 + k] = (int)v[k];
+          for (int k = 0; k < 8; ++k) {
+            const int j = j0 + k;
+            if (j >= J || caps[j] <= 0 || xrow[j] <= 0) continue;
+            const float sc = rq[j] - fmaf(__uint_as_float(vx[k]), kLoInv, __uint_as_float(vh[k]));
+            const double ex = ps2 ? (rw[j] - ps[j]) - ps2[j] : rw[j] - ps[j];
+            emax = fmaxf(emax, __double2float_ru(fabs((double)sc - ex)));
+          }
         }
-      }
-      const int* infF = sInfo + Rf * kInfo;
-      for (int j = ht; j < J; j += kHalfThreads) xrow[j] = S.xloc[(size_t)infF[RI_X] * J + j];
-      bar_half(h);
-      rc::half_recheck(S.model, (double*)(sAh + kAH), caps, xrow, infF[RI_T], res, ht, h, (PROF && prof_on) ? pacc + 15 : nullptr);
-      if (ht == 0) {
-        int* infw = sInfo + Rf * kInfo;
-        const int exact = res[0], nonfinite = res[1];
-        if (nonfinite)
-          atomicMin(&S.scal->err_nonfinite, ((unsigned long long)infw[RI_M] << 32) | (unsigned)infw[RI_OT]);
-        if (infw[RI_FLAG] == 1) {
-          ctl[CT_FLAG] += 1;
-          ctl[CT_DIS] += exact != infw[RI_DEC] ? 1 : 0;
-        } else {
-          ctl[CT_BAD] += exact != infw[RI_DEC] ? 1 : 0;
+        if (rr == rf && emax > 0.f) atomicMax(&ctl[CT_MAXERR], __float_as_int(emax));
+      };
+      for (int f0 = 0; f0 < nflag; f0 += rc::kRcBatch) {
+        const int nb = min(rc::kRcBatch, nflag - f0);
+        // the step's capacities (TMEM cap columns, from the rows' threads) and inventory rows
+        for (int b = 0; b < nb; ++b) {
+          const int rf = ctl[2 + f0 + b] - kHalfRows * h;
+          if ((rf >> 4) == q) {  // warp-uniform
+            int* caps = rints + b * 2 * kScrJ;
+            for (int i = 0; i < ni; ++i) {
+              uint32_t v[8];
+              ld8s(tmem + tl + kColCap + 16 * p2 + 32 * i, v);
+              tmem_wait_ld();
+              const int j0 = 8 * (g + 4 * i);
+              if (rr == rf && j0 < kScrJ)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) caps[j0 + k] = (int)v[k];
+            }
+          }
         }
-        infw[RI_DEC] = exact;
-      }
-      bar_half(h);
-      if (f + 1 == nflag) {
-        // the scratch overlaps K-padding columns of the layer-1 operand when
-        // 2J+1 < kScratchCols: leave zeros behind, as the setup did
-        uint4* zh = (uint4*)sAh;
-        uint4* zl = (uint4*)(sAh + kAH);
-        for (int i = ht; i < kRcScratchHi / 16; i += kHalfThreads) zh[i] = make_uint4(0, 0, 0, 0);
-        for (int i = ht; i < kRcScratchLo / 16; i += kHalfThreads) zl[i] = make_uint4(0, 0, 0, 0);
+        for (int idx = ht; idx < nb * J; idx += kHalfThreads) {
+          const int b = idx / J, j = idx - b * J;
+          const int* infF = sInfo + ctl[2 + f0 + b] * kInfo;
+          rints[b * 2 * kScrJ + kScrJ + j] = S.xloc[(size_t)infF[RI_X] * J + j];
+        }
+        if (ht < nb) rtb[ht] = sInfo[ctl[2 + f0 + ht] * kInfo + RI_T];
+        bar_half(h);
+        rc::half_recheck_fast_batch(S.model, rlo, rints, rtb, nb, ht, h, (PROF && prof_on) ? pacc + 15 : nullptr);
+        if (PROF && prof_on) pacc[11] += 1 + ((long long)nb << 20);  // batches | rows << 20
+        if (a.verify)
+          for (int b = 0; b < nb; ++b)
+            if (rres[4 * b + 2]) verify_row(f0 + b, rlo + b * rc::kRcRow + kTcH, nullptr);
+        // rows the fast path could not certify: the ordered chain (reuses the double scratch)
+        for (int b = 0; b < nb; ++b) {
+          if (rres[4 * b + 2]) continue;  // uniform (shared memory)
+          const int* caps = rints + b * 2 * kScrJ;
+          rc::half_recheck_ordered(S.model, rlo, caps, caps + kScrJ, rtb[b], rres + 4 * b, ht, h);
+          if (PROF && prof_on) pacc[11] += 1LL << 40;  // ordered-chain rows
+          if (a.verify) verify_row(f0 + b, rlo + rc::kRcOpr, rlo + rc::kRcOpr + J);
+        }
+        if (ht == 0) {
+          for (int b = 0; b < nb; ++b) {
+            int* infw = sInfo + ctl[2 + f0 + b] * kInfo;
+            const int exact = rres[4 * b], nonfinite = rres[4 * b + 1];
+            if (nonfinite)
+              atomicMin(&S.scal->err_nonfinite, ((unsigned long long)infw[RI_M] << 32) | (unsigned)infw[RI_OT]);
+            if (infw[RI_FLAG] == 1) {
+              ctl[CT_FLAG] += 1;
+              ctl[CT_DIS] += exact != infw[RI_DEC] ? 1 : 0;
+            } else {
+              ctl[CT_BAD] += exact != infw[RI_DEC] ? 1 : 0;
+            }
+            infw[RI_DEC] = exact;
+          }
+        }
         bar_half(h);
       }
+      // the scratch overlaps K-padding columns of the layer-1 operand when
+      // 2J+1 < kScratchCols: leave zeros behind, as the setup did
+      uint4* zh = (uint4*)sAh;
+      uint4* zl = (uint4*)(sAh + kAH);
+      for (int i = ht; i < kRcScratchHi / 16; i += kHalfThreads) zh[i] = make_uint4(0, 0, 0, 0);
+      for (int i = ht; i < kRcScratchLo / 16; i += kHalfThreads) zl[i] = make_uint4(0, 0, 0, 0);
+      bar_half(h);
     }
     PMARK(8);
 
@@ -735,6 +798,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
       if (c[CT_FLAG]) atomicAdd(&a.stats[1], (unsigned long long)(unsigned)c[CT_FLAG]);
       if (c[CT_DIS]) atomicAdd(&a.stats[2], (unsigned long long)(unsigned)c[CT_DIS]);
       if (c[CT_BAD]) atomicAdd(&a.stats[3], (unsigned long long)(unsigned)c[CT_BAD]);
+      if (c[CT_MAXERR]) atomicMax(&a.stats[4], (unsigned long long)(unsigned)c[CT_MAXERR]);
     }
   }
   tc_fence_before();
@@ -748,24 +812,24 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a) {
 }  // namespace pp
 
 template <bool PROF, int N3>
-static cudaError_t launch_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
+static cudaError_t launch_pp(const TcArgs& a, const CUtensorMap& wmap, int ntiles, cudaStream_t stream) {
   constexpr int KS1 = (2 * N3 + 1 + 15) / 16 < kTcK1 / 16 ? (2 * N3 + 1 + 15) / 16 : kTcK1 / 16;
   const size_t smem = pp::Layout::total;
   const cudaError_t e = ensure_dyn_smem((const void*)pp::k_sweep_pp<PROF, N3, KS1>, smem);
   if (e != cudaSuccess) return e;
-  pp::k_sweep_pp<PROF, N3, KS1><<<ntiles, pp::kBlock, smem, stream>>>(a);
+  pp::k_sweep_pp<PROF, N3, KS1><<<ntiles, pp::kBlock, smem, stream>>>(a, wmap);
   return cudaGetLastError();
 }
 
 int tc_pp_width_class(int J) { return J <= 16 ? 16 : J <= 32 ? 32 : J <= 64 ? 64 : kTcN3; }
 
-cudaError_t launch_tc_pp(const TcArgs& a, int ntiles, cudaStream_t stream) {
-  if (a.prof) return launch_pp<true, kTcN3>(a, ntiles, stream);  // (debug profiles: the C3 shape)
+cudaError_t launch_tc_pp(const TcArgs& a, const CUtensorMap& wmap, int ntiles, cudaStream_t stream) {
+  if (a.prof) return launch_pp<true, kTcN3>(a, wmap, ntiles, stream);  // (debug profiles: the C3 shape)
   switch (a.n3) {
-    case 16: return launch_pp<false, 16>(a, ntiles, stream);
-    case 32: return launch_pp<false, 32>(a, ntiles, stream);
-    case 64: return launch_pp<false, 64>(a, ntiles, stream);
-    default: return launch_pp<false, kTcN3>(a, ntiles, stream);
+    case 16: return launch_pp<false, 16>(a, wmap, ntiles, stream);
+    case 32: return launch_pp<false, 32>(a, wmap, ntiles, stream);
+    case 64: return launch_pp<false, 64>(a, wmap, ntiles, stream);
+    default: return launch_pp<false, kTcN3>(a, wmap, ntiles, stream);
   }
 }
 

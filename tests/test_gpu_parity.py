@@ -529,3 +529,33 @@ def test_single_rank_nccl_path_matches():
         assert r.actions.tolist() == seq.tolist()
         assert [x.astuple() for x in r.trace] == [x.astuple() for x in want.trace]
         assert (r.conflicts, r.iterations_to_correct) == (want.conflicts, want.iterations_to_correct)
+
+
+@pytest.mark.parametrize("J,I,T,M,scale,shrink", [(10, 300, 20000, 512, 1.0, 1), (30, 200, 12000, 256, 1.0, 1),
+                                                   (30, 200, 12000, 256, 2.0, 1), (30, 200, 12000, 256, 1.0, 4),
+                                                   (30, 200, 12000, 256, 3.0, 2), (100, 300, 30000, 512, 1.0, 1)])
+def test_derived_guard_bounds_the_observed_score_error(J, I, T, M, scale, shrink):
+    """The tensor-core guard is derived (tc_error_bound: split / rounding
+    errors, the measured tcgen05 accumulation and tanh_mufu errors, weight-wise
+    propagation), not calibrated: in verify mode every row is re-evaluated in
+    FP64 and the largest observed |score_tc - score_exact| must stay below the
+    a-priori bound B; the guard the sweep used is 2B (1 + 2^-10)."""
+    ons, inst, owner, _, _ = _dual_case(J, I, T, M, "product")
+    p = P.MlpParams.seeded_uniform(2 * J + 1, 2 * J, 5)
+    for a in (p.w1, p.b1, p.w2, p.b2, p.w3, p.b3):
+        a *= scale
+    cap0 = np.maximum(np.asarray(inst.capacity) // shrink, 1)
+    inv0 = np.asarray(inst.inventory) // shrink
+    pol = P.DualNetworkPolicy(p, cap0, inv0, inst.horizon, J)
+    B, guard = P.tc_error_bound(inst, pol)
+    assert B > 0 and guard == pytest.approx(2 * B * (1 + 2 ** -10), rel=1e-15)
+    fp64 = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(engine="product_fp64"))
+    r = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(engine="product", tc_verify=True))
+    t = r.timing
+    assert t["tc_used"] == 1 and t["tc_rows"] > 0
+    assert t["tc_score_bound"] == B and t["tc_guard"] == guard
+    assert t["tc_unflagged_bad"] == 0
+    assert 0 < t["tc_max_score_err"] <= B, (t["tc_max_score_err"], B)
+    assert r.actions.tolist() == fp64.actions.tolist()
+    print(f"J={J} scale={scale} shrink={shrink}: B={B:.3e} observed max {t['tc_max_score_err']:.3e} "
+          f"(B / observed = {B / t['tc_max_score_err']:.0f})")
