@@ -443,6 +443,53 @@ inline std::vector<double> picard_convergence_curve(const linear::LinearSystemSp
   curve.resize(static_cast<std::size_t>(len));
   return curve;
 }
+
+// The same curve with the reference's MlpParams as the linear env's feedback
+// policy, a_t = mlp.forward(s_t) (no reference counterpart: BASELINE config 4's
+// "non-SCO env with MLP policy"; pcd_linear_mlp_convergence_curve). `mlp` has
+// widths {state_dim, hidden, hidden, input_dim}. Also returns, through the
+// optional pointer, picard_simulate's iterations_to_converged for the
+// single-step plan.
+inline std::vector<double> picard_convergence_curve(const linear::LinearSystemSpec& spec, const fo::MlpParams& mlp,
+                                                    std::span<const std::vector<double>> initial_cache = {},
+                                                    const linear::ConvergenceCurveOptions& options = {},
+                                                    std::int64_t* iterations_to_converged = nullptr,
+                                                    int device = 0) {
+  spec.validate();
+  if (mlp.widths.size() != 4 || mlp.widths[0] != spec.state_dim || mlp.widths[3] != spec.input_dim ||
+      mlp.widths[1] != mlp.widths[2])
+    throw std::invalid_argument("mlp widths must be {state_dim, hidden, hidden, input_dim}");
+  const auto n = static_cast<std::size_t>(spec.state_dim), p = static_cast<std::size_t>(spec.input_dim);
+  const auto T = static_cast<std::size_t>(spec.horizon);
+  std::vector<double> A, B, W, init;
+  A.reserve(T * n * n);
+  B.reserve(T * n * p);
+  W.reserve(T * n);
+  for (std::size_t t = 0; t < T; ++t) {
+    A.insert(A.end(), spec.dynamics[t].begin(), spec.dynamics[t].end());
+    B.insert(B.end(), spec.input[t].begin(), spec.input[t].end());
+    W.insert(W.end(), spec.disturbances[t].begin(), spec.disturbances[t].end());
+  }
+  if (!initial_cache.empty()) {
+    if (initial_cache.size() != T) throw ContractViolation("initial cache length must equal the horizon");
+    for (const auto& a : initial_cache) init.insert(init.end(), a.begin(), a.end());
+  }
+  const pcd_linear_spec c{spec.state_dim, spec.input_dim, spec.horizon, A.data(), B.data(), W.data(),
+                          spec.gain.data()};
+  const pcd_linear_mlp m{mlp.widths[1], 0, mlp.w1.data(), mlp.b1.data(), mlp.w2.data(), mlp.b2.data(),
+                         mlp.w3.data(), mlp.b3.data()};
+  const std::int64_t cap = options.max_iterations > 0 ? options.max_iterations : spec.horizon;
+  std::vector<double> curve(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)));
+  pcd_linear_mlp_result res{};
+  const int rc = pcd_linear_mlp_convergence_curve(
+      &c, &m, init.empty() ? nullptr : init.data(), options.tolerance, options.max_iterations,
+      options.normalization == linear::RmseNormalization::draft ? 1 : 0, device, curve.data(),
+      static_cast<std::int64_t>(curve.size()), &res, nullptr, nullptr);
+  if (rc) detail::raise(rc);
+  curve.resize(static_cast<std::size_t>(res.curve_len));
+  if (iterations_to_converged) *iterations_to_converged = res.iterations_to_converged;
+  return curve;
+}
 #endif
 
 // Product-chunk plan (no reference counterpart; pcd_product_chunk_partition):

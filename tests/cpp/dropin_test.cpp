@@ -83,6 +83,17 @@ static void compare(const Instance& inst, const P& policy, const PartitionPlan& 
   CHECK(seq.policy_evals == oracle.policy_evals);
 }
 
+// the reference's MlpParams as a PolicyFor<linear::LinearEnv> (engine.hpp:57-61)
+struct MlpFeedback {
+  static constexpr picard::EvalCost cost_class = picard::EvalCost::expensive;
+  const picard::fo::MlpParams* m;
+  std::vector<double> evaluate(const std::vector<double>& s, const picard::linear::LinearStep&) const {
+    std::vector<double> a(static_cast<std::size_t>(m->widths[3]));
+    m->forward(s, a);
+    return a;
+  }
+};
+
 int main() {
   // toy two-process hand trace (test_engine.cpp:100-138)
   {
@@ -204,6 +215,27 @@ int main() {
     CHECK(got.size() == want.size());
     for (std::size_t k = 0; k < std::min(got.size(), want.size()); ++k)
       CHECK(std::abs(got[k] - want[k]) <= 1e-9 * std::max(1.0, std::abs(want[k])));
+  }
+  // linear env with the reference's MlpParams as the feedback policy (BASELINE
+  // config 4): the device curve's iteration count equals the reference
+  // picard_simulate's for the single-step plan
+  {
+    const auto spec = linear::make_contractive_spec(4, 3, 300, 0.6, 17, 0.3);
+    auto mlp = MlpParams::seeded_uniform(4, 3, 5);
+    for (auto& w : mlp.w3) w *= 20.0;
+    for (auto& b : mlp.b3) b *= 20.0;
+    linear::ConvergenceCurveOptions o;
+    o.tolerance = 1e-7;
+    std::int64_t it = -1;
+    const auto got = b200::picard_convergence_curve(spec, mlp, {}, o, &it);
+    const linear::LinearEnv lenv(spec);
+    const auto steps = linear::make_steps(spec);
+    PartitionPlan plan;
+    plan.processes = static_cast<std::int32_t>(spec.horizon);
+    for (std::int64_t t = 0; t < spec.horizon; ++t) plan.owner.push_back(static_cast<std::int32_t>(t));
+    const auto ref = picard_simulate(lenv, MlpFeedback{&mlp}, std::span<const linear::LinearStep>(steps), plan);
+    CHECK(it == ref.iterations_to_converged);
+    CHECK(!got.empty() && got.back() <= 1e-7);
   }
   // iteration cap (test_engine.cpp:525-545)
   {
