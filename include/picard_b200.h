@@ -122,12 +122,12 @@ typedef struct pcd_config {
   int32_t threads;         /* accepted for API parity; the device ignores it */
   int32_t engine;          /* PCD_ENGINE_* */
   double tc_guard;         /* tensor-core decision margin below which a row is
-                              re-evaluated in exact FP64. 0 = the DERIVED guard
-                              2B (1 + 2^-10), B an a-priori bound on the
-                              tensor-core score error for this policy and
-                              instance (pcd_tc_error_bound), which makes every
-                              accepted decision the reference's. A value > 0
-                              overrides it (tuning / experiments only).       */
+                              re-evaluated in exact FP64. 0 = the DERIVED guards
+                              of pcd_tc_error_bound (an a-priori bound on the
+                              tensor-core score errors for this policy and
+                              instance), which make every accepted decision the
+                              reference's. A value > 0 overrides both tests
+                              (tuning / experiments only).                    */
   int32_t tc_verify;       /* debug: re-evaluate EVERY row in FP64 and count
                               unflagged disagreements (pcd_timing.tc_unflagged_bad) */
   int32_t tc_tiles;        /* CTAs of the tensor-core sweep; 0 = one per SM (tests
@@ -181,7 +181,7 @@ typedef struct pcd_timing {
   int32_t tc_tiles;       /* CTAs (128 processes each) */
   int32_t tc_kernel;      /* sweep kernel of the last tensor-core iteration: 1 fused, 2 incremental */
   int32_t tc_inc_iters;   /* iterations that ran the incremental-layer-1 sweep */
-  double tc_guard;        /* decision-margin guard the sweep used (derived: 2B (1 + 2^-10)) */
+  double tc_guard;        /* best-minus-second margin guard the sweep used */
   double tc_score_bound;  /* B: derived bound on |score_tc - score_ref| (0: no tensor-core path) */
   double tc_max_score_err;/* tc_verify only: largest observed |score_tc - score_exact| (<= B) */
 } pcd_timing;
@@ -320,9 +320,11 @@ int pcd_linear_mlp_convergence_curve(const pcd_linear_spec* spec, const pcd_line
 /* The tensor-core sweep's derived exactness bound (no
  * reference counterpart, host only, no device needed): *bound = B, an
  * a-priori bound on |score_tc - score_ref| of the dual policy on this
- * instance; *guard = 2B (1 + 2^-10), the decision margin pcd_create uses, or
- * 0 when the policy keeps the exact FP64 path (non-finite weights, bound too
- * large, shapes the tensor-core sweep does not take). */
+ * instance (the |best| test uses B (1 + 2^-10)); *guard = D (1 + 2^-10), D a
+ * bound on the error of the difference of two scores of one row (<= 2B: the
+ * hidden-layer error is shared), the best-minus-second margin pcd_create
+ * uses; 0 when the policy keeps the exact FP64 path (non-finite weights,
+ * bound too large, shapes the tensor-core sweep does not take). */
 int pcd_tc_error_bound(const pcd_instance* instance, const pcd_policy* policy, double* bound, double* guard);
 
 /* Page-locked host buffers from a process-wide pool (no reference

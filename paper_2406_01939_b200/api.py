@@ -683,9 +683,11 @@ def device_count() -> int:
 
 def tc_error_bound(instance: "Instance", policy: "Policy") -> tuple:
     """(B, guard) of the tensor-core sweep for a dual policy on an instance
-    (pcd_tc_error_bound; host only): B bounds |score_tc - score_ref| a priori,
-    guard = 2B (1 + 2^-10) is the decision margin the sweep uses by default,
-    0 when the policy keeps the exact FP64 path."""
+    (pcd_tc_error_bound; host only): B bounds |score_tc - score_ref| a priori
+    (the |best| test uses B (1 + 2^-10)); guard bounds the error of a
+    difference of two scores of one row, times 1 + 2^-10 (the best-minus-second
+    margin the sweep uses by default); 0 when the policy keeps the exact FP64
+    path."""
     b, g = C.c_double(), C.c_double()
     ci, cp = instance.to_c(), policy.to_c()
     _check(LIB.pcd_tc_error_bound(C.byref(ci), C.byref(cp), C.byref(b), C.byref(g)))

@@ -320,6 +320,7 @@ struct pcd_handle {
   bool tc_ok = false;                    // dual policy with 2J+1 <= 208, hidden 64
   double tc_guard = 0.0;                 // derived guard 2B (1 + 2^-10), tc_error_bound
   double tc_bound = 0.0;                 // B: bound on |score_tc - score_ref|
+  double tc_guard_abs = 0.0;             // B (1 + 2^-10): the |best| test
   int tc_n3 = 0;                         // layer-3 width class of the ping-pong image (prepare_tc)
   pcd::DBuf<unsigned char> tc_wimg2;
   pcd::DBuf<float> tc_b1, tc_b2, tc_ic0, tc_ix0, tc_rtq;
@@ -615,11 +616,14 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabq = h->tc_rtq.p;
-  {  // the guard as a float rounded up, so the kernel's margin test never undercuts it
-    const double g = guard > 0 ? guard : h->tc_guard;
-    float gf = (float)g;
-    if ((double)gf < g) gf = nextafterf(gf, INFINITY);
-    a.guard = gf;
+  {  // the guards as floats rounded up, so the kernel's margin tests never undercut them
+    auto up = [](double g) {
+      float gf = (float)g;
+      if ((double)gf < g) gf = nextafterf(gf, INFINITY);
+      return gf;
+    };
+    a.guard = up(guard > 0 ? guard : h->tc_guard);
+    a.guard_abs = up(guard > 0 ? guard : h->tc_guard_abs);
   }
   a.verify = verify;
   a.stats = h->tc_stats.p;
@@ -1249,7 +1253,8 @@ static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax
 // used (non-finite weights, operands outside fp16 range, features > 1e4).
 constexpr double kTanhErr = 0x1p-22;  // >= max |tanh_mufu(z) - tanh(z)| over all floats (probe)
 static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, const int32_t* pcap,
-                             const int32_t* pinv, int64_t horizon, int J, int H) {
+                             const int32_t* pinv, int64_t horizon, int J, int H, double* bdiff) {
+  *bdiff = 0.0;
   const int inw = 2 * J + 1;
   const double u = 0x1p-24, t36 = 0x1p-36;
   double wmax = 0;
@@ -1290,26 +1295,40 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
   // one layer: inputs with magnitude bound X[c] and error bound dX[c] (relative
   // representation error of the inputs themselves: rel_in), weights w(r, c);
   // returns the error bound of every output (before the activation)
+  // nonneg: the inputs are >= 0 (layer 1's features), so each hi.hi product has
+  // its weight's sign and the per-term truncations (toward zero) of one MMA
+  // can only add up within one sign class: max(n+, n-) + 1 (the accumulator,
+  // sign unknown) terms instead of 17
   auto layer = [&](int rows, int K, auto w, const std::vector<double>& X, const std::vector<double>& dX,
-                   double rel_in, auto bias) {
+                   double rel_in, auto bias, bool nonneg) {
     std::vector<double> dz((size_t)rows);
     const int steps = (K + 15) / 16;
     for (int r = 0; r < rows; ++r) {
-      double P = 0, accsum = 0, prop = 0, absw = 0;
+      double P = 0, accsum = 0, psum = 0, prop = 0, absw = 0;
       for (int s = 0; s < steps; ++s) {
+        int npos = 0, nneg = 0;
+        const double Pin = P;  // bound on the accumulator entering the MMA
+        double pmax = 0;       // bound on its largest product
         for (int c = 16 * s; c < std::min(K, 16 * s + 16); ++c) {
-          const double aw = std::fabs(w(r, c));
+          const double wv = w(r, c), aw = std::fabs(wv);
           P += aw * X[(size_t)c] * slack;
+          pmax = std::max(pmax, aw * X[(size_t)c] * slack);
           prop += aw * dX[(size_t)c];
           absw += aw + X[(size_t)c];
+          npos += wv > 0 && X[(size_t)c] > 0;
+          nneg += wv < 0 && X[(size_t)c] > 0;
         }
-        accsum += P;  // sum over MMAs of the partial-sum bound after the k-step
+        // one MMA errs by < n u 2^e + 2u |D|: n truncated terms (the products,
+        // or with nonneg inputs one sign class of them, plus the accumulator),
+        // 2^e <= max(|C|, max |p|) <= max(Pin, pmax), |D| <= P
+        accsum += (nonneg ? std::max(npos, nneg) + 1 : 17) * std::max(Pin, pmax) + 2 * P;
+        psum += P;
       }
       const double b = std::fabs(bias(r));
       // per product: feature/weight roundings + both splits + dropped lo.lo
       const double terms = (rel_in + 2 * 0x1p-22 + u + 0x1p-22) * P + 2 * t36 * absw;
-      const double acc_hh = 19 * u * accsum;                  // hi.hi MMAs
-      const double acc_x = 0x1p-11 * 2 * 19 * u * 2 * accsum;  // hi.lo + lo.hi MMAs (x2 terms, x2 per k-step)
+      const double acc_hh = u * accsum;                       // hi.hi MMAs
+      const double acc_x = 0x1p-11 * 2 * 19 * u * 2 * psum;  // hi.lo + lo.hi MMAs (x2 terms, x2 per k-step)
       const double rnd = u * P * 1.01 + u * b + u * (P + b) * 1.01;  // fmaf combine, fp32 bias, bias add
       dz[(size_t)r] = prop + terms + acc_hh + acc_x + rnd;
     }
@@ -1318,24 +1337,40 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
   // layer 1 (features: 3 fp32 roundings each)
   std::vector<double> zeros((size_t)inw, 0.0);
   const auto dz1 = layer(H, inw, [&](int r, int c) { return pol->w1[(size_t)r * inw + c]; }, F, zeros, 3 * u,
-                         [&](int r) { return pol->b1[r]; });
+                         [&](int r) { return pol->b1[r]; }, true);
   std::vector<double> X2((size_t)H, 1.0), dh1((size_t)H);
   for (int n = 0; n < H; ++n) dh1[(size_t)n] = dz1[(size_t)n] + kTanhErr;
   const auto dz2 = layer(H, H, [&](int r, int c) { return pol->w2[(size_t)r * H + c]; }, X2, dh1, 0.0,
-                         [&](int r) { return pol->b2[r]; });
+                         [&](int r) { return pol->b2[r]; }, false);
   std::vector<double> dh2((size_t)H);
   for (int n = 0; n < H; ++n) dh2[(size_t)n] = dz2[(size_t)n] + kTanhErr;
   const auto dq = layer(J, H, [&](int r, int c) { return pol->w3[(size_t)r * H + c] + pol->w3[(size_t)(J + r) * H + c]; },
-                        X2, dh2, 0.0, [&](int) { return 0.0; });
+                        X2, dh2, 0.0, [&](int) { return 0.0; }, false);
   double B = 0;
+  std::vector<double> own((size_t)J);
+  auto w3s = [&](int j, int l) { return pol->w3[(size_t)j * H + l] + pol->w3[(size_t)(J + j) * H + l]; };
   for (int j = 0; j < J; ++j) {
-    double P3 = 0;
-    for (int l = 0; l < H; ++l) P3 += std::fabs(pol->w3[(size_t)j * H + l] + pol->w3[(size_t)(J + j) * H + l]);
+    double P3 = 0, prop = 0;
+    for (int l = 0; l < H; ++l) {
+      P3 += std::fabs(w3s(j, l));
+      prop += std::fabs(w3s(j, l)) * dh2[(size_t)l];
+    }
     const double b3s = std::fabs(pol->b3[j] + pol->b3[J + j]);
     // rtabq = fl32(r - b3s), score = fl32(rtabq - q)
     const double ds = dq[(size_t)j] + u * (rmax + b3s) + u * (rmax + b3s + P3) * 1.01;
+    own[(size_t)j] = ds - prop;  // everything but the propagated h2 error
     B = std::max(B, ds);
   }
+  // the margin test compares two scores of the same row: their h2 error is
+  // shared, so the difference s_i - s_j errs by at most
+  //   sum_l |W3'_il - W3'_jl| |dh2_l| + own_i + own_j
+  double D = 0;
+  for (int i = 0; i < J; ++i)
+    for (int j = i + 1; j < J; ++j) {
+      double a = 0;
+      for (int l = 0; l < H; ++l) a += std::fabs(w3s(i, l) - w3s(j, l)) * dh2[(size_t)l];
+      D = std::max(D, a + own[(size_t)i] + own[(size_t)j]);
+    }
   // the reference's FP64 scores against exact arithmetic (the same analysis as
   // fast_margin_bound with u = 2^-53 and one ordered chain)
   double fmaxall = 1.0;
@@ -1343,7 +1378,8 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
   const double fm = fast_margin_bound(pol, J, H, rmax, fmaxall);
   if (!(fm > 0)) return 0.0;  // the FP64 scores themselves are not known to 1e-6
   B += fm;
-  return std::isfinite(B) ? B : 0.0;
+  *bdiff = std::isfinite(D) ? D + 2 * fm : 0.0;
+  return std::isfinite(B) && std::isfinite(D) ? B : 0.0;
 }
 constexpr double kMaxTcGuard = 2e-2;  // beyond this most rows would be re-evaluated: FP64 path
 
@@ -1514,11 +1550,13 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
       const int32_t* pc = pol->init_capacity ? pol->init_capacity : in->capacity;
       const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
                                              : in->inventory;
-      const double B = tc_error_bound(pol, in, pc, pi, h->p_horizon, h->J, H);
-      const double g = 2.0 * B * (1.0 + 0x1p-10);
+      double Bd = 0;
+      const double B = tc_error_bound(pol, in, pc, pi, h->p_horizon, h->J, H, &Bd);
+      const double g = Bd * (1.0 + 0x1p-10);
       if (B > 0 && g <= kMaxTcGuard) {
         prepare_tc(h.get(), pol, pc, pi, in->reward_table);
         h->tc_guard = g;
+        h->tc_guard_abs = B * (1.0 + 0x1p-10);
         h->tc_bound = B;
       }
     }
@@ -1547,8 +1585,9 @@ extern "C" int pcd_tc_error_bound(const pcd_instance* in, const pcd_policy* pol,
   const int32_t* pc = pol->init_capacity ? pol->init_capacity : in->capacity;
   const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory) : in->inventory;
   const int64_t ph = pol->horizon >= 0 ? pol->horizon : in->horizon;
-  const double B = tc_error_bound(pol, in, pc, pi, ph, J, H);
-  const double g = 2.0 * B * (1.0 + 0x1p-10);
+  double Bd = 0;
+  const double B = tc_error_bound(pol, in, pc, pi, ph, J, H, &Bd);
+  const double g = Bd * (1.0 + 0x1p-10);
   *bound = B;
   *guard = (B > 0 && g <= kMaxTcGuard) ? g : 0.0;
   return PCD_OK;

@@ -733,7 +733,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_inc(IncArgs x, const __grid
         } else {
           inf[RI_ANY] = 1;
           inf[RI_DEC] = v1 >= 0.f ? i1 : -1;
-          const bool flag = bad || i1 < 0 || !(v1 - v2 >= a.guard) || !(fabsf(v1) >= a.guard);
+          const float g = fmaxf(a.guard, a.guard_abs);  // (the derived bound is proven for tc_pp's layer 1)
+          const bool flag = bad || i1 < 0 || !(v1 - v2 >= g) || !(fabsf(v1) >= g);
           cn_tc += 1;
           if (flag || a.verify) {
             inf[RI_FLAG] = flag ? 1 : 2;

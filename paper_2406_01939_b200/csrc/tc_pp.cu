@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
         } else {
           inf[RI_ANY] = 1;
           inf[RI_DEC] = v1 >= 0.f ? i1 : -1;
-          const bool flag = bad || i1 < 0 || !(v1 - v2 >= a.guard) || !(fabsf(v1) >= a.guard);
+          const bool flag = bad || i1 < 0 || !(v1 - v2 >= a.guard) || !(fabsf(v1) >= a.guard_abs);
           sCnt[CN_TC * kTcRows + R] += 1;
           if (flag || a.verify) {
             inf[RI_FLAG] = flag ? 1 : 2;

@@ -539,7 +539,7 @@ def test_derived_guard_bounds_the_observed_score_error(J, I, T, M, scale, shrink
     errors, the measured tcgen05 accumulation and tanh_mufu errors, weight-wise
     propagation), not calibrated: in verify mode every row is re-evaluated in
     FP64 and the largest observed |score_tc - score_exact| must stay below the
-    a-priori bound B; the guard the sweep used is 2B (1 + 2^-10)."""
+    a-priori bound B; the sweep's margin guard bounds score differences."""
     ons, inst, owner, _, _ = _dual_case(J, I, T, M, "product")
     p = P.MlpParams.seeded_uniform(2 * J + 1, 2 * J, 5)
     for a in (p.w1, p.b1, p.w2, p.b2, p.w3, p.b3):
@@ -548,7 +548,9 @@ def test_derived_guard_bounds_the_observed_score_error(J, I, T, M, scale, shrink
     inv0 = np.asarray(inst.inventory) // shrink
     pol = P.DualNetworkPolicy(p, cap0, inv0, inst.horizon, J)
     B, guard = P.tc_error_bound(inst, pol)
-    assert B > 0 and guard == pytest.approx(2 * B * (1 + 2 ** -10), rel=1e-15)
+    # the margin guard bounds the error of a DIFFERENCE of two scores of one
+    # row (shared hidden-layer error): between B and 2B (times 1 + 2^-10)
+    assert B > 0 and B < guard <= 2 * B * (1 + 2 ** -10)
     fp64 = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(engine="product_fp64"))
     r = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(engine="product", tc_verify=True))
     t = r.timing
