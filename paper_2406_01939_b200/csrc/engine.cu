@@ -1304,24 +1304,30 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
     std::vector<double> dz((size_t)rows);
     const int steps = (K + 15) / 16;
     for (int r = 0; r < rows; ++r) {
-      double P = 0, accsum = 0, psum = 0, prop = 0, absw = 0;
+      // P: sum |w| X over the inputs so far; Pp / Pn: the same over positive /
+      // negative weights. With nonneg inputs (0 <= x <= X) every partial sum
+      // lies in [-Pn, Pp], so |C|, |D| <= max(Pp, Pn) (a linear form over a box
+      // peaks at a vertex); otherwise they are bounded by P.
+      double P = 0, Pp = 0, Pn = 0, accsum = 0, psum = 0, prop = 0, absw = 0;
       for (int s = 0; s < steps; ++s) {
         int npos = 0, nneg = 0;
-        const double Pin = P;  // bound on the accumulator entering the MMA
-        double pmax = 0;       // bound on its largest product
+        const double Cin = nonneg ? std::max(Pp, Pn) : P;  // bound on the accumulator entering the MMA
+        double pmax = 0;                                   // bound on its largest product
         for (int c = 16 * s; c < std::min(K, 16 * s + 16); ++c) {
-          const double wv = w(r, c), aw = std::fabs(wv);
-          P += aw * X[(size_t)c] * slack;
-          pmax = std::max(pmax, aw * X[(size_t)c] * slack);
+          const double wv = w(r, c), aw = std::fabs(wv), t = aw * X[(size_t)c] * slack;
+          P += t;
+          (wv > 0 ? Pp : Pn) += t;
+          pmax = std::max(pmax, t);
           prop += aw * dX[(size_t)c];
           absw += aw + X[(size_t)c];
           npos += wv > 0 && X[(size_t)c] > 0;
           nneg += wv < 0 && X[(size_t)c] > 0;
         }
+        const double Dout = nonneg ? std::max(Pp, Pn) : P;
         // one MMA errs by < n u 2^e + 2u |D|: n truncated terms (the products,
         // or with nonneg inputs one sign class of them, plus the accumulator),
-        // 2^e <= max(|C|, max |p|) <= max(Pin, pmax), |D| <= P
-        accsum += (nonneg ? std::max(npos, nneg) + 1 : 17) * std::max(Pin, pmax) + 2 * P;
+        // 2^e <= max(|C|, max |p|)
+        accsum += (nonneg ? std::max(npos, nneg) + 1 : 17) * std::max(Cin, pmax) + 2 * Dout;
         psum += P;
       }
       const double b = std::fabs(bias(r));

@@ -5,7 +5,8 @@ partitioner; at most I processes carry work), product-chunk partitions and
 (C5_PARTS=uniform) the reference's uniform time partition on the general
 closed-form engine.
 
-  [C5_PARTS=product,chunk,uniform] [C5_REPS=2] python tools/c5_sweep.py [M ...]
+  [C5_PARTS=product,chunk,uniform] [C5_REPS=2] [C5_WINDOW=300000] python tools/c5_sweep.py [M ...]
+  (C5_WINDOW: PicardConfig::max_steps; default the CLI's 300*M)
   -> one JSON line per (partition, M)
 """
 import json
@@ -23,6 +24,7 @@ pol = P.DualNetworkPolicy.seeded(inst, 5)
 seq = None
 PARTS = os.environ.get("C5_PARTS", "product,chunk").split(",")
 REPS = int(os.environ.get("C5_REPS", "2"))
+WINDOW = int(os.environ.get("C5_WINDOW", "0"))
 for part in PARTS:
     for M in Ms:
         if part == "chunk":
@@ -33,7 +35,7 @@ for part in PARTS:
             plan = P.make_product_partition(inst, M, 1)
         with P.Simulator(inst, pol) as sim:
             sim.set_plan(plan)
-            cfg = P.PicardConfig(max_steps=300 * M)
+            cfg = P.PicardConfig(max_steps=WINDOW or 300 * M)
             r = sim.simulate_resident(cfg)  # warm-up (the timed run when REPS = 0)
             best = r.timing["total_ms"] if REPS == 0 else None
             for _ in range(REPS):
@@ -43,7 +45,8 @@ for part in PARTS:
             acts = sim.download_actions()
         if seq is None:
             seq = acts
-        print(json.dumps({"config": "c5", "partition": part, "M": M, "engine_used": r.timing["engine_used"],
+        print(json.dumps({"config": "c5", "partition": part, "M": M, "max_steps": WINDOW or 300 * M,
+                          "engine_used": r.timing["engine_used"], "tc_flagged": r.timing["tc_flagged"],
                           "iterations": r.iterations_to_converged,
                           "steps_critical": r.timing["steps_critical"], "total_evals": r.total_policy_evals,
                           "ms": best, "steps_per_s": T / (best / 1000.0),
