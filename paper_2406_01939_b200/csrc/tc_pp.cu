@@ -47,12 +47,19 @@ constexpr int kChunkB = kHalfRows * 8 * 2;  // bytes per k-chunk of a half's ope
 enum {
   RI_T = 0, RI_P, RI_POS, RI_END, RI_ANY, RI_DEC, RI_FLAG, RI_RR, RI_TN, RI_XDIRTY, RI_XUPD, RI_OT, RI_EVT,
   RI_X, RI_M, RI_DRESET,
-  RI_UEV, RI_UOLD, RI_UWR, RI_UREF, RI_UPN, RI_URRN, RI_UOTN, RI_UTNN, RI_UXN
+  RI_UEV, RI_UOLD, RI_UWR, RI_UREF, RI_UPN, RI_URRN, RI_UOTN, RI_UTNN, RI_UXN,
+  RI_WAIT,   // steps this row's current slot has waited for its FP64 re-evaluation
+  RI_PAUSE   // the slot's re-evaluation is deferred: redo the step, no update
 };
-static_assert(RI_UXN < kInfo, "per-row state fits");
+static_assert(RI_PAUSE < kInfo, "per-row state fits");
+// Flagged rows wait (redoing their step, which is deterministic: same slot,
+// same state) until kRcBatch of them are pending in the half, one has waited
+// kMaxWait steps, or they are at least half of the active rows; then the
+// whole pending set is re-evaluated in batches (tc_recheck.cuh)
+constexpr int kMaxWait = 3;
 enum { CN_CHANGED = 0, CN_CONFLICTS, CN_FIRST, CN_MISM, CN_NEV, CN_TC, CN_COUNT };
 // per-half control block: [0] active rows, [1] flagged rows, [2..66) flagged rows
-enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, CT_MAXERR = CT_QACT + 4, kCtl = 80 };
+enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, CT_MAXERR = CT_QACT + 4, CT_MAXWAIT, kCtl = 80 };
 
 struct Layout {
   static constexpr int w = 0;
@@ -182,6 +189,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     inf[RI_DRESET] = 1;
     inf[RI_P] = -1;
     inf[RI_X] = -1;
+    inf[RI_WAIT] = 0;
+    inf[RI_PAUSE] = 0;
     if (pos < end) {
       const int t = S.pslots[pos];
       inf[RI_T] = t;
@@ -601,11 +610,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
           inf[RI_ANY] = 1;
           inf[RI_DEC] = v1 >= 0.f ? i1 : -1;
           const bool flag = bad || i1 < 0 || !(v1 - v2 >= a.guard) || !(fabsf(v1) >= a.guard_abs);
-          sCnt[CN_TC * kTcRows + R] += 1;
+          if (!flag) sCnt[CN_TC * kTcRows + R] += 1;  // (flagged rows: when re-evaluated)
           if (flag || a.verify) {
             inf[RI_FLAG] = flag ? 1 : 2;
             const int k = atomicAdd(&ctl[1], 1);
             ctl[2 + k] = R;
+            if (flag) atomicMax(&ctl[CT_MAXWAIT], inf[RI_WAIT]);
           }
         }
       }
@@ -617,7 +627,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     // in batches of rc::kRcBatch: one order-free FP64 pass certifies most
     // rows (fast_margin), the rest take the reference's ordered chain
     const int nflag = ctl[1];
-    if (nflag > 0) {
+    const bool rc_run =
+        nflag > 0 && (a.verify || nflag >= rc::kRcBatch || ctl[CT_MAXWAIT] >= kMaxWait || 2 * nflag >= ctl[0]);
+    if (!rc_run && nflag > 0 && agent && inf[RI_FLAG] == 1) {  // defer: redo this step
+      inf[RI_PAUSE] = 1;
+      inf[RI_WAIT] += 1;
+    }
+    if (rc_run) {
       int* rints = (int*)(sAh + kRcInts);
       int* rres = rints + rc::kRcBatch * 2 * kScrJ;
       int* rtb = rres + 4 * rc::kRcBatch;
@@ -695,9 +711,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
             const int exact = rres[4 * b], nonfinite = rres[4 * b + 1];
             if (nonfinite)
               atomicMin(&S.scal->err_nonfinite, ((unsigned long long)infw[RI_M] << 32) | (unsigned)infw[RI_OT]);
+            infw[RI_WAIT] = 0;
             if (infw[RI_FLAG] == 1) {
               ctl[CT_FLAG] += 1;
               ctl[CT_DIS] += exact != infw[RI_DEC] ? 1 : 0;
+              sCnt[CN_TC * kTcRows + ctl[2 + f0 + b]] += 1;
             } else {
               ctl[CT_BAD] += exact != infw[RI_DEC] ? 1 : 0;
             }
@@ -719,7 +737,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     // ============================ U: update + publish (row agents)
     if (agent) {
       inf[RI_DRESET] = 0;
-      if (inf[RI_ANY] >= 0) {
+      if (inf[RI_PAUSE]) {  // deferred re-evaluation: same slot next step, no state change
+        inf[RI_PAUSE] = 0;
+        inf[RI_EVT] = -1;
+        inf[RI_XUPD] = -1;
+      } else if (inf[RI_ANY] >= 0) {
         const int t = inf[RI_T], x = inf[RI_X], dec = inf[RI_DEC];
         const int uo = inf[RI_UOLD], uxn = inf[RI_UXN];
         // D deltas are applied by the row's F threads next step
@@ -771,6 +793,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     if (ht == kHalfThreads - 1) {
       ctl[0] = 0;
       ctl[1] = 0;
+      ctl[CT_MAXWAIT] = 0;
     }
     bar_half(h);
     PMARK(9);
