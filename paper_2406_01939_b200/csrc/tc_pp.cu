@@ -115,7 +115,7 @@ __device__ __forceinline__ void put_feature(unsigned char* sAh, int off, float v
 //   lo [0, ...)  f / h1 / h2 / pr (doubles)
 constexpr int kRcInts = 0;
 using rc::kRcVec;
-constexpr int kRcScratchHi = (kRcInts + (rc::kRcBatchInts + rc::kRcBatch) * 4 + 15) & ~15;
+constexpr int kRcScratchHi = (kRcInts + rc::kRcBatchInts * 4 + 15) & ~15;
 constexpr int kRcScratchLo = ((rc::kRcBatch * rc::kRcRow > kRcVec ? rc::kRcBatch * rc::kRcRow : kRcVec) * 8 + 15) & ~15;
 static_assert(kRcScratchHi <= 12 * kChunkB && kRcScratchLo <= 12 * kChunkB, "recheck scratch in k-chunks 0..11");
 // operand columns the recheck scratch may overwrite (the x/x0 features persist
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     if (rc_run) {
       int* rints = (int*)(sAh + kRcInts);
       int* rres = rints + rc::kRcBatch * 2 * kScrJ;
-      int* rtb = rres + 4 * rc::kRcBatch;
+      int* rinfo = rres + 4 * rc::kRcBatch;  // rc::kRcRowInfo per row
       double* rlo = (double*)(sAh + kAH);
       // verify mode: the row's tensor-core scores (TMEM layer-3 columns) against
       // the exact ones; ps2 == nullptr: ps holds summed prices
@@ -685,14 +685,18 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
             }
           }
         }
-        for (int idx = ht; idx < nb * J; idx += kHalfThreads) {
-          const int b = idx / J, j = idx - b * J;
-          const int* infF = sInfo + ctl[2 + f0 + b] * kInfo;
-          rints[b * 2 * kScrJ + kScrJ + j] = S.xloc[(size_t)infF[RI_X] * J + j];
+        if (ht < nb) {
+          const int* infF = sInfo + ctl[2 + f0 + ht] * kInfo;
+          int* ri = rinfo + rc::kRcRowInfo * ht;
+          ri[0] = infF[RI_T];
+          ri[1] = infF[RI_P];
+          ri[2] = infF[RI_X];
+          ri[3] = infF[RI_RR];
+          ri[4] = infF[RI_OT];
         }
-        if (ht < nb) rtb[ht] = sInfo[ctl[2 + f0 + ht] * kInfo + RI_T];
         bar_half(h);
-        rc::half_recheck_fast_batch(S.model, rlo, rints, rtb, nb, ht, h, (PROF && prof_on) ? pacc + 15 : nullptr);
+        rc::half_recheck_fast_batch(S.model, S.xloc, rlo, rints, rinfo, nb, ht, h,
+                                    (PROF && prof_on) ? pacc + 15 : nullptr);
         if (PROF && prof_on) pacc[11] += 1 + ((long long)nb << 20);  // batches | rows << 20
         if (a.verify)
           for (int b = 0; b < nb; ++b)
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
         for (int b = 0; b < nb; ++b) {
           if (rres[4 * b + 2]) continue;  // uniform (shared memory)
           const int* caps = rints + b * 2 * kScrJ;
-          rc::half_recheck_ordered(S.model, rlo, caps, caps + kScrJ, rtb[b], rres + 4 * b, ht, h);
+          rc::half_recheck_ordered(S.model, rlo, caps, caps + kScrJ, rinfo[rc::kRcRowInfo * b], rres + 4 * b, ht, h);
           if (PROF && prof_on) pacc[11] += 1LL << 40;  // ordered-chain rows
           if (a.verify) verify_row(f0 + b, rlo + rc::kRcOpr, rlo + rc::kRcOpr + J);
         }

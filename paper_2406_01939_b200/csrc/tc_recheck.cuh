@@ -241,10 +241,18 @@ __device__ __forceinline__ void ldg1_group(double (&v)[N], const double* p, size
 constexpr int kRcBatch = 4;
 constexpr int kRcH1 = 2 * kRcMaxJ + 2;
 constexpr int kRcRow = kRcH1 + kTcH;
-constexpr int kRcBatchInts = kRcBatch * 2 * kRcMaxJ + 4 * kRcBatch;
+// per-row slot description: [0] t, [1] product, [2] run (row of xloc), [3]
+// reward row, [4] order time (the row agent's bookkeeping, so no dependent
+// lookups through the order tape)
+constexpr int kRcRowInfo = 5;
+constexpr int kRcBatchInts = kRcBatch * 2 * kRcMaxJ + 4 * kRcBatch + kRcRowInfo * kRcBatch;
 
-__device__ inline void half_recheck_fast_batch(const DevModel& P, double* lo, int* ints, const int* tb, int nb,
-                                               int ht, int h, long long* rprof = nullptr) {
+// caps[J] of every row must be in ints + b 2 kRcMaxJ; the inventory rows are
+// loaded here (xrow[J] filled in for the argmax) together with the
+// normalisers, so the whole operand fetch is one round trip
+__device__ inline void half_recheck_fast_batch(const DevModel& P, const int* xloc, double* lo, int* ints,
+                                               const int* rinfo, int nb, int ht, int h,
+                                               long long* rprof = nullptr) {
   long long t0 = rprof ? clock64() : 0;
   auto mark = [&](int k) {
     if (rprof) { const long long n = clock64(); rprof[k] += n - t0; t0 = n; }
@@ -253,19 +261,20 @@ __device__ inline void half_recheck_fast_batch(const DevModel& P, double* lo, in
   int* rb = ints + kRcBatch * 2 * kRcMaxJ;
   for (int idx = ht; idx < nb * in; idx += kRcThreads) {
     const int b = idx / in, j = idx - b * in;
-    const int* caps = ints + b * 2 * kRcMaxJ;
-    const int* xrow = caps + kRcMaxJ;
-    const int t = tb[b];
+    int* caps = ints + b * 2 * kRcMaxJ;
+    int* xrow = caps + kRcMaxJ;
+    const int* ri = rinfo + kRcRowInfo * b;
     double f;
     if (j < J) {
       const int c0 = __ldg(P.pcap0 + j);
       f = c0 > 0 ? __ddiv_rn((double)caps[j], (double)c0) : 0.0;
     } else if (j < 2 * J) {
-      const int x0 = __ldg(P.pinv0 + (size_t)P.product[t] * J + (j - J));
-      f = x0 > 0 ? __ddiv_rn((double)xrow[j - J], (double)x0) : 0.0;
+      const int x = xloc[(size_t)ri[2] * J + (j - J)];
+      const int x0 = __ldg(P.pinv0 + (size_t)ri[1] * J + (j - J));
+      xrow[j - J] = x;
+      f = x0 > 0 ? __ddiv_rn((double)x, (double)x0) : 0.0;
     } else {
-      const int ot = P.order_t ? P.order_t[t] : t;
-      f = P.horizon > 0 ? __ddiv_rn((double)ot, (double)P.horizon) : 0.0;
+      f = P.horizon > 0 ? __ddiv_rn((double)ri[4], (double)P.horizon) : 0.0;
     }
     lo[b * kRcRow + j] = f;
   }
@@ -367,7 +376,7 @@ __device__ inline void half_recheck_fast_batch(const DevModel& P, double* lo, in
     if (b < nb) {
       const int* caps = ints + b * 2 * kRcMaxJ;
       const int* xrow = caps + kRcMaxJ;
-      const double* rw = P.rtab + (size_t)P.rrow[tb[b]] * J;
+      const double* rw = P.rtab + (size_t)rinfo[kRcRowInfo * b + 3] * J;
       const double* ps = lo + b * kRcRow + kTcH;
       double b1v = -INFINITY, b2v = -INFINITY;
       int bi = -1;

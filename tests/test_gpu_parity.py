@@ -561,3 +561,49 @@ def test_derived_guard_bounds_the_observed_score_error(J, I, T, M, scale, shrink
     assert r.actions.tolist() == fp64.actions.tolist()
     print(f"J={J} scale={scale} shrink={shrink}: B={B:.3e} observed max {t['tc_max_score_err']:.3e} "
           f"(B / observed = {B / t['tc_max_score_err']:.0f})")
+
+
+@pytest.mark.parametrize("shape", ["positive_w1", "positive_all", "heavy_tail", "large_bias", "sparse"])
+def test_derived_guard_holds_for_adversarial_weights(shape):
+    """Weight structures built to make the tensor-core errors large and
+    aligned (all-positive layers: every fp32 truncation goes the same way;
+    heavy tails; large biases; sparse rows): the observed max |score error|
+    in verify mode stays below the a-priori bound B, no accepted decision
+    differs from the FP64 engine, and policies whose guard would be too
+    large keep the FP64 path."""
+    J, I, T, M = 30, 200, 12000, 256
+    ons, inst, owner, _, _ = _dual_case(J, I, T, M, "product")
+    rng = np.random.default_rng({"positive_w1": 1, "positive_all": 2, "heavy_tail": 3, "large_bias": 4,
+                                 "sparse": 5}[shape])
+    p = P.MlpParams.seeded_uniform(2 * J + 1, 2 * J, 5)
+    if shape == "positive_w1":
+        p.w1 = np.abs(p.w1)
+    elif shape == "positive_all":
+        p.w1, p.w2, p.w3 = np.abs(p.w1), np.abs(p.w2), np.abs(p.w3)
+    elif shape == "heavy_tail":
+        for name in ("w1", "w2", "w3"):
+            a = getattr(p, name)
+            setattr(p, name, a * np.minimum(rng.pareto(1.5, a.shape) + 1.0, 20.0) / 3.0)
+    elif shape == "large_bias":
+        p.b1 = p.b1 * 30.0
+        p.b2 = p.b2 * 30.0
+        p.b3 = p.b3 * 10.0
+    else:
+        for name in ("w1", "w2", "w3"):
+            a = getattr(p, name)
+            setattr(p, name, np.where(rng.random(a.shape) < 0.8, 0.0, a * 3.0))
+    pol = P.DualNetworkPolicy(p, None, None, inst.horizon, J)
+    B, guard = P.tc_error_bound(inst, pol)
+    fp64 = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(engine="product_fp64"))
+    r = P.picard_simulate(inst, pol, P.PartitionPlan(M, owner), P.PicardConfig(engine="product", tc_verify=True))
+    t = r.timing
+    assert r.actions.tolist() == fp64.actions.tolist()
+    assert t["tc_unflagged_bad"] == 0
+    if guard > 0:
+        assert t["tc_used"] == 1
+        assert t["tc_max_score_err"] <= B, (t["tc_max_score_err"], B)
+        print(f"{shape}: B={B:.3e} guard={guard:.3e} observed={t['tc_max_score_err']:.3e} "
+              f"flagged={t['tc_flagged'] / max(t['tc_rows'], 1):.2%}")
+    else:
+        assert t["tc_used"] == 0
+        print(f"{shape}: B={B:.3e}: FP64 path")
