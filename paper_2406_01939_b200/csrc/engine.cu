@@ -301,6 +301,8 @@ struct pcd_handle {
   pcd::DBuf<unsigned char> wtmp;
   // dynamic state
   pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, segtot, scratch, tau;
+  int adv_buf = -1;                      // backup of the last checkpoint advance (deferred check), -1 none
+  int64_t adv_from = 0, adv_to = 0;
   pcd::DBuf<unsigned char> written;
   pcd::DBuf<long long> evals;
   // general closed form (general.cuh): same-product chains of the plan,
@@ -428,13 +430,16 @@ static void build_csr(pcd_handle* h, const int* d_keys, int nkeys, DBuf<int>& st
   CK(cudaStreamSynchronize(h->stream));
 }
 
-static void reset_scalars(pcd_handle* h) {
+// all = false keeps neg_flag: the checkpoint advance's negativity flag stays
+// set on the device until the next scalar read checks it (advance_checkpoint)
+static void reset_scalars(pcd_handle* h, bool all = true) {
   Scalars s{};
   s.first_changed = ~0ull;
   s.err_nonfinite = ~0ull;
   s.err_infeasible = ~0ull;
   *h->h_scal = s;
-  CK(cudaMemcpyAsync(h->scal, h->h_scal, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->scal, h->h_scal, all ? sizeof(Scalars) : offsetof(Scalars, neg_flag),
+                     cudaMemcpyHostToDevice, h->stream));
 }
 
 static void read_scalars(pcd_handle* h) {
@@ -782,11 +787,13 @@ static void launch_general_sweep(pcd_handle* h, int lo, int hi, long long* evals
   CK(cudaGetLastError());
 }
 
+static void check_advance(pcd_handle* h);
+
 static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
                              double guard = 0.0, int verify = 0, int tiles = 0) {
   IterOut out;
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
-  reset_scalars(h);
+  reset_scalars(h, false);
   if (W <= 0) return out;
   PhaseTimer tm(h->stream);
   if (engine == PCD_ENGINE_GENERAL) {
@@ -807,7 +814,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     const int wpb = 8;  // warps (products) per block
     const int pgrid = (h->I + wpb - 1) / wpb;
     const int nb = build_hck(h, lo, hi);
-    k_tau<<<(J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
+    k_tau<<<(32 * J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
     k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
                                                                  h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
     CK(cudaGetLastError());
@@ -844,6 +851,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     h->timing.kernel_launches += 1;
     // errors surface before publishing (the reference throws out of the sweep)
     read_scalars(h);
+    check_advance(h);
     throw_sweep_error(h);
     tm.start();
     k_publish<<<grid_for(W, 256), 256, 0, h->stream>>>(h->fresh.p, h->cache.p, h->written.p,
@@ -853,6 +861,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     h->timing.kernel_launches += 1;
   }
   read_scalars(h);
+  check_advance(h);  // the previous iteration's checkpoint advance (deferred check)
   throw_sweep_error(h);
   const Scalars& s = *h->h_scal;
   out.changed = (int64_t)s.changed;
@@ -864,34 +873,67 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   return out;
 }
 
-static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to) {
+// advance_checkpoint (engine.hpp:514-526): subtract the stable prefix's
+// fulfilments from the checkpoint; a negative count means an infeasible
+// cached action, for which the reference throws ContractViolation at the
+// first such order. The check is deferred: the flag stays set on the device
+// and is read with the next iteration's scalars (no extra host round trip per
+// iteration); the state before the advance is kept in one of two backup
+// buffers so the serial error search can replay it. defer = false checks now.
+static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to, bool defer = true) {
   if (to <= from) return;
   PhaseTimer tm(h->stream);
   tm.start();
   const size_t IJ = (size_t)h->I * h->J;
-  CK(cudaMemcpyAsync(h->ckbak.p, h->ckinv.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->ckbak.p + IJ, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  const int buf = h->adv_buf < 0 ? 0 : 1 - h->adv_buf;
+  int* bak = h->ckbak.p + (size_t)buf * (IJ + h->J);
+  CK(cudaMemcpyAsync(bak, h->ckinv.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(bak + IJ, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
   k_advance<<<grid_for(to - from, 256), 256, (size_t)h->J * 4, h->stream>>>(
-      h->cache.p, h->product.p, (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p);
-  CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
-  k_advance_check<<<grid_for(std::max<long long>((long long)IJ, to - from), 256), 256, 0, h->stream>>>(
-      h->cache.p, (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p, (long long)IJ, h->scal);
+      h->cache.p, h->product.p, (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p, &h->scal->neg_flag);
   CK(cudaGetLastError());
-  int flag = 0;
-  CK(cudaMemcpyAsync(&flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  h->adv_buf = buf;
+  h->adv_from = from;
+  h->adv_to = to;
   h->timing.advance_ms += tm.stop_ms();
-  h->timing.kernel_launches += 2;
-  if (flag) {
-    CK(cudaMemcpyAsync(h->ckinv.p, h->ckbak.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->ckcap.p, h->ckbak.p + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
-    k_advance_serial<<<1, 1, 0, h->stream>>>(h->cache.p, h->product.p, h->order_t.n ? h->order_t.p : nullptr,
-                                             (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p, h->d_errt);
-    long long et = -1;
-    CK(cudaMemcpyAsync(&et, h->d_errt, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  h->timing.kernel_launches += 1;
+  if (!defer) {
+    CK(cudaMemcpyAsync(&h->h_scal->neg_flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    throw ContractViolation("infeasible fulfillment at t=" + std::to_string(et), et);
+    check_advance(h);
   }
+}
+
+// h_scal->neg_flag was just read from the device: a set flag belongs to the
+// last advance (earlier ones were checked at earlier reads)
+static void check_advance(pcd_handle* h) {
+  if (!h->h_scal->neg_flag) return;
+  if (h->adv_buf < 0) {  // a stale flag of another path (Time Warp checks its own merges)
+    CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
+    h->h_scal->neg_flag = 0;
+    return;
+  }
+  const size_t IJ = (size_t)h->I * h->J;
+  const int* bak = h->ckbak.p + (size_t)h->adv_buf * (IJ + h->J);
+  CK(cudaMemcpyAsync(h->ckinv.p, bak, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->ckcap.p, bak + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
+  k_advance_serial<<<1, 1, 0, h->stream>>>(h->cache.p, h->product.p, h->order_t.n ? h->order_t.p : nullptr,
+                                           (int)h->adv_from, (int)h->adv_to, h->J, h->ckcap.p, h->ckinv.p,
+                                           h->d_errt);
+  long long et = -1;
+  CK(cudaMemcpyAsync(&et, h->d_errt, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->adv_buf = -1;
+  throw ContractViolation("infeasible fulfillment at t=" + std::to_string(et), et);
+}
+
+// the pending advance checked now (before returning or throwing otherwise)
+static void flush_advance_check(pcd_handle* h) {
+  if (h->adv_buf < 0) return;
+  CK(cudaMemcpyAsync(&h->h_scal->neg_flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  check_advance(h);
 }
 
 static int choose_engine(pcd_handle* h, int requested) {
@@ -914,7 +956,7 @@ static void ensure_state_buffers(pcd_handle* h) {
   h->written.alloc(T + 4);  // + 4: the incremental sweep copies whole 4-byte words
   h->ckcap.alloc(std::max(1, h->J));
   h->ckinv.alloc(IJ);
-  h->ckbak.alloc(IJ + h->J);
+  h->ckbak.alloc(2 * (IJ + h->J));  // two backups: the deferred advance check
   h->xloc.alloc(std::max<size_t>(1, (size_t)h->runs * std::max(1, h->J)));
   h->tau.alloc(std::max(1, h->J));
   const size_t nb = (T + kK - 1) / kK + 1;  // + 1: blocks start at lo & ~(K-1)
@@ -959,9 +1001,12 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   }
   std::vector<pcd_trace_row> rows;
   int64_t ws = 0, iteration = 0, episodes = 0;
+  h->adv_buf = -1;
+  CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
   while (ws < T) {
     const int64_t we = cfg->max_steps > 0 ? std::min(T, ws + cfg->max_steps) : T;
     if (iteration >= cap_it) {
+      flush_advance_check(h);  // the reference throws from the advance before reaching the cap
       res->iterations_run = iteration;
       res->trace_rows = (int64_t)rows.size();
       throw IterationLimit("picard iteration cap exceeded (" + std::to_string(cap_it) +
@@ -990,6 +1035,8 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
       ws = it.first_changed;
     }
   }
+  flush_advance_check(h);
+  h->adv_buf = -1;
   CK(cudaEventRecord(e1, h->stream));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -1928,11 +1975,9 @@ extern "C" int pcd_time_warp(pcd_handle* h, int32_t processes, uint64_t seed, in
     {
       CK(cudaMemcpyAsync(h->ckbak.p, h->ckinv.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
       CK(cudaMemcpyAsync(h->ckbak.p + IJ, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
-      k_advance<<<grid_for(hi - t0, 256), 256, (size_t)h->J * 4, h->stream>>>(h->cache.p, h->product.p, lo32, hi32,
-                                                                              h->J, h->ckcap.p, h->ckinv.p);
       CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
-      k_advance_check<<<grid_for(std::max<long long>((long long)IJ, hi - t0), 256), 256, 0, h->stream>>>(
-          h->cache.p, lo32, hi32, h->J, h->ckcap.p, h->ckinv.p, (long long)IJ, h->scal);
+      k_advance<<<grid_for(hi - t0, 256), 256, (size_t)h->J * 4, h->stream>>>(
+          h->cache.p, h->product.p, lo32, hi32, h->J, h->ckcap.p, h->ckinv.p, &h->scal->neg_flag);
       int flag = 0;
       CK(cudaMemcpyAsync(&flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));

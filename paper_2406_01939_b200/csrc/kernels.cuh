@@ -149,25 +149,41 @@ static __global__ void k_effective(const int* __restrict__ qstart, const int* __
 // effective attempt at node j whose index (in window order) is ckcap[j] —
 // the first one that finds the node empty when the cache is replayed from
 // the checkpoint; INT_MAX when the node never empties in the window.
+// Death slot of every node under the frozen cache: one warp per node runs a
+// 32-ary search for the last checkpoint row with H <= ckcap (4 dependent
+// rounds over ~4e4 rows instead of 16 binary-search steps), then scans that
+// row's <= 8-slot block for the effective attempt numbered ckcap.
 static __global__ void k_tau(const int* __restrict__ hck, const int* __restrict__ ev, const int* __restrict__ ckcap,
                              int lo, int hi, int J, int nb, int* __restrict__ tau) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= J) return;
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= J) return;  // warp-uniform
   const int HJ = hck_stride(J), c = ckcap[j], base = hck_base(lo);
-  // last checkpoint row with H <= c (row 0 holds 0)
+  // last checkpoint row with H <= c (row 0 holds 0); H is nondecreasing in the row
   int l = 0, r = nb - 1;
   while (l < r) {
-    const int mid = (l + r + 1) >> 1;
-    if (hck[(size_t)mid * HJ + j] <= c) l = mid; else r = mid - 1;
+    const long long span = r - l;
+    const int pos = l + (int)((span * (lane + 1) + 31) / 32);  // pos(31) == r, pos(0) >= l + 1
+    const unsigned ok = __ballot_sync(0xffffffffu, hck[(size_t)pos * HJ + j] <= c);
+    if (!ok) {
+      r = l + (int)((span + 31) / 32) - 1;
+    } else {
+      const int k = 31 - __clz(ok);  // the ok lanes are a prefix
+      const int lk = l + (int)((span * (k + 1) + 31) / 32);
+      r = k == 31 ? lk : l + (int)((span * (k + 2) + 31) / 32) - 1;
+      l = lk;
+    }
   }
-  int h = hck[(size_t)l * HJ + j], out = 0x7fffffff;
-  const int s1 = min(hi, base + ((l + 1) << kLogK));
-  for (int s = max(lo, base + (l << kLogK)); s < s1; ++s) {
-    if (ev[s] != j) continue;
-    if (h == c) { out = s; break; }
-    ++h;
+  if (lane == 0) {
+    int h = hck[(size_t)l * HJ + j], out = 0x7fffffff;
+    const int s1 = min(hi, base + ((l + 1) << kLogK));
+    for (int s = max(lo, base + (l << kLogK)); s < s1; ++s) {
+      if (ev[s] != j) continue;
+      if (h == c) { out = s; break; }
+      ++h;
+    }
+    tau[j] = out;
   }
-  tau[j] = out;
 }
 
 // Inventory of every run at its first slot in the window (run partitions:
@@ -734,34 +750,33 @@ static __global__ void k_mismatches(const int* __restrict__ cache, const int* __
 
 // Checkpoint advance (engine.hpp:514-526 -> apply_in_place, fo/types.hpp:89-100):
 // subtract the cache prefix's fulfilments from the checkpoint state.
+// The stable prefix's fulfilments subtracted from the checkpoint (capacity by
+// a per-block smem histogram, inventory by atomics). A count that goes
+// negative, or an action >= J, is an infeasible cached action: the atomics
+// return the old values, and a subtraction that crosses zero is seen by the
+// thread (block) that makes it, so the check costs no extra pass over the
+// checkpoint (neg |= 1; the serial search then finds the order).
 static __global__ void k_advance(const int* __restrict__ cache, const int* __restrict__ product, int lo,
-                          int hi, int J, int* __restrict__ ckcap, int* __restrict__ ckinv) {
+                          int hi, int J, int* __restrict__ ckcap, int* __restrict__ ckinv, int* __restrict__ neg) {
   extern __shared__ int hcap[];
   for (int j = threadIdx.x; j < J; j += blockDim.x) hcap[j] = 0;
   __syncthreads();
+  bool bad = false;
   for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
     const int a = cache[t];
     if (a >= 0 && a < J) {
       atomicAdd(&hcap[a], 1);
-      atomicSub(&ckinv[(size_t)product[t] * J + a], 1);
-    }  // a >= J is infeasible: flagged by k_advance_check
+      bad |= atomicSub(&ckinv[(size_t)product[t] * J + a], 1) <= 0;
+    } else if (a >= J) {
+      bad = true;
+    }
   }
   __syncthreads();
   for (int j = threadIdx.x; j < J; j += blockDim.x)
-    if (hcap[j]) atomicSub(&ckcap[j], hcap[j]);
+    if (hcap[j]) bad |= atomicSub(&ckcap[j], hcap[j]) < hcap[j];
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(neg, 1);
 }
 
-static __global__ void k_advance_check(const int* __restrict__ cache, int lo, int hi, int J,
-                                const int* __restrict__ ckcap, const int* __restrict__ ckinv,
-                                long long IJ, Scalars* scal) {
-  int bad = 0;
-  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = tid; i < J; i += stride) bad |= ckcap[i] < 0;
-  for (long long i = tid; i < IJ; i += stride) bad |= ckinv[i] < 0;
-  for (long long t = lo + tid; t < hi; t += stride) bad |= cache[t] >= J;
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&scal->neg_flag, 1);
-}
 
 // Error path only: serial re-application to find the first infeasible order.
 static __global__ void k_advance_serial(const int* __restrict__ cache, const int* __restrict__ product,
