@@ -96,12 +96,34 @@ __device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
 // equal (product, node) attempts of the round comes from __match_any_sync,
 // the running per-node counts live in the warp's smem row.
 // ---------------------------------------------------------------------------
+// First index in [0, n) with a[i] >= key (n if none), by the whole warp: a
+// 32-ary search (every lane probes one point per round, a ballot picks the
+// sub-range), ~log32(n) dependent loads instead of log2(n). Warp-uniform call.
+__device__ __forceinline__ int warp_lower_bound(const int* __restrict__ a, int n, int key) {
+  const int lane = threadIdx.x & 31;
+  int l = 0, r = n;  // the answer lies in [l, r]
+  while (l < r) {
+    const long long span = r - l;
+    const int pos = l + (int)(span * lane / 32);  // in [l, r - 1], nondecreasing in the lane
+    const unsigned ge = __ballot_sync(0xffffffffu, a[pos] >= key);
+    if (!ge) {
+      l = l + (int)(span * 31 / 32) + 1;  // beyond the last probe
+    } else {
+      const int k = __ffs(ge) - 1;        // first lane at or above the key (a is sorted)
+      r = l + (int)(span * k / 32);
+      if (k > 0) l = l + (int)(span * (k - 1) / 32) + 1;
+    }
+  }
+  return l;
+}
+
+// [k0, k1): product p's slots inside the window [lo, hi) (warp-uniform call)
 __device__ __forceinline__ void product_window(const int* __restrict__ qstart, const int* __restrict__ qslots, int p,
                                                int lo, int hi, const int*& sl, int& k0, int& k1) {
   const int beg = qstart[p], n = qstart[p + 1] - beg;
   sl = qslots + beg;
-  k0 = lower_bound_i32(sl, n, lo);
-  k1 = k0 + lower_bound_i32(sl + k0, n - k0, hi);
+  k0 = warp_lower_bound(sl, n, lo);
+  k1 = k0 + warp_lower_bound(sl + k0, n - k0, hi);
 }
 
 static __global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
