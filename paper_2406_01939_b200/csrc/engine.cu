@@ -302,6 +302,11 @@ struct pcd_handle {
   // dynamic state
   pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, segtot, scratch, tau;
   int adv_buf = -1;                      // backup of the last checkpoint advance (deferred check), -1 none
+  struct TimedPhase { cudaEvent_t a, b; double* acc; };
+  std::vector<cudaEvent_t> evpool;       // phase-timer events (flush_timers), reused
+  size_t evnext = 0;
+  std::vector<TimedPhase> tlog;          // recorded, not yet resolved phases
+  bool defer_timers = false;
   int64_t adv_from = 0, adv_to = 0;
   pcd::DBuf<unsigned char> written;
   pcd::DBuf<long long> evals;
@@ -362,6 +367,8 @@ struct pcd_handle {
     return m;
   }
   ~pcd_handle() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     comm.reset();
     if (scal) cudaFree(scal);
     if (h_scal) cudaFreeHost(h_scal);
@@ -453,21 +460,45 @@ struct IterOut {
 };
 
 // Events used for the per-phase device timing (pcd_timing).
-struct PhaseTimer {
-  cudaEvent_t a = nullptr, b = nullptr;
-  cudaStream_t s;
-  explicit PhaseTimer(cudaStream_t st) : s(st) {
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
+// Phase timers: an event pair per phase, resolved into the pcd_timing field
+// when the stream is synchronised anyway (flush_timers) -- inside simulate()
+// the timers are deferred to its end, so timing a phase costs no host
+// round trip (outside, each phase is resolved at once).
+static cudaEvent_t timer_event(pcd_handle* h) {
+  if (h->evnext == h->evpool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->evpool.push_back(e);
   }
-  ~PhaseTimer() { cudaEventDestroy(a); cudaEventDestroy(b); }
-  void start() { cudaEventRecord(a, s); }
-  double stop_ms() {
-    cudaEventRecord(b, s);
-    cudaEventSynchronize(b);
+  return h->evpool[h->evnext++];
+}
+static void flush_timers(pcd_handle* h) {
+  if (h->tlog.empty()) {
+    h->evnext = 0;
+    return;
+  }
+  CK(cudaEventSynchronize(h->tlog.back().b));
+  for (const auto& t : h->tlog) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, a, b);
-    return ms;
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    *t.acc += ms;
+  }
+  h->tlog.clear();
+  h->evnext = 0;
+}
+struct PhaseTimer {
+  pcd_handle* h;
+  cudaEvent_t a = nullptr;
+  explicit PhaseTimer(pcd_handle* hh) : h(hh) {}
+  void start() {
+    a = timer_event(h);
+    CK(cudaEventRecord(a, h->stream));
+  }
+  void stop(double* acc) {
+    cudaEvent_t b = timer_event(h);
+    CK(cudaEventRecord(b, h->stream));
+    h->tlog.push_back({a, b, acc});
+    if (!h->defer_timers) flush_timers(h);
   }
 };
 
@@ -795,17 +826,17 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
   reset_scalars(h, false);
   if (W <= 0) return out;
-  PhaseTimer tm(h->stream);
+  PhaseTimer tm(h);
   if (engine == PCD_ENGINE_GENERAL) {
     tm.start();
     build_hck(h, lo, hi);
     build_gen_lists(h, lo, hi);
-    h->timing.prep_ms += tm.stop_ms();
+    tm.stop(&h->timing.prep_ms);
     tm.start();
     dispatch_kind(h->kind, [&](auto k) { launch_general_sweep<decltype(k)::value>(h, lo, hi, evals_out); });
     exchange(h, h->cache.p, true, lo, hi);  // N>1: owned window slots + convergence scalars
     if (h->comm) CK(cudaMemsetAsync(h->written.p + lo, 1, (size_t)W, h->stream));
-    h->timing.sweep_ms += tm.stop_ms();
+    tm.stop(&h->timing.sweep_ms);
     h->timing.kernel_launches += 1;
     h->timing.sweep_launches += 1;
   } else if (engine == PCD_ENGINE_PRODUCT || engine == PCD_ENGINE_PRODUCT_FP64) {
@@ -818,7 +849,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
                                                                  h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
     CK(cudaGetLastError());
-    h->timing.prep_ms += tm.stop_ms();
+    tm.stop(&h->timing.prep_ms);
     h->timing.kernel_launches += 2;
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
@@ -832,7 +863,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     exchange(h, h->cache.p, true, lo, hi);  // N>1: owned window slots + convergence scalars
     if (h->comm)  // every window slot is owned by some rank: all written now
       CK(cudaMemsetAsync(h->written.p + lo, 1, (size_t)W, h->stream));
-    h->timing.sweep_ms += tm.stop_ms();
+    tm.stop(&h->timing.sweep_ms);
     h->timing.kernel_launches += 1;
     h->timing.sweep_launches += 1;
   } else {
@@ -846,7 +877,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
       h->comm->all_reduce(h->d_red.p + 7, 1, RedOp::MaxU64, h->stream);
       k_scalars_unpack<<<1, 1, 0, h->stream>>>(h->d_red.p, h->scal);
     }
-    h->timing.sweep_ms += tm.stop_ms();
+    tm.stop(&h->timing.sweep_ms);
     h->timing.sweep_launches += 1;
     h->timing.kernel_launches += 1;
     // errors surface before publishing (the reference throws out of the sweep)
@@ -857,7 +888,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     k_publish<<<grid_for(W, 256), 256, 0, h->stream>>>(h->fresh.p, h->cache.p, h->written.p,
                                                         h->ref.n ? h->ref.p : nullptr, lo, hi, h->scal);
     CK(cudaGetLastError());
-    h->timing.publish_ms += tm.stop_ms();
+    tm.stop(&h->timing.publish_ms);
     h->timing.kernel_launches += 1;
   }
   read_scalars(h);
@@ -882,7 +913,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
 // buffers so the serial error search can replay it. defer = false checks now.
 static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to, bool defer = true) {
   if (to <= from) return;
-  PhaseTimer tm(h->stream);
+  PhaseTimer tm(h);
   tm.start();
   const size_t IJ = (size_t)h->I * h->J;
   const int buf = h->adv_buf < 0 ? 0 : 1 - h->adv_buf;
@@ -895,7 +926,7 @@ static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to, bool def
   h->adv_buf = buf;
   h->adv_from = from;
   h->adv_to = to;
-  h->timing.advance_ms += tm.stop_ms();
+  tm.stop(&h->timing.advance_ms);
   h->timing.kernel_launches += 1;
   if (!defer) {
     CK(cudaMemcpyAsync(&h->h_scal->neg_flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -978,9 +1009,16 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   const int engine = choose_engine(h, cfg->engine);
   if (cfg->tc_kernel < 0 || cfg->tc_kernel > 2) throw InvalidArgument("tc_kernel must be 0, 1 or 2");
   h->tc_kernel_req = cfg->tc_kernel;
+  h->tlog.clear();  // (phases of an earlier call that threw: their fields are reset next)
+  h->evnext = 0;
+  struct DeferTimers {
+    pcd_handle* h;
+    ~DeferTimers() { h->defer_timers = false; }
+  } defer_guard{h};
   h->timing = pcd_timing{};
   h->timing.engine_used = engine;
   h->timing.device = h->device;
+  h->defer_timers = true;
   if (h->tc_stats.n) CK(cudaMemsetAsync(h->tc_stats.p, 0, sizeof(unsigned long long) * kTcStats, h->stream));
   const int64_t cap_it = cfg->max_iterations > 0 ? cfg->max_iterations : 2 * T + 4;
   cudaEvent_t e0, e1;
@@ -1039,6 +1077,8 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   h->adv_buf = -1;
   CK(cudaEventRecord(e1, h->stream));
   CK(cudaEventSynchronize(e1));
+  flush_timers(h);
+  h->defer_timers = false;
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
@@ -1562,13 +1602,16 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
     if (!pol->w1 || !pol->b1 || !pol->w2 || !pol->b2 || !pol->w3 || !pol->b3)
       throw InvalidArgument("dual network: parameters missing");
     const int inw = 2 * h->J + 1, outw = 2 * h->J, H = h->H;
-    DBuf<double> tmp;
+    // staging buffers live until the sync at the end of this block, so the
+    // uploads, transposes and the host-side bound computations below overlap
+    DBuf<double> tmp[3];
+    int nt = 0;
     auto upload_t = [&](const double* src, int rows, int cols, DBuf<double>& dst) {
-      tmp.upload(src, (size_t)rows * cols, s);
+      DBuf<double>& t = tmp[nt++];
+      t.upload(src, (size_t)rows * cols, s);
       dst.alloc((size_t)rows * cols);
-      k_transpose_f64<<<(rows * cols + 255) / 256, 256, 0, s>>>(tmp.p, rows, cols, dst.p);
+      k_transpose_f64<<<(rows * cols + 255) / 256, 256, 0, s>>>(t.p, rows, cols, dst.p);
       CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(s));
     };
     upload_t(pol->w1, H, inw, h->w1t);
     upload_t(pol->w2, H, H, h->w2t);
@@ -1613,6 +1656,7 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
         h->tc_bound = B;
       }
     }
+    CK(cudaStreamSynchronize(s));  // the staging buffers (tmp) are released below
   }
   CK(cudaMalloc(&h->scal, sizeof(Scalars)));
   CK(cudaMallocHost(&h->h_scal, sizeof(Scalars)));
