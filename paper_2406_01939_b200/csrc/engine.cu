@@ -1427,10 +1427,18 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
     }
     return dz;
   };
-  // layer 1 (features: 3 fp32 roundings each)
-  std::vector<double> zeros((size_t)inw, 0.0);
-  const auto dz1 = layer(H, inw, [&](int r, int c) { return pol->w1[(size_t)r * inw + c]; }, F, zeros, 3 * u,
-                         [&](int r) { return pol->b1[r]; }, true);
+  // layer 1 (features: 3 fp32 roundings each), in the operand's column order
+  // (tc_l1_input: the k-steps group the inputs as the MMAs do)
+  const int K1 = tc_k1_needed(J);
+  std::vector<double> Fk((size_t)K1, 0.0), zeros((size_t)K1, 0.0);
+  for (int k = 0; k < K1; ++k) {
+    const int c = tc_l1_input(k, J);
+    Fk[(size_t)k] = c >= 0 ? F[(size_t)c] : 0.0;
+  }
+  const auto dz1 = layer(H, K1, [&](int r, int k) {
+                           const int c = tc_l1_input(k, J);
+                           return c >= 0 ? pol->w1[(size_t)r * inw + c] : 0.0;
+                         }, Fk, zeros, 3 * u, [&](int r) { return pol->b1[r]; }, true);
   std::vector<double> X2((size_t)H, 1.0), dh1((size_t)H);
   for (int n = 0; n < H; ++n) dh1[(size_t)n] = dz1[(size_t)n] + kTanhErr;
   const auto dz2 = layer(H, H, [&](int r, int c) { return pol->w2[(size_t)r * H + c]; }, X2, dh1, 0.0,
@@ -1501,7 +1509,10 @@ static void prepare_tc(pcd_handle* h, const pcd_policy* pol, const int32_t* pcap
   };
   const size_t w2base = 2 * (size_t)kW1Bytes, w3base = w2base + 2 * (size_t)kW2Bytes;
   for (int r = 0; r < kTcH; ++r)
-    for (int k = 0; k < kTcK1; ++k) put(0, kTcH, r, k, k < in ? pol->w1[(size_t)r * in + k] : 0.0);
+    for (int k = 0; k < kTcK1; ++k) {
+      const int c = tc_l1_input(k, J);
+      put(0, kTcH, r, k, c >= 0 ? pol->w1[(size_t)r * in + c] : 0.0);
+    }
   for (int r = 0; r < kTcH; ++r)
     for (int k = 0; k < kTcH; ++k) put(w2base, kTcH, r, k, pol->w2[(size_t)r * kTcH + k]);
   for (int r = 0; r < kTcN3; ++r)
@@ -1642,7 +1653,7 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
       h->pinv0.upload(in->inventory, IJ, s);
     }
     h->p_horizon = pol->horizon >= 0 ? pol->horizon : in->horizon;
-    if (2 * h->J + 1 <= kTcK1 && h->J <= kTcN3 && H == kTcH) {
+    if (tc_k1_needed(h->J) <= kTcK1 && h->J <= kTcN3 && H == kTcH) {
       const int32_t* pc = pol->init_capacity ? pol->init_capacity : in->capacity;
       const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
                                              : in->inventory;
@@ -1677,7 +1688,7 @@ extern "C" int pcd_tc_error_bound(const pcd_instance* in, const pcd_policy* pol,
   *guard = 0.0;
   if (pol->kind != PCD_POLICY_DUAL) return PCD_OK;
   const int J = in->nodes, H = pol->hidden;
-  if (!(2 * J + 1 <= kTcK1 && J <= kTcN3 && H == kTcH)) return PCD_OK;
+  if (!(tc_k1_needed(J) <= kTcK1 && J <= kTcN3 && H == kTcH)) return PCD_OK;
   if (!pol->w1 || !pol->b1 || !pol->w2 || !pol->b2 || !pol->w3 || !pol->b3) throw InvalidArgument("policy weights missing");
   const int32_t* pc = pol->init_capacity ? pol->init_capacity : in->capacity;
   const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory) : in->inventory;

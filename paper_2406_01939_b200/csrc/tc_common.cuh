@@ -44,6 +44,18 @@ constexpr int kWImgBytes = 2 * (kW1Bytes + kW2Bytes + kW3Bytes);
 constexpr int kWImgRows = kWImgBytes / 256;  // TMA view of the image: [kWImgRows][128] fp16
 static_assert(kWImgBytes % 512 == 0 && kWImgRows / 2 <= 256, "two TMA boxes of <= 256 rows");
 
+// layer-1 operand columns: capacities at [0, J), zero padding to RJ = J
+// rounded up to 8 (every capacity 8-column chunk is whole, so a row's
+// capacity slots can take the prefetched checkpoint row, tc_pp.cu), inventory
+// features at [RJ, RJ + J), the time feature at RJ + J
+__host__ __device__ constexpr int tc_rj(int J) { return (J + 7) & ~7; }
+__host__ __device__ constexpr int tc_k1_needed(int J) { return tc_rj(J) + J + 1; }
+// reference input index (MlpParams::forward's order: c/c0, x/x0, t/T) of a
+// layer-1 operand column, or -1 for a zero column
+__host__ __device__ constexpr int tc_l1_input(int k, int J) {
+  return k < J ? k : k < tc_rj(J) ? -1 : k < tc_rj(J) + J ? J + (k - tc_rj(J)) : k == tc_rj(J) + J ? 2 * J : -1;
+}
+
 __host__ __device__ constexpr int canon_off(int R, int r, int k) {
   return (k >> 3) * 16 * R + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
 }

@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
   const int rowo = ro64(rr);
   const int nchunk = (J + 7) >> 3;
   const int ni = (nchunk - 2 * p2 + 3) >> 2;  // node chunks of this warp pair (warp-uniform)
-  const bool xpersist = J >= kTcH && J >= kScratchCols;  // x/x0 columns never overwritten
+  const int XO = tc_rj(J);  // first inventory-feature column (capacity chunks are whole)
+  const bool xpersist = XO >= kTcH && XO >= kScratchCols;  // x/x0 columns never overwritten
 
   // ---------------------------------------------------------------- setup
   {
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
         for (int k = 0; k < 8; ++k) {
           const int d = (int)(dv[k] & dmask) + (int)((dpk >> (4 * k)) & 15u) - 1;
           dv[k] = (uint32_t)d;
-          const int cc = max(capv[k] - (int)hv[i][k] + d - (int)((pk[i] >> (4 * k)) & 15u), 0);
+          const int cc = j0 + k < J ? max(capv[k] - (int)hv[i][k] + d - (int)((pk[i] >> (4 * k)) & 15u), 0) : 0;
           cv[k] = (uint32_t)cc;
           bits |= (cc > 0 ? 1u : 0u) << k;
           fv[k] = (float)cc * inv[k];
@@ -386,23 +387,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
           uint32_t h4[4], l4[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) split2(fv[2 * k], fv[2 * k + 1], h4[k], l4[k]);
-          if (act) {
+          if (act) {  // whole chunk: columns [J, RJ) are zero padding (cc = 0 there)
             const int off = rowo + kc64(j0);
-            if (j0 + 8 <= J) {
-              *(uint4*)(sAh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
-              *(uint4*)(sAh + kAH + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
-            } else {  // last partial chunk: the columns from J on are inventory features
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (j0 + 2 * k + 1 < J) {
-                  *(uint32_t*)(sAh + off + 4 * k) = h4[k];
-                  *(uint32_t*)(sAh + kAH + off + 4 * k) = l4[k];
-                } else if (j0 + 2 * k < J) {
-                  *(uint16_t*)(sAh + off + 4 * k) = (uint16_t)h4[k];
-                  *(uint16_t*)(sAh + kAH + off + 4 * k) = (uint16_t)l4[k];
-                }
-              }
-            }
+            *(uint4*)(sAh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+            *(uint4*)(sAh + kAH + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
           }
         }
       }
@@ -420,16 +408,16 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
           for (int k = 0; k < 8; ++k) {
             if (j0 + k >= J) break;
             const int xj = xr[j0 + k];
-            put_feature(sAh, rowo + kc64(J + j0 + k), (float)xj * __ldg(ix + j0 + k));
+            put_feature(sAh, rowo + kc64(XO + j0 + k), (float)xj * __ldg(ix + j0 + k));
             nb |= (xj > 0 ? 1u : 0u) << (8 * i + k);
           }
         }
         xb = nb;
       } else if (act && ciX >= 0) {
-        put_feature(sAh, rowo + kc64(J + xu), (float)xuv * xui);
+        put_feature(sAh, rowo + kc64(XO + xu), (float)xuv * xui);
         if (xuv <= 0) xb &= ~(1u << (8 * ciX + (xu & 7)));
       }
-      if (act && agent) put_feature(sAh, rowo + kc64(2 * J), (float)inf[RI_OT] * invT);
+      if (act && agent) put_feature(sAh, rowo + kc64(XO + J), (float)inf[RI_OT] * invT);
       fmask = act ? (fmask & xb) : 0u;
       if (p2 == 0) {
         const uint32_t bal = __ballot_sync(0xffffffffu, act) & 0xffffu;
@@ -840,6 +828,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
 
 template <bool PROF, int N3>
 static cudaError_t launch_pp(const TcArgs& a, const CUtensorMap& wmap, int ntiles, cudaStream_t stream) {
+  // layer-1 k-steps for the width class (tc_k1_needed(J) <= tc_rj(N3) + N3 + 1 = 2 N3 + 1)
   constexpr int KS1 = (2 * N3 + 1 + 15) / 16 < kTcK1 / 16 ? (2 * N3 + 1 + 15) / 16 : kTcK1 / 16;
   const size_t smem = pp::Layout::total;
   const cudaError_t e = ensure_dyn_smem((const void*)pp::k_sweep_pp<PROF, N3, KS1>, smem);
