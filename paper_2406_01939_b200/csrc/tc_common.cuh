@@ -13,9 +13,11 @@
 // score_j = r_j - q_j needs only the SUM of the two prices, hence W3'.
 //
 // Exactness: the tensor-core argmax is accepted only when its decision
-// margin (best - second best, and |best| vs the decline score 0) exceeds
-// `guard`; otherwise the row is re-evaluated with the exact FP64 path
-// (bit-identical to the reference). The state of each row is the
+// margins (best - second best >= guard, |best| >= guard_abs vs the decline
+// score 0) clear guards derived a priori from the policy's weights and the
+// measured tcgen05 / MUFU error behaviour (engine.cu tc_error_bound,
+// DESIGN.md §4.3a); otherwise the row is re-evaluated with the exact FP64
+// path (bit-identical to the reference). The state of each row is the
 // run-partition closed form, identical to k_sweep_product.
 #pragma once
 
@@ -256,9 +258,11 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   hi = *(const uint32_t*)&hh;
   lo = *(const uint32_t*)&l;
 }
-// tanh(z) = 1 - 2/(1 + e^{2z}): MUFU ex2 and rcp (each ~1 ulp; ~2e-7
-// absolute; the verify-mode tests bound the end-to-end margin). Weights are
-// finite (tc_scaled_guard), so z is finite and the clamp loses nothing.
+// tanh(z) = 1 - 2/(1 + e^{2z}): MUFU ex2 and rcp; max |tanh_mufu(z) - tanh(z)|
+// over every float is 3.97 * 2^-24 (tools/tanh_mufu_probe.cu), the kTanhErr
+// of the derived guard (engine.cu tc_error_bound). Weights are finite (the
+// tensor-core path is refused otherwise), so z is finite and the clamp at
+// +-9 costs < 2^-24.
 __device__ __forceinline__ float tanh_mufu(float z) {
   z = fminf(fmaxf(z, -9.f), 9.f);
   const float d = 1.f + exp2f_approx(2.8853900817779268f * z);
