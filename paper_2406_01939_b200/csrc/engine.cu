@@ -328,6 +328,7 @@ struct pcd_handle {
   double tc_guard = 0.0;                 // derived guard 2B (1 + 2^-10), tc_error_bound
   double tc_bound = 0.0;                 // B: bound on |score_tc - score_ref|
   double tc_guard_abs = 0.0;             // B (1 + 2^-10): the |best| test
+  pcd::DBuf<float> tc_gnode;             // per best node: [0, kTcN3) margin, [kTcN3, 2 kTcN3) |best| thresholds
   int tc_n3 = 0;                         // layer-3 width class of the ping-pong image (prepare_tc)
   pcd::DBuf<unsigned char> tc_wimg2;
   pcd::DBuf<float> tc_b1, tc_b2, tc_ic0, tc_ix0, tc_rtq;
@@ -660,6 +661,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     };
     a.guard = up(guard > 0 ? guard : h->tc_guard);
     a.guard_abs = up(guard > 0 ? guard : h->tc_guard_abs);
+    a.gnode = guard > 0 ? nullptr : h->tc_gnode.p;  // (an override applies to every node)
   }
   a.verify = verify;
   a.stats = h->tc_stats.p;
@@ -1339,8 +1341,12 @@ static double fast_margin_bound(const pcd_policy* pol, int J, int H, double rmax
 // subtraction v1 - v2. Returns B, or 0 when the tensor-core path must not be
 // used (non-finite weights, operands outside fp16 range, features > 1e4).
 constexpr double kTanhErr = 0x1p-22;  // >= max |tanh_mufu(z) - tanh(z)| over all floats (probe)
+// Per node j (optional outputs): babs[j] >= |score_tc_j - score_ref_j| and
+// rdiff[j] >= max_{i != j} error of s_j - s_i (the margin test's threshold
+// when j is the best node); B = max babs, *bdiff = max rdiff.
 static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, const int32_t* pcap,
-                             const int32_t* pinv, int64_t horizon, int J, int H, double* bdiff) {
+                             const int32_t* pinv, int64_t horizon, int J, int H, double* bdiff,
+                             std::vector<double>* babs = nullptr, std::vector<double>* rdiff = nullptr) {
   *bdiff = 0.0;
   const int inw = 2 * J + 1;
   const double u = 0x1p-24, t36 = 0x1p-36;
@@ -1448,7 +1454,7 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
   const auto dq = layer(J, H, [&](int r, int c) { return pol->w3[(size_t)r * H + c] + pol->w3[(size_t)(J + r) * H + c]; },
                         X2, dh2, 0.0, [&](int) { return 0.0; }, false);
   double B = 0;
-  std::vector<double> own((size_t)J);
+  std::vector<double> own((size_t)J), bj((size_t)J), rj((size_t)J, 0.0);
   auto w3s = [&](int j, int l) { return pol->w3[(size_t)j * H + l] + pol->w3[(size_t)(J + j) * H + l]; };
   for (int j = 0; j < J; ++j) {
     double P3 = 0, prop = 0;
@@ -1460,6 +1466,7 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
     // rtabq = fl32(r - b3s), score = fl32(rtabq - q)
     const double ds = dq[(size_t)j] + u * (rmax + b3s) + u * (rmax + b3s + P3) * 1.01;
     own[(size_t)j] = ds - prop;  // everything but the propagated h2 error
+    bj[(size_t)j] = ds;
     B = std::max(B, ds);
   }
   // the margin test compares two scores of the same row: their h2 error is
@@ -1470,7 +1477,10 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
     for (int j = i + 1; j < J; ++j) {
       double a = 0;
       for (int l = 0; l < H; ++l) a += std::fabs(w3s(i, l) - w3s(j, l)) * dh2[(size_t)l];
-      D = std::max(D, a + own[(size_t)i] + own[(size_t)j]);
+      const double dij = a + own[(size_t)i] + own[(size_t)j];
+      D = std::max(D, dij);
+      rj[(size_t)i] = std::max(rj[(size_t)i], dij);
+      rj[(size_t)j] = std::max(rj[(size_t)j], dij);
     }
   // the reference's FP64 scores against exact arithmetic (the same analysis as
   // fast_margin_bound with u = 2^-53 and one ordered chain)
@@ -1480,6 +1490,14 @@ static double tc_error_bound(const pcd_policy* pol, const pcd_instance* in, cons
   if (!(fm > 0)) return 0.0;  // the FP64 scores themselves are not known to 1e-6
   B += fm;
   *bdiff = std::isfinite(D) ? D + 2 * fm : 0.0;
+  if (babs && rdiff) {
+    babs->resize((size_t)J);
+    rdiff->resize((size_t)J);
+    for (int j = 0; j < J; ++j) {
+      (*babs)[(size_t)j] = bj[(size_t)j] + fm;
+      (*rdiff)[(size_t)j] = rj[(size_t)j] + 2 * fm;
+    }
+  }
   return std::isfinite(B) && std::isfinite(D) ? B : 0.0;
 }
 constexpr double kMaxTcGuard = 2e-2;  // beyond this most rows would be re-evaluated: FP64 path
@@ -1658,13 +1676,26 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
       const int32_t* pi = pol->init_capacity ? (pol->init_inventory ? pol->init_inventory : in->inventory)
                                              : in->inventory;
       double Bd = 0;
-      const double B = tc_error_bound(pol, in, pc, pi, h->p_horizon, h->J, H, &Bd);
+      std::vector<double> babs, rdiff;
+      const double B = tc_error_bound(pol, in, pc, pi, h->p_horizon, h->J, H, &Bd, &babs, &rdiff);
       const double g = Bd * (1.0 + 0x1p-10);
       if (B > 0 && g <= kMaxTcGuard) {
         prepare_tc(h.get(), pol, pc, pi, in->reward_table);
         h->tc_guard = g;
         h->tc_guard_abs = B * (1.0 + 0x1p-10);
         h->tc_bound = B;
+        // per-node thresholds (indexed by the best node), as floats rounded up
+        std::vector<float> gt(2 * (size_t)kTcN3, 0.f);
+        auto up = [](double x) {
+          float f = (float)x;
+          if ((double)f < x) f = nextafterf(f, INFINITY);
+          return f;
+        };
+        for (int j = 0; j < h->J; ++j) {
+          gt[(size_t)j] = up(rdiff[(size_t)j] * (1.0 + 0x1p-10));
+          gt[(size_t)kTcN3 + j] = up(babs[(size_t)j] * (1.0 + 0x1p-10));
+        }
+        h->tc_gnode.upload(gt.data(), gt.size(), s);
       }
     }
     CK(cudaStreamSynchronize(s));  // the staging buffers (tmp) are released below

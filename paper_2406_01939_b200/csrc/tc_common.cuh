@@ -75,6 +75,7 @@ struct TcArgs {
   const float* rtabq;   // [R*J] rewards minus the combined output bias b3[:J] + b3[J:], in fp32
   float guard;          // decision margin (best - second) below which a row is re-evaluated
   float guard_abs;      // |best| (vs the decline score 0) below which a row is re-evaluated
+  const float* gnode;   // or per best node j: [j] margin and [kTcN3 + j] |best| thresholds (<= the above)
   int verify;           // debug: exact re-evaluation of every row
   long long* prof;      // debug: per-phase clock64 totals of CTA 0 (or nullptr)
   unsigned long long* stats;  // [0] tc rows, [1] flagged, [2] flagged & tc wrong,

@@ -69,7 +69,8 @@ struct Layout {
   static constexpr int cap = best + kTcRows * 4 * 3 * 4;     // checkpoint capacities [112]
   static constexpr int ctl = cap + kScrJ * 4;                // 2 x kCtl
   static constexpr int cst = ctl + 2 * kCtl * 4;             // invc0[112] b1[64] b2[64] b3[112]
-  static constexpr int cnt = cst + 352 * 4;                  // per-row counters
+  static constexpr int gnode = cst + 352 * 4;                // per-node guards: margin [112], |best| [112]
+  static constexpr int cnt = gnode + 2 * kTcN3 * 4;          // per-row counters
   static constexpr int prof = cnt + CN_COUNT * kTcRows * 4;  // debug phase clocks [20]
   static constexpr int bar = prof + 20 * 8;                  // one mbarrier per half + the weight load's
   static constexpr int tmem = bar + 32;
@@ -173,6 +174,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     sB1[i] = a.b1f[i];
     sB2[i] = a.b2f[i];
   }
+  float* sGn = (float*)(smem + Layout::gnode);
+  for (int i = tid; i < 2 * kTcN3; i += kBlock)
+    sGn[i] = a.gnode ? a.gnode[i] : (i < kTcN3 ? a.guard : a.guard_abs);
   const int nq = a.wctl[0], dealt = (int)gridDim.x * kTcRows;
   auto begin_proc = [&](int* inf, int m) {
     int pos = 0, end = 0;
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
         } else {
           inf[RI_ANY] = 1;
           inf[RI_DEC] = v1 >= 0.f ? i1 : -1;
-          const bool flag = bad || i1 < 0 || !(v1 - v2 >= a.guard) || !(fabsf(v1) >= a.guard_abs);
+          const bool flag = bad || i1 < 0 || !(v1 - v2 >= sGn[i1]) || !(fabsf(v1) >= sGn[kTcN3 + i1]);
           if (!flag) sCnt[CN_TC * kTcRows + R] += 1;  // (flagged rows: when re-evaluated)
           if (flag || a.verify) {
             inf[RI_FLAG] = flag ? 1 : 2;
