@@ -184,6 +184,8 @@ typedef struct pcd_timing {
   double tc_guard;        /* best-minus-second margin guard the sweep used */
   double tc_score_bound;  /* B: derived bound on |score_tc - score_ref| (0: no tensor-core path) */
   double tc_max_score_err;/* tc_verify only: largest observed |score_tc - score_exact| (<= B) */
+  int64_t tc_speculated;  /* rows within the guard decided speculatively and verified after the sweep */
+  int64_t tc_spec_reruns; /* iterations re-run because a speculated decision was wrong */
 } pcd_timing;
 
 typedef struct pcd_handle pcd_handle;
@@ -429,7 +431,11 @@ enum { PCD_DEBUG_TC_PROFILE = 1, /* per-phase clock64 totals of the tensor-core
                                     sweep's CTA 0, printed to stderr per launch */
        PCD_DEBUG_TC_FUSED = 2,    /* entry points without a pcd_config (pcd_iterate_once,
                                     pcd_sequential) use the fused-layer-1 sweep ... */
-       PCD_DEBUG_TC_INC = 4 };    /* ... or the incremental-layer-1 sweep (tests) */
+       PCD_DEBUG_TC_INC = 4,      /* ... or the incremental-layer-1 sweep (tests) */
+       PCD_DEBUG_NO_SPEC = 8,     /* no speculative decisions (every row within the
+                                    guard re-evaluated in the sweep, as in verify mode) */
+       PCD_DEBUG_SPEC_RERUN = 16 }; /* treat every speculated decision as wrong: the
+                                    iteration is re-run without speculation (tests) */
 int pcd_set_debug(pcd_handle* h, int32_t flags);
 
 /* The device checkpoint FoState (capacity[J], dense inventory[I*J]): the

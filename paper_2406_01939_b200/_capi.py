@@ -89,7 +89,8 @@ class pcd_timing(C.Structure):
                 ("tc_flagged", C.c_int64), ("tc_disagree", C.c_int64), ("tc_unflagged_bad", C.c_int64),
                 ("tc_used", C.c_int32), ("tc_tiles", C.c_int32),
                 ("tc_kernel", C.c_int32), ("tc_inc_iters", C.c_int32),
-                ("tc_guard", C.c_double), ("tc_score_bound", C.c_double), ("tc_max_score_err", C.c_double)]
+                ("tc_guard", C.c_double), ("tc_score_bound", C.c_double), ("tc_max_score_err", C.c_double),
+                ("tc_speculated", C.c_int64), ("tc_spec_reruns", C.c_int64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/picard_b200.h

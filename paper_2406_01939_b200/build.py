@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           f"-I{os.path.join(ROOT, 'include')}"]
 
-SOURCES = ["engine.cu", "tc_pp.cu", "tc_inc.cu", "linear.cu", "host_inputs.cpp", "capi.cpp"]
+SOURCES = ["engine.cu", "tc_pp.cu", "tc_inc.cu", "tc_spec.cu", "linear.cu", "host_inputs.cpp", "capi.cpp"]
 
 
 def _stale() -> bool:

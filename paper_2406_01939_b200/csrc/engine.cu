@@ -32,7 +32,9 @@
 
 namespace pcd {
 
-cudaError_t launch_tc_pp(const TcArgs& a, const CUtensorMap& wmap, int ntiles, cudaStream_t stream);  // tc_pp.cu (two 64-row halves)
+cudaError_t launch_tc_pp(const TcArgs& a, const CUtensorMap& wmap, int ntiles, cudaStream_t stream);
+cudaError_t launch_spec_verify(const SweepArgs& S, const int* q, const int* qn, int cap, int force_bad,
+                               cudaStream_t stream);  // tc_spec.cu  // tc_pp.cu (two 64-row halves)
 cudaError_t launch_tc_inc(const IncArgs& a, const CUtensorMap& gmap, int ntiles, cudaStream_t stream);  // tc_inc.cu
 cudaError_t launch_inc_prep(const IncPrep& p, cudaStream_t stream);  // tc_inc.cu: G rows + node transitions
 int tc_pp_width_class(int J);  // tc_pp.cu: layer-3 width class of the ping-pong sweep for J nodes
@@ -329,6 +331,8 @@ struct pcd_handle {
   double tc_bound = 0.0;                 // B: bound on |score_tc - score_ref|
   double tc_guard_abs = 0.0;             // B (1 + 2^-10): the |best| test
   pcd::DBuf<float> tc_gnode;             // per best node: [0, kTcN3) margin, [kTcN3, 2 kTcN3) |best| thresholds
+  pcd::DBuf<int> spec_q, spec_n, cbak;   // speculation queue (tc_spec.cu) and the window's cache backup
+  pcd::DBuf<unsigned char> wbak;         // ... and written flags backup
   int tc_n3 = 0;                         // layer-3 width class of the ping-pong image (prepare_tc)
   pcd::DBuf<unsigned char> tc_wimg2;
   pcd::DBuf<float> tc_b1, tc_b2, tc_ic0, tc_ix0, tc_rtq;
@@ -620,8 +624,17 @@ static void ensure_gmap(pcd_handle* h, size_t rows) {
 
 // One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
 static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify,
-                      int tiles_req = 0) {
+                      int tiles_req = 0, bool spec = false) {
   TcArgs a{};
+  if (spec) {
+    a.spec = 1;
+    a.spec_cap = (int)std::min<int64_t>((int64_t)(hi - lo), 1 << 20);
+    h->spec_q.alloc((size_t)a.spec_cap * kSpecStride);
+    h->spec_n.alloc(1);
+    CK(cudaMemsetAsync(h->spec_n.p, 0, sizeof(int), h->stream));
+    a.spec_n = h->spec_n.p;
+    a.spec_q = h->spec_q.p;
+  }
   SweepArgs& s = a.s;
   s.model = h->model();
   s.M = h->M; s.J = h->J; s.lo = lo; s.hi = hi;
@@ -682,6 +695,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   if (req == 2 && !inc_fits)
     throw InvalidArgument("tc_kernel=incremental does not apply (Time Warp window, J > 104 or window load >= 32000)");
   if (inc_fits && req != 1 && (req == 2 || kIncDefault)) {
+    a.spec = 0;  // (the incremental sweep re-evaluates every row within the guard itself)
     const int nb = hck_rows(lo, hi);
     ensure_gmap(h, (size_t)nb);
     IncPrep pr{};
@@ -701,6 +715,11 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   } else {
     CK(launch_tc_pp(a, h->wmap, tiles, h->stream));
     h->timing.tc_kernel = 1;
+    if (a.spec) {  // the speculated decisions checked against the reference policy
+      CK(launch_spec_verify(a.s, a.spec_q, a.spec_n, a.spec_cap, (h->debug & PCD_DEBUG_SPEC_RERUN) ? 1 : 0,
+                            h->stream));
+      h->timing.kernel_launches += 1;
+    }
   }
   if (prof) {
     long long v[20];
@@ -825,6 +844,7 @@ static void check_advance(pcd_handle* h);
 static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
                              double guard = 0.0, int verify = 0, int tiles = 0) {
   IterOut out;
+  bool spec = false;  // the tensor-core sweep speculated (tc_spec.cu)
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
   reset_scalars(h, false);
   if (W <= 0) return out;
@@ -856,7 +876,19 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     tm.start();
     const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {
-      launch_tc(h, lo, hi, evals_out, guard, verify, tiles);
+      // speculation (tc_spec.cu) needs the derived per-node guards and a
+      // single rank; the window's cache / written flags are backed up for the
+      // re-run a wrong speculated decision triggers
+      spec = !(h->debug & PCD_DEBUG_NO_SPEC) && !verify && !(guard > 0) && !h->nocache && !h->comm &&
+             h->tc_gnode.n > 0;
+      if (spec) {
+        h->cbak.alloc((size_t)W);
+        h->wbak.alloc((size_t)W);
+        CK(cudaMemcpyAsync(h->cbak.p, h->cache.p + lo, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->wbak.p, h->written.p + lo, (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->stream));
+      }
+      launch_tc(h, lo, hi, evals_out, guard, verify, tiles, spec);
       h->timing.tc_used = 1;
       h->timing.tc_tiles = h->tc_tiles;
     } else {
@@ -895,6 +927,27 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   }
   read_scalars(h);
   check_advance(h);  // the previous iteration's checkpoint advance (deferred check)
+  if (spec && h->h_scal->spec_bad) {
+    // a speculated decision differs from the reference policy: the iteration
+    // again from the backed-up window without speculation (every row within
+    // the guard re-evaluated in the sweep)
+    PhaseTimer tm(h);
+    tm.start();
+    const int W = (int)(hi64 - lo64);
+    CK(cudaMemcpyAsync(h->cache.p + lo64, h->cbak.p, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->written.p + lo64, h->wbak.p, (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
+    const int J = h->J, wpb = 8, pgrid = (h->I + wpb - 1) / wpb;
+    k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, (int)lo64,
+                                                                 (int)hi64, h->ev.p, h->rid.p, h->tau.p, h->ckinv.p, J,
+                                                                 h->xloc.p);
+    reset_scalars(h, false);
+    CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->stream));
+    launch_tc(h, (int)lo64, (int)hi64, evals_out, guard, verify, tiles, false);
+    tm.stop(&h->timing.sweep_ms);
+    h->timing.tc_spec_reruns += 1;
+    h->timing.kernel_launches += 2;
+    read_scalars(h);
+  }
   throw_sweep_error(h);
   const Scalars& s = *h->h_scal;
   out.changed = (int64_t)s.changed;
@@ -1095,6 +1148,7 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
     h->timing.tc_disagree = (int64_t)st[2];
     h->timing.tc_unflagged_bad = (int64_t)st[3];
     h->timing.tc_max_score_err = (double)__uint_as_float_host((uint32_t)st[4]);
+    h->timing.tc_speculated = (int64_t)st[5];
   }
   h->timing.tc_guard = cfg->tc_guard > 0 ? cfg->tc_guard : h->tc_guard;
   h->timing.tc_score_bound = h->tc_bound;

@@ -73,7 +73,7 @@ struct Scalars {
   unsigned long long err_nonfinite;  // min over (m << 32 | t)
   unsigned long long err_infeasible; // min over (m << 32 | t)
   int neg_flag;
-  int pad;
+  int spec_bad;                      // a speculated tensor-core decision was wrong (tc_spec.cu)
   long long mismatches;              // full-cache mismatch count (init kernel)
 };
 

@@ -30,7 +30,11 @@
 namespace pcd {
 
 constexpr int kTcRows = 128;
-constexpr int kTcStats = 5;  // TcArgs::stats entries
+constexpr int kTcStats = 6;  // TcArgs::stats entries
+// speculation queue entry: [0] t, [1] pos, [2] first window pos, [3] end pos
+// (indices into pslots), [4] process, [5] run, [6] product, [7] reward row,
+// [8] order time, [9] the speculated decision
+constexpr int kSpecStride = 12;
 constexpr int kTcK1 = 208;     // 2J+1 <= 208 (J <= 103)
 constexpr int kTcH = 64;
 constexpr int kTcN3 = 112;     // J <= 112
@@ -77,11 +81,20 @@ struct TcArgs {
   float guard_abs;      // |best| (vs the decline score 0) below which a row is re-evaluated
   const float* gnode;   // or per best node j: [j] margin and [kTcN3 + j] |best| thresholds (<= the above)
   int verify;           // debug: exact re-evaluation of every row
+  // speculation: a row whose margins lie between 1/16 of the guards and the
+  // guards takes the tensor-core decision at once and is queued for the
+  // post-sweep verification (tc_spec.cu); rows below 1/16 are re-evaluated
+  // in the sweep. spec == 0: every row within the guard is re-evaluated there.
+  int spec;
+  int spec_cap;         // entries of spec_q
+  int* spec_n;          // queued entries (atomic)
+  int* spec_q;          // [spec_cap][kSpecStride]
   long long* prof;      // debug: per-phase clock64 totals of CTA 0 (or nullptr)
   unsigned long long* stats;  // [0] tc rows, [1] flagged, [2] flagged & tc wrong,
                               // [3] (verify) unflagged & tc wrong -- must stay 0,
                               // [4] (verify) max |score_tc - score_exact| over
-                              //     feasible nodes of re-evaluated rows (float bits)
+                              //     feasible nodes of re-evaluated rows (float bits),
+                              // [5] speculated rows
 };
 
 // tc_inc.cu: the sweep with layer 1 off the tensor cores (nodes J <= kIncMaxJ)

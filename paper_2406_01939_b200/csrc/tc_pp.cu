@@ -49,9 +49,10 @@ enum {
   RI_X, RI_M, RI_DRESET,
   RI_UEV, RI_UOLD, RI_UWR, RI_UREF, RI_UPN, RI_URRN, RI_UOTN, RI_UTNN, RI_UXN,
   RI_WAIT,   // steps this row's current slot has waited for its FP64 re-evaluation
-  RI_PAUSE   // the slot's re-evaluation is deferred: redo the step, no update
+  RI_PAUSE,  // the slot's re-evaluation is deferred: redo the step, no update
+  RI_POS0    // the process's first window position (speculation entries)
 };
-static_assert(RI_PAUSE < kInfo, "per-row state fits");
+static_assert(RI_POS0 < kInfo, "per-row state fits");
 // Flagged rows wait (redoing their step, which is deterministic: same slot,
 // same state) until kRcBatch of them are pending in the half, one has waited
 // kMaxWait steps, or they are at least half of the active rows; then the
@@ -59,7 +60,7 @@ static_assert(RI_PAUSE < kInfo, "per-row state fits");
 constexpr int kMaxWait = 3;
 enum { CN_CHANGED = 0, CN_CONFLICTS, CN_FIRST, CN_MISM, CN_NEV, CN_TC, CN_COUNT };
 // per-half control block: [0] active rows, [1] flagged rows, [2..66) flagged rows
-enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, CT_MAXERR = CT_QACT + 4, CT_MAXWAIT, kCtl = 80 };
+enum { CT_FLAG = 66, CT_DIS, CT_BAD, CT_QACT, CT_MAXERR = CT_QACT + 4, CT_MAXWAIT, CT_SPEC, kCtl = 80 };
 
 struct Layout {
   static constexpr int w = 0;
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     }
     inf[RI_M] = m;
     inf[RI_POS] = pos;
+    inf[RI_POS0] = pos;
     inf[RI_END] = end;
     inf[RI_XDIRTY] = 1;
     inf[RI_XUPD] = -1;
@@ -601,7 +603,31 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
         } else {
           inf[RI_ANY] = 1;
           inf[RI_DEC] = v1 >= 0.f ? i1 : -1;
-          const bool flag = bad || i1 < 0 || !(v1 - v2 >= sGn[i1]) || !(fabsf(v1) >= sGn[kTcN3 + i1]);
+          bool flag = bad || i1 < 0;
+          if (!flag) {
+            const float gd = sGn[i1], ga = sGn[kTcN3 + i1], mg = v1 - v2, av = fabsf(v1);
+            if (!(mg >= gd) || !(av >= ga)) {  // within the guard: speculate or re-evaluate here
+              flag = true;
+              if (a.spec && mg >= gd * 0.0625f && av >= ga * 0.0625f) {
+                const int qi = atomicAdd(a.spec_n, 1);
+                if (qi < a.spec_cap) {  // (a full queue falls back to the re-evaluation here)
+                  int* e = a.spec_q + (size_t)qi * kSpecStride;
+                  e[0] = inf[RI_T];
+                  e[1] = inf[RI_POS];
+                  e[2] = inf[RI_POS0];
+                  e[3] = inf[RI_END];
+                  e[4] = inf[RI_M];
+                  e[5] = inf[RI_X];
+                  e[6] = inf[RI_P];
+                  e[7] = inf[RI_RR];
+                  e[8] = inf[RI_OT];
+                  e[9] = inf[RI_DEC];
+                  flag = false;
+                  atomicAdd(&ctl[CT_SPEC], 1);
+                }
+              }
+            }
+          }
           if (!flag) sCnt[CN_TC * kTcRows + R] += 1;  // (flagged rows: when re-evaluated)
           if (flag || a.verify) {
             inf[RI_FLAG] = flag ? 1 : 2;
@@ -818,6 +844,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
       if (c[CT_DIS]) atomicAdd(&a.stats[2], (unsigned long long)(unsigned)c[CT_DIS]);
       if (c[CT_BAD]) atomicAdd(&a.stats[3], (unsigned long long)(unsigned)c[CT_BAD]);
       if (c[CT_MAXERR]) atomicMax(&a.stats[4], (unsigned long long)(unsigned)c[CT_MAXERR]);
+      if (c[CT_SPEC]) atomicAdd(&a.stats[5], (unsigned long long)(unsigned)c[CT_SPEC]);
     }
   }
   tc_fence_before();

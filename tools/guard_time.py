@@ -25,4 +25,4 @@ with P.Simulator(inst, pol) as sim:
             print(f"guard={tm['tc_guard']:.3g} it={r.iterations_to_converged} total={1e3*(time.time()-t0):.1f}ms "
                   f"device={tm['total_ms']:.1f} sweep={tm['sweep_ms']:.1f} prep={tm['prep_ms']:.1f} "
                   f"rows={tm['tc_rows']} flagged={tm['tc_flagged']} ({100*tm['tc_flagged']/max(tm['tc_rows'],1):.3f}%) "
-                  f"tc_wrong_flagged={tm['tc_disagree']}", flush=True)
+                  f"tc_wrong_flagged={tm['tc_disagree']} spec={tm.get('tc_speculated')} reruns={tm.get('tc_spec_reruns')}", flush=True)
