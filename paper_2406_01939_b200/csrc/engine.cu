@@ -880,7 +880,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
       // single rank; the window's cache / written flags are backed up for the
       // re-run a wrong speculated decision triggers
       spec = !(h->debug & PCD_DEBUG_NO_SPEC) && !verify && !(guard > 0) && !h->nocache && !h->comm &&
-             h->tc_gnode.n > 0;
+             h->tc_gnode.n > 0 && h->J % 2 == 0;  // (the verification's paired loads)
       if (spec) {
         h->cbak.alloc((size_t)W);
         h->wbak.alloc((size_t)W);

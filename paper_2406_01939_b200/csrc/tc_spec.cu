@@ -29,13 +29,14 @@ namespace spec {
 constexpr int kWarps = 8;
 
 // shared memory: the FP64 weights (w1t [in][H] | w2t [H][H] | w3s [H][J] | b1 |
-// b2 | b3s [J]) then per warp: caps[J] | row[J] (ints), f[in] | h1[H] | h2[H] |
-// pr[out] (the ordered fallback's prices)
+// b2 | b3s [J]; J even, so every row of w3s starts 16-byte aligned) then per
+// warp: caps[J] | row[J] (ints), f[in, padded to even] | h1[H] | h2[H] | pr[out]
+// (the ordered fallback's prices)
 __host__ __device__ inline size_t weights_doubles(int J, int in, int H) {
   return (size_t)in * H + (size_t)H * H + (size_t)H * J + 2 * (size_t)H + J;
 }
 __host__ __device__ inline size_t warp_bytes(int J, int in, int H, int out) {
-  return (((size_t)2 * J * 4 + 15) & ~(size_t)15) + (size_t)(in + 2 * H + out) * 8;
+  return (((size_t)2 * J * 4 + 15) & ~(size_t)15) + (size_t)(((in + 1) & ~1) + 2 * H + out) * 8;
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, const int* __restrict__ q,
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, con
   int* crow = (int*)wb;
   int* prow = crow + J;
   double* f = (double*)(wb + (((size_t)2 * J * 4 + 15) & ~(size_t)15));
-  double* h1 = f + in;
+  double* h1 = f + ((in + 1) & ~1);  // (16-byte aligned pairs)
   double* h2 = h1 + H;
   const int base = hck_base(S.lo), HJ = hck_stride(J);
   for (int e = blockIdx.x * nw + warp; e < n; e += gridDim.x * nw) {
@@ -146,71 +147,80 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, con
     } else {
       // ---- order-free FP64 forward from shared memory (the in-sweep fast path's
       // arithmetic and certificate: margins above fast_margin decide exactly)
-      // (H == 64: two outputs per lane; each output's sum split over four
-      // partial chains so the dependent FMAs overlap — the certificate holds
-      // for any summation order, fast_margin_bound)
+      // (H == 64: lane l owns outputs 2l and 2l + 1, read as one 16-byte
+      // shared-memory word; inputs in pairs on two chains — the certificate
+      // holds for any summation order, fast_margin_bound)
       {
-        double a[4] = {b1[lane], 0.0, 0.0, 0.0}, d[4] = {b1[lane + 32], 0.0, 0.0, 0.0};
+        const int o = 2 * lane;
+        double2 ae = *(const double2*)(b1 + o), ao = make_double2(0.0, 0.0);
         int c = 0;
-        for (; c + 4 <= in; c += 4) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double fc = f[c + k];
-            a[k] = fma(w1[(size_t)(c + k) * H + lane], fc, a[k]);
-            d[k] = fma(w1[(size_t)(c + k) * H + lane + 32], fc, d[k]);
-          }
+        for (; c + 2 <= in; c += 2) {
+          const double2 fc = *(const double2*)(f + c);
+          const double2 we = *(const double2*)(w1 + (size_t)c * H + o);
+          const double2 wo = *(const double2*)(w1 + (size_t)(c + 1) * H + o);
+          ae.x = fma(we.x, fc.x, ae.x);
+          ae.y = fma(we.y, fc.x, ae.y);
+          ao.x = fma(wo.x, fc.y, ao.x);
+          ao.y = fma(wo.y, fc.y, ao.y);
         }
-        for (; c < in; ++c) {
+        if (c < in) {
           const double fc = f[c];
-          a[0] = fma(w1[(size_t)c * H + lane], fc, a[0]);
-          d[0] = fma(w1[(size_t)c * H + lane + 32], fc, d[0]);
+          const double2 we = *(const double2*)(w1 + (size_t)c * H + o);
+          ae.x = fma(we.x, fc, ae.x);
+          ae.y = fma(we.y, fc, ae.y);
         }
-        h1[lane] = gt_tanh((a[0] + a[1]) + (a[2] + a[3]), P.tanh_fma);
-        h1[lane + 32] = gt_tanh((d[0] + d[1]) + (d[2] + d[3]), P.tanh_fma);
+        *(double2*)(h1 + o) = make_double2(gt_tanh(ae.x + ao.x, P.tanh_fma), gt_tanh(ae.y + ao.y, P.tanh_fma));
       }
       __syncwarp();
       {
-        double a[2] = {b2[lane], 0.0}, d[2] = {b2[lane + 32], 0.0};
+        const int o = 2 * lane;
+        double2 ae = *(const double2*)(b2 + o), ao = make_double2(0.0, 0.0);
         for (int c = 0; c < H; c += 2) {
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const double hc = h1[c + k];
-            a[k] = fma(w2[(size_t)(c + k) * H + lane], hc, a[k]);
-            d[k] = fma(w2[(size_t)(c + k) * H + lane + 32], hc, d[k]);
-          }
+          const double2 hc = *(const double2*)(h1 + c);
+          const double2 we = *(const double2*)(w2 + (size_t)c * H + o);
+          const double2 wo = *(const double2*)(w2 + (size_t)(c + 1) * H + o);
+          ae.x = fma(we.x, hc.x, ae.x);
+          ae.y = fma(we.y, hc.x, ae.y);
+          ao.x = fma(wo.x, hc.y, ao.x);
+          ao.y = fma(wo.y, hc.y, ao.y);
         }
-        h2[lane] = gt_tanh(a[0] + a[1], P.tanh_fma);
-        h2[lane + 32] = gt_tanh(d[0] + d[1], P.tanh_fma);
+        *(double2*)(h2 + o) = make_double2(gt_tanh(ae.x + ao.x, P.tanh_fma), gt_tanh(ae.y + ao.y, P.tanh_fma));
       }
       __syncwarp();
       const double* rw = P.rtab + (size_t)rr * J;
       double b1v = -INFINITY, b2v = -INFINITY;
       int bi = -1;
       bool bad = false;
-      double zq[4], zr[4];
+      // layer 3: lane l owns nodes 2l, 2l + 1 and 64 + 2l, 65 + 2l (J even:
+      // 16-byte aligned pairs in the [H][J] rows)
+      double2 za = make_double2(0.0, 0.0), zb = make_double2(0.0, 0.0);
+      const int ja = 2 * lane, jb = 64 + 2 * lane;
+      const bool va = ja < J, vb = jb < J;
+      if (va) za = make_double2(b3s[ja], b3s[ja + 1]);
+      if (vb) zb = make_double2(b3s[jb], b3s[jb + 1]);
+      for (int l = 0; l < H; ++l) {
+        const double hl = h2[l];
+        const double* wr = w3 + (size_t)l * J;
+        if (va) {
+          const double2 w = *(const double2*)(wr + ja);
+          za.x = fma(w.x, hl, za.x);
+          za.y = fma(w.y, hl, za.y);
+        }
+        if (vb) {
+          const double2 w = *(const double2*)(wr + jb);
+          zb.x = fma(w.x, hl, zb.x);
+          zb.y = fma(w.y, hl, zb.y);
+        }
+      }
+      const double zq[4] = {za.x, za.y, zb.x, zb.y};
+      const int jq[4] = {ja, ja + 1, jb, jb + 1};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        zq[u] = lane + 32 * u < J ? b3s[lane + 32 * u] : 0.0;
-        zr[u] = 0.0;
-      }
-      for (int l = 0; l < H; l += 2) {
-        const double hl = h2[l], hm = h2[l + 1];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (lane + 32 * u < J) {
-            zq[u] = fma(w3[(size_t)l * J + lane + 32 * u], hl, zq[u]);
-            zr[u] = fma(w3[(size_t)(l + 1) * J + lane + 32 * u], hm, zr[u]);
-          }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) zq[u] += zr[u];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = lane + 32 * u;
+        const int j = jq[u];
         if (j >= J || crow[j] <= 0 || prow[j] <= 0) continue;
         const double sc = __ldg(rw + j) - zq[u];
         if (!isfinite(sc)) { bad = true; continue; }
-        if (sc > b1v) { b2v = b1v; b1v = sc; bi = j; }
+        if (sc > b1v || (sc == b1v && j < bi)) { b2v = b1v; b1v = sc; bi = j; }
         else if (sc > b2v) b2v = sc;
       }
 #pragma unroll
