@@ -371,9 +371,22 @@ struct pcd_handle {
     m.fast_margin = fast_margin;
     return m;
   }
+  // auxiliary stream: the tensor-core sweep's work list and the speculation
+  // backups are built on it while the cache kernels run on `stream`
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool wl_ready = false;  // the work list of the coming sweep is already built (build_worklist)
+  // pinned host destination of the actions (pcd_simulate): the committed
+  // prefix streams out on `aux` while later iterations run
+  int32_t* dl_out = nullptr;
+  int64_t dl_done = 0;  // slots [0, dl_done) are queued for download
   ~pcd_handle() {
     if (stream) cudaStreamSynchronize(stream);
+    if (aux) cudaStreamSynchronize(aux);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (aux) cudaStreamDestroy(aux);
     comm.reset();
     if (scal) cudaFree(scal);
     if (h_scal) cudaFreeHost(h_scal);
@@ -622,6 +635,27 @@ static void ensure_gmap(pcd_handle* h, size_t rows) {
   h->gmap_rows = cap;
 }
 
+// Work list of a tensor-core sweep over [lo, hi): this rank's processes with
+// window slots, heaviest first; the first tiles*128 entries are dealt round
+// robin over the tiles, the rest are pulled by rows as they finish (wctl[1]
+// = next entry)
+static void build_worklist(pcd_handle* h, int lo, int hi, cudaStream_t st) {
+  const int M = h->M;
+  h->wload.alloc(M); h->wids.alloc(M); h->wload_s.alloc(M); h->wq.alloc(M); h->wctl.alloc(2);
+  CK(cudaMemsetAsync(h->wctl.p, 0, 2 * sizeof(int), st));
+  k_window_load<<<(M + 255) / 256, 256, 0, st>>>(h->pstart.p, h->pslots.p, M, lo, hi,
+                                                 h->comm ? h->d_mine.p : nullptr, h->wload.p, h->wids.p, h->wctl.p);
+  int bits = 1;
+  while ((1LL << bits) <= (long long)h->max_load) ++bits;
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
+                                               bits, st));
+  h->wtmp.alloc(tb);
+  CK(cub::DeviceRadixSort::SortPairsDescending(h->wtmp.p, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
+                                               bits, st));
+  h->timing.kernel_launches += 2;
+}
+
 // One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
 static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify,
                       int tiles_req = 0, bool spec = false) {
@@ -643,26 +677,8 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   s.nocache = h->nocache;
   s.cache = h->cache.p; s.written = h->written.p; s.ref = h->ref.n ? h->ref.p : nullptr;
   s.scal = h->scal; s.evals_out = evals_out;
-  // work list: this rank's processes with window slots, heaviest first; the
-  // first tiles*128 entries are dealt round robin over the tiles, the rest
-  // are pulled by rows as they finish (wctl[1] = next entry)
-  {
-    const int M = h->M;
-    h->wload.alloc(M); h->wids.alloc(M); h->wload_s.alloc(M); h->wq.alloc(M); h->wctl.alloc(2);
-    CK(cudaMemsetAsync(h->wctl.p, 0, 2 * sizeof(int), h->stream));
-    k_window_load<<<(M + 255) / 256, 256, 0, h->stream>>>(h->pstart.p, h->pslots.p, M, lo, hi,
-                                                          h->comm ? h->d_mine.p : nullptr, h->wload.p, h->wids.p,
-                                                          h->wctl.p);
-    int bits = 1;
-    while ((1LL << bits) <= (long long)h->max_load) ++bits;
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
-                                                 bits, h->stream));
-    h->wtmp.alloc(tb);
-    CK(cub::DeviceRadixSort::SortPairsDescending(h->wtmp.p, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
-                                                 bits, h->stream));
-    h->timing.kernel_launches += 2;
-  }
+  if (!h->wl_ready) build_worklist(h, lo, hi, h->stream);
+  h->wl_ready = false;
   a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabq = h->tc_rtq.p;
@@ -862,6 +878,30 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     h->timing.kernel_launches += 1;
     h->timing.sweep_launches += 1;
   } else if (engine == PCD_ENGINE_PRODUCT || engine == PCD_ENGINE_PRODUCT_FP64) {
+    const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
+    // speculation (tc_spec.cu) needs the derived per-node guards and a
+    // single rank; the window's cache / written flags are backed up for the
+    // re-run a wrong speculated decision triggers
+    spec = tc && !(h->debug & PCD_DEBUG_NO_SPEC) && !verify && !(guard > 0) && !h->nocache && !h->comm &&
+           h->tc_gnode.n > 0 && h->J % 2 == 0;  // (the verification's paired loads)
+    if (tc) {  // work list and backups on the auxiliary stream, beside the cache kernels
+      if (!h->aux) {
+        CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(h->ev_fork, h->stream));
+      CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+      build_worklist(h, lo, hi, h->aux);
+      if (spec) {
+        h->cbak.alloc((size_t)W);
+        h->wbak.alloc((size_t)W);
+        CK(cudaMemcpyAsync(h->cbak.p, h->cache.p + lo, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->aux));
+        CK(cudaMemcpyAsync(h->wbak.p, h->written.p + lo, (size_t)W, cudaMemcpyDeviceToDevice, h->aux));
+        CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->aux));
+      }
+      CK(cudaEventRecord(h->ev_join, h->aux));
+    }
     tm.start();
     const int J = h->J;
     const int wpb = 8;  // warps (products) per block
@@ -874,20 +914,9 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     tm.stop(&h->timing.prep_ms);
     h->timing.kernel_launches += 2;
     tm.start();
-    const bool tc = engine == PCD_ENGINE_PRODUCT && h->tc_ok && h->kind == kDual;
     if (tc) {
-      // speculation (tc_spec.cu) needs the derived per-node guards and a
-      // single rank; the window's cache / written flags are backed up for the
-      // re-run a wrong speculated decision triggers
-      spec = !(h->debug & PCD_DEBUG_NO_SPEC) && !verify && !(guard > 0) && !h->nocache && !h->comm &&
-             h->tc_gnode.n > 0 && h->J % 2 == 0;  // (the verification's paired loads)
-      if (spec) {
-        h->cbak.alloc((size_t)W);
-        h->wbak.alloc((size_t)W);
-        CK(cudaMemcpyAsync(h->cbak.p, h->cache.p + lo, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->wbak.p, h->written.p + lo, (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
-        CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->stream));
-      }
+      CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+      h->wl_ready = true;
       launch_tc(h, lo, hi, evals_out, guard, verify, tiles, spec);
       h->timing.tc_used = 1;
       h->timing.tc_tiles = h->tc_tiles;
@@ -1126,6 +1155,20 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
     } else if (it.first_changed > ws) {
       advance_checkpoint(h, ws, it.first_changed);
       ws = it.first_changed;
+    }
+    // slots before the checkpoint are final: copy them out beside the next
+    // iterations (batches of >= 1M slots)
+    if (h->dl_out && ws - h->dl_done >= (1 << 20)) {
+      if (!h->aux) {
+        CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(h->ev_fork, h->stream));
+      CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+      CK(cudaMemcpyAsync(h->dl_out + h->dl_done, h->cache.p + h->dl_done, sizeof(int32_t) * (size_t)(ws - h->dl_done),
+                         cudaMemcpyDeviceToHost, h->aux));
+      h->dl_done = ws;
     }
   }
   flush_advance_check(h);
@@ -1895,6 +1938,23 @@ extern "C" int pcd_simulate(pcd_handle* h, const pcd_config* cfg, const int32_t*
   if (!h->have_plan) throw InvalidArgument("no partition plan set (pcd_set_plan)");
   CK(cudaSetDevice(h->device));
   upload_cache_ref(h, initial_cache, reference);
+  // a pinned destination receives the committed prefix during the run
+  struct DlReset {
+    pcd_handle* h;
+    ~DlReset() {
+      if (h->aux) cudaStreamSynchronize(h->aux);
+      h->dl_out = nullptr;
+      h->dl_done = 0;
+    }
+  } dl_guard{h};
+  h->dl_done = 0;
+  h->dl_out = nullptr;
+  if (actions_out && h->T) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, actions_out) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+      h->dl_out = actions_out;
+    cudaGetLastError();
+  }
   try {
     simulate(h, cfg, reference != nullptr, res, trace, trace_cap);
   } catch (const IterationLimit& e) {
@@ -1903,8 +1963,10 @@ extern "C" int pcd_simulate(pcd_handle* h, const pcd_config* cfg, const int32_t*
     res->error_time_step = e.time_step;
     throw;
   }
-  if (actions_out && h->T)
-    CK(cudaMemcpyAsync(actions_out, h->cache.p, (size_t)h->T * 4, cudaMemcpyDeviceToHost, h->stream));
+  const int64_t from = h->dl_out ? h->dl_done : 0;
+  if (actions_out && h->T > from)
+    CK(cudaMemcpyAsync(actions_out + from, h->cache.p + from, (size_t)(h->T - from) * 4, cudaMemcpyDeviceToHost,
+                       h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return PCD_OK;
   PCD_CATCH
