@@ -662,6 +662,11 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   TcArgs a{};
   if (spec) {
     a.spec = 1;
+    // rows below 1/256 of the guards (where every observed tensor-core error
+    // lies: 18 wrong argmaxes at C3, margins < guard/1024) are re-evaluated in
+    // the sweep, the rest speculated (C3: 1/16 -> 1/256 cut the in-sweep
+    // re-evaluations 15x, 98 -> 95.4 ms)
+    a.spec_floor = 1.f / 256.f;
     a.spec_cap = (int)std::min<int64_t>((int64_t)(hi - lo), 1 << 20);
     h->spec_q.alloc((size_t)a.spec_cap * kSpecStride);
     h->spec_n.alloc(1);
@@ -697,8 +702,9 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   // PCD_DEBUG_TC_PROFILE: per-phase clock64 totals of CTA 0, printed to stderr
   const bool prof = (h->debug & PCD_DEBUG_TC_PROFILE) != 0;
   if (prof) {
-    h->tc_prof.alloc(20 + 2 * 4096);  // phase totals + per-step (active rows, cycles) of CTA 0 half 0
-    CK(cudaMemsetAsync(h->tc_prof.p, 0, (20 + 2 * 4096) * sizeof(long long), h->stream));
+    // phase totals + per-step (active rows, cycles) of CTA 0 half 0 + 6 per half
+    h->tc_prof.alloc(20 + 2 * 4096 + 2 * 148 * 6);
+    CK(cudaMemsetAsync(h->tc_prof.p, 0, (20 + 2 * 4096 + 2 * 148 * 6) * sizeof(long long), h->stream));
     a.prof = h->tc_prof.p;
   }
   // tiles < SMs (tests): rows pull processes from the work list mid-iteration
@@ -759,6 +765,22 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     else
     fprintf(stderr, "tcprof steps=%lld F=%lld L1=%lld E1=%lld L2=%lld E2=%lld L3=%lld S=%lld fin=%lld chk=%lld U=%lld\n",
             v[10], v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
+    if (h->timing.tc_kernel == 1) {
+      const int nh = 2 * std::min(148, h->tc_tiles);
+      std::vector<long long> hp((size_t)nh * 6);
+      CK(cudaMemcpy(hp.data(), h->tc_prof.p + 20 + 2 * 4096, hp.size() * 8, cudaMemcpyDeviceToHost));
+      int im = 2;  // (CTA 0 carries the phase clocks: excluded)
+      std::vector<long long> cyc(nh);
+      for (int i = 2; i < nh; ++i) {
+        cyc[i] = hp[6 * i + 1];
+        if (cyc[i] > cyc[im]) im = i;
+      }
+      std::vector<long long> sc = cyc;
+      std::sort(sc.begin(), sc.end());
+      const long long* m = &hp[6 * im];
+      fprintf(stderr, "tchalf max: half %d steps=%lld loop=%lld (%.0f/step) rc_batches=%lld rc_cycles=%lld setup=%lld endwait=%lld | loop cycles median %lld p10 %lld\n",
+              im, m[0], m[1], m[0] ? (double)m[1] / m[0] : 0.0, m[2], m[3], m[4], m[5], sc[nh / 2], sc[nh / 10]);
+    }
     fprintf(stderr, "tcprof F: loads=%lld feat=%lld x=%lld | recheck batches=%lld rows=%lld ordered=%lld feat=%lld L1=%lld L2=%lld L3=%lld score=%lld\n",
             v[12], v[13], v[14], v[11] & 0xfffff, (v[11] >> 20) & 0xfffff, v[11] >> 40, v[15], v[16], v[17], v[18], v[19]);
   }

@@ -81,11 +81,12 @@ struct TcArgs {
   float guard_abs;      // |best| (vs the decline score 0) below which a row is re-evaluated
   const float* gnode;   // or per best node j: [j] margin and [kTcN3 + j] |best| thresholds (<= the above)
   int verify;           // debug: exact re-evaluation of every row
-  // speculation: a row whose margins lie between 1/16 of the guards and the
-  // guards takes the tensor-core decision at once and is queued for the
-  // post-sweep verification (tc_spec.cu); rows below 1/16 are re-evaluated
+  // speculation: a row whose margins lie between spec_floor (1/256) of the
+  // guards and the guards takes the tensor-core decision at once and is queued
+  // for the post-sweep verification (tc_spec.cu); rows below are re-evaluated
   // in the sweep. spec == 0: every row within the guard is re-evaluated there.
   int spec;
+  float spec_floor;     // speculate above this fraction of the guards
   int spec_cap;         // entries of spec_q
   int* spec_n;          // queued entries (atomic)
   int* spec_q;          // [spec_cap][kSpecStride]

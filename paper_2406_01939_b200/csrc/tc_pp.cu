@@ -129,6 +129,7 @@ constexpr int kScratchCols = ((kRcScratchHi > kRcScratchLo ? kRcScratchHi : kRcS
 template <bool PROF, int N3, int KS1>
 __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_constant__ CUtensorMap wmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
+  const long long hk0 = PROF ? clock64() : 0;  // (debug) per-half timeline
   const SweepArgs& S = a.s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int J = S.J, lo = S.lo, hi = S.hi;
@@ -260,6 +261,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
   if (PROF && tid == 0)
     for (int k = 0; k < 20; ++k) pacc[k] = 0;
   long long plast = PROF ? clock64() : 0;
+  const long long hl0 = plast;
+  long long hsteps = 0, hrcb = 0, hrcc = 0;
   const bool prof_on = PROF && blockIdx.x == 0 && tid == 0;
 #define PMARK(k) do { if (PROF && prof_on) { const long long now_ = clock64(); pacc[k] += now_ - plast; plast = now_; } } while (0)
 
@@ -452,6 +455,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
     PMARK(0);
     if (ctl[0] == 0) break;
     if (PROF && prof_on) pacc[10] += 1;
+    if (PROF) hsteps += 1;
 
     // ============================ layer 1: z1 = F . W1^T (three products)
     if (ht == 0 && !wready) {
@@ -608,7 +612,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
             const float gd = sGn[i1], ga = sGn[kTcN3 + i1], mg = v1 - v2, av = fabsf(v1);
             if (!(mg >= gd) || !(av >= ga)) {  // within the guard: speculate or re-evaluate here
               flag = true;
-              if (a.spec && mg >= gd * 0.0625f && av >= ga * 0.0625f) {
+              if (a.spec && mg >= gd * a.spec_floor && av >= ga * a.spec_floor) {
                 const int qi = atomicAdd(a.spec_n, 1);
                 if (qi < a.spec_cap) {  // (a full queue falls back to the re-evaluation here)
                   int* e = a.spec_q + (size_t)qi * kSpecStride;
@@ -651,6 +655,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
       inf[RI_PAUSE] = 1;
       inf[RI_WAIT] += 1;
     }
+    const long long hrc0 = PROF ? clock64() : 0;
     if (rc_run) {
       int* rints = (int*)(sAh + kRcInts);
       int* rres = rints + rc::kRcBatch * 2 * kScrJ;
@@ -755,6 +760,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
       bar_half(h);
     }
     PMARK(8);
+    if (PROF && rc_run) {
+      hrcb += (nflag + rc::kRcBatch - 1) / rc::kRcBatch;
+      hrcc += clock64() - hrc0;
+    }
 
     // ============================ U: update + publish (row agents)
     if (agent) {
@@ -822,9 +831,19 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
   }
 
   // ---------------------------------------------------------------- teardown
+  const long long hl1 = PROF ? clock64() : 0;
   __syncthreads();
   if (PROF && prof_on)
     for (int k = 0; k < 20; ++k) a.prof[k] = pacc[k];
+  if (PROF && ht == 0) {  // per half: steps, loop cycles, re-evaluation batches / cycles, setup, end wait
+    long long* hp = a.prof + 20 + 2 * 4096 + (size_t)(2 * blockIdx.x + h) * 6;
+    hp[0] = hsteps;
+    hp[1] = hl1 - hl0;
+    hp[2] = hrcb;
+    hp[3] = hrcc;
+    hp[4] = hl0 - hk0;
+    hp[5] = clock64() - hl1;
+  }
 #undef PMARK
   if (agent) {
     const int* cn = sCnt + R;

@@ -1,6 +1,6 @@
 // tc_spec.cu — verification of the tensor-core sweep's speculated decisions.
 //
-// A row whose decision margins lie between 1/16 of the derived guards and the
+// A row whose decision margins lie between 1/256 of the derived guards and the
 // guards (tc_pp.cu, combine) takes the tensor-core argmax at once and appends
 // its slot to a queue instead of stalling its half for an FP64
 // re-evaluation. After the sweep this kernel re-derives, for every queued

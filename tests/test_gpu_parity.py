@@ -496,8 +496,9 @@ def test_tensor_core_guard_scales_with_policy(scale, shrink, tc):
         if runs[key][2] is not None:
             assert runs[key][2]["tc_used"] == tc
             assert runs[key][2]["tc_unflagged_bad"] == 0
-    if tc:
-        assert runs[("product", False)][2]["tc_flagged"] > 0
+    if tc:  # rows within the guard: re-evaluated in the sweep or speculated and verified after it
+        t = runs[("product", False)][2]
+        assert t["tc_flagged"] + t["tc_speculated"] > 0
 
 
 def test_cpp_dropin_matches_reference_engine():
