@@ -434,8 +434,10 @@ enum { PCD_DEBUG_TC_PROFILE = 1, /* per-phase clock64 totals of the tensor-core
        PCD_DEBUG_TC_INC = 4,      /* ... or the incremental-layer-1 sweep (tests) */
        PCD_DEBUG_NO_SPEC = 8,     /* no speculative decisions (every row within the
                                     guard re-evaluated in the sweep, as in verify mode) */
-       PCD_DEBUG_SPEC_RERUN = 16 }; /* treat every speculated decision as wrong: the
+       PCD_DEBUG_SPEC_RERUN = 16, /* treat every speculated decision as wrong: the
                                     iteration is re-run without speculation (tests) */
+       PCD_DEBUG_SPEC_FLIP = 32 }; /* publish a wrong decision for every 4th speculated
+                                    slot: the verification must detect it and re-run (tests) */
 int pcd_set_debug(pcd_handle* h, int32_t flags);
 
 /* The device checkpoint FoState (capacity[J], dense inventory[I*J]): the

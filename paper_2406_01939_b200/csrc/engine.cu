@@ -667,6 +667,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
     // the sweep, the rest speculated (C3: 1/16 -> 1/256 cut the in-sweep
     // re-evaluations 15x, 98 -> 95.4 ms)
     a.spec_floor = 1.f / 256.f;
+    a.spec_flip = (h->debug & PCD_DEBUG_SPEC_FLIP) ? 1 : 0;
     a.spec_cap = (int)std::min<int64_t>((int64_t)(hi - lo), 1 << 20);
     h->spec_q.alloc((size_t)a.spec_cap * kSpecStride);
     h->spec_n.alloc(1);

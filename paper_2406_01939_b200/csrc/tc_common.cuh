@@ -87,6 +87,7 @@ struct TcArgs {
   // in the sweep. spec == 0: every row within the guard is re-evaluated there.
   int spec;
   float spec_floor;     // speculate above this fraction of the guards
+  int spec_flip;        // debug: publish wrong speculated decisions (the verification must catch them)
   int spec_cap;         // entries of spec_q
   int* spec_n;          // queued entries (atomic)
   int* spec_q;          // [spec_cap][kSpecStride]

@@ -625,6 +625,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
                   e[6] = inf[RI_P];
                   e[7] = inf[RI_RR];
                   e[8] = inf[RI_OT];
+                  // (debug, tests) publish a wrong decision for every 4th
+                  // speculated slot: the verification must catch it
+                  if (a.spec_flip && (inf[RI_T] & 3) == 0) inf[RI_DEC] = inf[RI_DEC] >= 0 ? -1 : i1;
                   e[9] = inf[RI_DEC];
                   flag = false;
                   atomicAdd(&ctl[CT_SPEC], 1);

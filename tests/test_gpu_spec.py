@@ -1,11 +1,13 @@
 """Speculative tensor-core decisions (tc_spec.cu): rows whose margins lie
-between 1/16 of the derived guards and the guards take the tensor-core
+between 1/256 of the derived guards and the guards take the tensor-core
 decision at once and are verified against the reference policy after the
 sweep; a wrong one re-runs the iteration without speculation. Results must be
 identical to the non-speculative sweep (PCD_DEBUG_NO_SPEC) -- actions,
 counters, every trace row -- and to the oracle, also when every speculated
 decision is forced to count as wrong (PCD_DEBUG_SPEC_RERUN: every iteration
-with a speculated row is re-run from its backups)."""
+with a speculated row is re-run from its backups), and when every 4th
+speculated decision is published wrong on purpose (PCD_DEBUG_SPEC_FLIP: the
+verification must detect each such iteration and re-run it)."""
 from types import SimpleNamespace as NS
 
 import numpy as np
@@ -17,7 +19,7 @@ from tests.helpers import product_instance
 
 pytestmark = pytest.mark.gpu
 
-NO_SPEC, SPEC_RERUN = 8, 16
+NO_SPEC, SPEC_RERUN, SPEC_FLIP = 8, 16, 32
 
 
 def _case(J, I, T, seed=7, scale=1.0):
@@ -49,11 +51,11 @@ def test_speculation_equals_the_non_speculative_sweep(J, I, T, M, part, window, 
     plan = (P.make_product_chunk_partition(inst, M, 1) if part == "chunk" else P.make_product_partition(inst, M, 1))
     seq, _ = ORC.sequential(ons, opol)
     cfg = P.PicardConfig(max_steps=window, record_trace=True)
-    runs = {f: _run(inst, pol, plan, cfg, f, seq) for f in (0, NO_SPEC, SPEC_RERUN)}
+    runs = {f: _run(inst, pol, plan, cfg, f, seq) for f in (0, NO_SPEC, SPEC_RERUN, SPEC_FLIP)}
     base = runs[NO_SPEC]
     assert base.actions.tolist() == seq.tolist()
     assert base.timing["tc_speculated"] == 0
-    for f in (0, SPEC_RERUN):
+    for f in (0, SPEC_RERUN, SPEC_FLIP):
         r = runs[f]
         assert r.timing["tc_used"] == 1
         assert r.actions.tolist() == seq.tolist()
@@ -66,3 +68,4 @@ def test_speculation_equals_the_non_speculative_sweep(J, I, T, M, part, window, 
     assert spec["tc_speculated"] > 0
     assert spec["tc_spec_reruns"] == 0  # (no wrong speculated decision in these cases)
     assert rerun["tc_spec_reruns"] > 0
+    assert runs[SPEC_FLIP].timing["tc_spec_reruns"] > 0  # the planted wrong decisions were caught
