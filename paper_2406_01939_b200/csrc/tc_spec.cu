@@ -26,17 +26,18 @@
 namespace pcd {
 namespace spec {
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 16;
 
 // shared memory: the FP64 weights (w1t [in][H] | w2t [H][H] | w3s [H][J] | b1 |
 // b2 | b3s [J]; J even, so every row of w3s starts 16-byte aligned) then per
-// warp: caps[J] | row[J] (ints), f[in, padded to even] | h1[H] | h2[H] | pr[out]
-// (the ordered fallback's prices)
+// warp: caps[J] | row[J] (ints), f[max(in, out), padded to even] (the ordered
+// fallback's prices overwrite f once layer 1 has read it) | h1[H] | h2[H]
 __host__ __device__ inline size_t weights_doubles(int J, int in, int H) {
   return (size_t)in * H + (size_t)H * H + (size_t)H * J + 2 * (size_t)H + J;
 }
 __host__ __device__ inline size_t warp_bytes(int J, int in, int H, int out) {
-  return (((size_t)2 * J * 4 + 15) & ~(size_t)15) + (size_t)(((in + 1) & ~1) + 2 * H + out) * 8;
+  const int fo = ((in > out ? in : out) + 1) & ~1;  // f, later the fallback's prices
+  return (((size_t)2 * J * 4 + 15) & ~(size_t)15) + (size_t)(fo + 2 * H) * 8;
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, const int* __restrict__ q,
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, con
   int* crow = (int*)wb;
   int* prow = crow + J;
   double* f = (double*)(wb + (((size_t)2 * J * 4 + 15) & ~(size_t)15));
-  double* h1 = f + ((in + 1) & ~1);  // (16-byte aligned pairs)
+  double* h1 = f + (((in > P.out ? in : P.out) + 1) & ~1);  // (16-byte aligned pairs)
   double* h2 = h1 + H;
   const int base = hck_base(S.lo), HJ = hck_stride(J);
   for (int e = blockIdx.x * nw + warp; e < n; e += gridDim.x * nw) {
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, con
       ws.f = f;
       ws.h1 = h1;
       ws.h2 = h2;
-      ws.pr = h2 + H;
+      ws.pr = f;  // (the prices are written after layer 1 has consumed f)
       int nonfinite = 0;
       exact = warp_policy_eval<kDual>(P, crow, prow, t, ws, lane, &nonfinite);
       if (nonfinite) exact = -2;  // the sweep must report it: re-run without speculation
@@ -257,10 +258,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spec_verify(SweepArgs S, con
 
 }  // namespace spec
 
-// warps per CTA: as many as fit next to the weights (8 at J = 100)
+// warps per CTA: as many as fit next to the weights (12 at J = 100)
 static int spec_warps(int J, int in, int H, int out) {
   const size_t wbytes = spec::weights_doubles(J, in, H) * 8, per = spec::warp_bytes(J, in, H, out);
-  const size_t avail = 232448 > wbytes ? 232448 - wbytes : 0;
+  const size_t cap = 232448 - 64;  // (the static mbarrier)
+  const size_t avail = cap > wbytes ? cap - wbytes : 0;
   return (int)std::min<size_t>((size_t)spec::kWarps, avail / per);
 }
 
