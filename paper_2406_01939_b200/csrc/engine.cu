@@ -299,7 +299,7 @@ struct pcd_handle {
   pcd::DBuf<int> rid;     // run of every slot (run partitions)
   int64_t runs = 0;       // R
   // per-iteration work list of the tensor-core sweep (window load desc)
-  pcd::DBuf<int> wload, wids, wload_s, wq, wctl;  // wctl = {nq, head}
+  pcd::DBuf<int> wload, wids, wload_s, wq, wctl, wbeg;  // wctl = {nq, head}; wbeg: first window position
   pcd::DBuf<unsigned char> wtmp;
   // dynamic state
   pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, segtot, scratch, tau;
@@ -641,10 +641,11 @@ static void ensure_gmap(pcd_handle* h, size_t rows) {
 // = next entry)
 static void build_worklist(pcd_handle* h, int lo, int hi, cudaStream_t st) {
   const int M = h->M;
-  h->wload.alloc(M); h->wids.alloc(M); h->wload_s.alloc(M); h->wq.alloc(M); h->wctl.alloc(2);
+  h->wload.alloc(M); h->wids.alloc(M); h->wload_s.alloc(M); h->wq.alloc(M); h->wctl.alloc(2); h->wbeg.alloc(M);
   CK(cudaMemsetAsync(h->wctl.p, 0, 2 * sizeof(int), st));
   k_window_load<<<(M + 255) / 256, 256, 0, st>>>(h->pstart.p, h->pslots.p, M, lo, hi,
-                                                 h->comm ? h->d_mine.p : nullptr, h->wload.p, h->wids.p, h->wctl.p);
+                                                 h->comm ? h->d_mine.p : nullptr, h->wload.p, h->wids.p, h->wctl.p,
+                                                 h->wbeg.p);
   int bits = 1;
   while ((1LL << bits) <= (long long)h->max_load) ++bits;
   size_t tb = 0;
@@ -685,7 +686,7 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   s.scal = h->scal; s.evals_out = evals_out;
   if (!h->wl_ready) build_worklist(h, lo, hi, h->stream);
   h->wl_ready = false;
-  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
+  a.wq = h->wq.p; a.wctl = h->wctl.p; a.wbeg = h->wbeg.p; a.wlen = h->wload.p; a.wimg2 = h->tc_wimg2.p; a.n3 = h->tc_n3;
   a.b1f = h->tc_b1.p; a.b2f = h->tc_b2.p;
   a.inv_c0 = h->tc_ic0.p; a.inv_x0 = h->tc_ix0.p; a.rtabq = h->tc_rtq.p;
   {  // the guards as floats rounded up, so the kernel's margin tests never undercut them

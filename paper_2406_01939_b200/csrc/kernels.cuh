@@ -395,17 +395,19 @@ static __global__ void k_check_runs(const int* __restrict__ nruns, const int* __
 // tensor-core sweep pull the longest processes first.
 static __global__ void k_window_load(const int* __restrict__ pstart, const int* __restrict__ pslots, int M, int lo,
                                      int hi, const unsigned char* __restrict__ mine, int* __restrict__ load,
-                                     int* __restrict__ ids, int* __restrict__ nq) {
+                                     int* __restrict__ ids, int* __restrict__ nq, int* __restrict__ wbeg) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
-  int n = 0;
+  int n = 0, k0 = 0;
+  const int beg = pstart[m];
   if (!mine || mine[m]) {
-    const int beg = pstart[m], c = pstart[m + 1] - beg;
-    const int k0 = lower_bound_i32(pslots + beg, c, lo);
+    const int c = pstart[m + 1] - beg;
+    k0 = lower_bound_i32(pslots + beg, c, lo);
     n = k0 < c && pslots[beg + k0] < hi ? lower_bound_i32(pslots + beg, c, hi) - k0 : 0;
   }
   load[m] = n;
   ids[m] = m;
+  if (wbeg) wbeg[m] = beg + k0;  // the process's first window position (the sweep's rows start there)
   if (n) atomicAdd(nq, 1);
 }
 

@@ -70,6 +70,8 @@ struct TcArgs {
   SweepArgs s;          // state, publish and counter pointers (as k_sweep_product)
   const int* wq;        // work list: processes with window slots, heaviest first
   int* wctl;            // {entries of wq, next entry beyond the dealt ones}
+  const int* wbeg;      // [M] first window position of each process in pslots (k_window_load)
+  const int* wlen;      // [M] its window slot count
   const unsigned char* wimg2; // kWImgBytes: per layer one 2N-row K-major operand [hi; lo]
   int n3;                     // layer-3 width class (tc_pp_width_class(J))
   const float* b1f;     // [64]

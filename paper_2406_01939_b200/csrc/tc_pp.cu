@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
   const long long hk0 = PROF ? clock64() : 0;  // (debug) per-half timeline
   const SweepArgs& S = a.s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int J = S.J, lo = S.lo, hi = S.hi;
+  const int J = S.J, lo = S.lo;
   const int base = hck_base(lo), HJ = hck_stride(J), RJ = (J + 7) & ~7;
   unsigned char* sW = smem + Layout::w;
   int* sInfo = (int*)(smem + Layout::info);
@@ -182,10 +182,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
   const int nq = a.wctl[0], dealt = (int)gridDim.x * kTcRows;
   auto begin_proc = [&](int* inf, int m) {
     int pos = 0, end = 0;
-    if (m >= 0) {
-      const int beg = S.pstart[m], n = S.pstart[m + 1] - beg;
-      pos = beg + lower_bound_i32(S.pslots + beg, n, lo);
-      end = beg + lower_bound_i32(S.pslots + beg, n, hi);
+    if (m >= 0) {  // (window positions from the work-list build: one round trip)
+      pos = a.wbeg[m];
+      end = pos + a.wlen[m];
     }
     inf[RI_M] = m;
     inf[RI_POS] = pos;
