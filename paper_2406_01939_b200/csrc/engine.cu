@@ -376,6 +376,13 @@ struct pcd_handle {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool wl_ready = false;  // the work list of the coming sweep is already built (build_worklist)
+  // post-sweep verification of speculated decisions running on `aux` while
+  // the host reads the iteration's scalars and launches the checkpoint
+  // advance (simulate: finish_verify); it reads the checkpoint capacities
+  // from a snapshot, as the advance may already be rewriting them
+  bool verify_pending = false;
+  cudaEvent_t ev_sweep = nullptr;
+  pcd::DBuf<int> ckcap_v;
   // pinned host destination of the actions (pcd_simulate): the committed
   // prefix streams out on `aux` while later iterations run
   int32_t* dl_out = nullptr;
@@ -385,6 +392,7 @@ struct pcd_handle {
     if (aux) cudaStreamSynchronize(aux);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_sweep) cudaEventDestroy(ev_sweep);
     if (ev_join) cudaEventDestroy(ev_join);
     if (aux) cudaStreamDestroy(aux);
     comm.reset();
@@ -658,8 +666,16 @@ static void build_worklist(pcd_handle* h, int lo, int hi, cudaStream_t st) {
 }
 
 // One iteration over [lo, hi) on the resident cache. engine: REPLAY/PRODUCT.
+static void ensure_aux(pcd_handle* h) {
+  if (h->aux) return;
+  CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_sweep, cudaEventDisableTiming));
+}
+
 static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify,
-                      int tiles_req = 0, bool spec = false) {
+                      int tiles_req = 0, bool spec = false, bool verify_async = false) {
   TcArgs a{};
   if (spec) {
     a.spec = 1;
@@ -739,7 +755,18 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
   } else {
     CK(launch_tc_pp(a, h->wmap, tiles, h->stream));
     h->timing.tc_kernel = 1;
-    if (a.spec) {  // the speculated decisions checked against the reference policy
+    if (a.spec && verify_async) {  // the speculated decisions checked on `aux` (finish_verify)
+      ensure_aux(h);
+      h->ckcap_v.alloc(std::max(1, h->J));
+      CK(cudaMemcpyAsync(h->ckcap_v.p, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+      CK(cudaEventRecord(h->ev_sweep, h->stream));
+      CK(cudaStreamWaitEvent(h->aux, h->ev_sweep, 0));
+      SweepArgs sv = a.s;
+      sv.ckcap = h->ckcap_v.p;
+      CK(launch_spec_verify(sv, a.spec_q, a.spec_n, a.spec_cap, (h->debug & PCD_DEBUG_SPEC_RERUN) ? 1 : 0, h->aux));
+      h->verify_pending = true;
+      h->timing.kernel_launches += 1;
+    } else if (a.spec) {  // the speculated decisions checked against the reference policy
       CK(launch_spec_verify(a.s, a.spec_q, a.spec_n, a.spec_cap, (h->debug & PCD_DEBUG_SPEC_RERUN) ? 1 : 0,
                             h->stream));
       h->timing.kernel_launches += 1;
@@ -881,8 +908,52 @@ static void launch_general_sweep(pcd_handle* h, int lo, int hi, long long* evals
 
 static void check_advance(pcd_handle* h);
 
+static IterOut iter_out(pcd_handle* h) {
+  IterOut out;
+  const Scalars& s = *h->h_scal;
+  out.changed = (int64_t)s.changed;
+  out.first_changed = s.changed ? (int64_t)s.first_changed : -1;
+  out.conflicts = (int64_t)s.conflicts;
+  out.mismatch_delta = (int64_t)s.mismatch_delta;
+  out.max_evals = (int64_t)s.max_evals;
+  out.total_evals = (int64_t)s.total_evals;
+  return out;
+}
+
+// A speculated decision differs from the reference policy: the iteration
+// again from the backed-up window without speculation (every row within the
+// guard re-evaluated in the sweep); the scalars are read afterwards.
+static void rerun_without_spec(pcd_handle* h, int64_t lo64, int64_t hi64, long long* evals_out, double guard,
+                               int verify, int tiles) {
+  PhaseTimer tm(h);
+  tm.start();
+  const int W = (int)(hi64 - lo64);
+  CK(cudaMemcpyAsync(h->cache.p + lo64, h->cbak.p, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->written.p + lo64, h->wbak.p, (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
+  const int J = h->J, wpb = 8, pgrid = (h->I + wpb - 1) / wpb;
+  k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, (int)lo64,
+                                                               (int)hi64, h->ev.p, h->rid.p, h->tau.p, h->ckinv.p, J,
+                                                               h->xloc.p);
+  reset_scalars(h, false);
+  CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->stream));
+  launch_tc(h, (int)lo64, (int)hi64, evals_out, guard, verify, tiles, false);
+  tm.stop(&h->timing.sweep_ms);
+  h->timing.tc_spec_reruns += 1;
+  h->timing.kernel_launches += 2;
+  read_scalars(h);
+}
+
+// Waits for a deferred verification; true if a speculated decision was wrong.
+static bool finish_verify(pcd_handle* h) {
+  if (!h->verify_pending) return false;
+  h->verify_pending = false;
+  CK(cudaMemcpyAsync(&h->h_scal->spec_bad, &h->scal->spec_bad, sizeof(int), cudaMemcpyDeviceToHost, h->aux));
+  CK(cudaStreamSynchronize(h->aux));
+  return h->h_scal->spec_bad != 0;
+}
+
 static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
-                             double guard = 0.0, int verify = 0, int tiles = 0) {
+                             double guard = 0.0, int verify = 0, int tiles = 0, bool defer_verify = false) {
   IterOut out;
   bool spec = false;  // the tensor-core sweep speculated (tc_spec.cu)
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
@@ -909,11 +980,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     spec = tc && !(h->debug & PCD_DEBUG_NO_SPEC) && !verify && !(guard > 0) && !h->nocache && !h->comm &&
            h->tc_gnode.n > 0 && h->J % 2 == 0;  // (the verification's paired loads)
     if (tc) {  // work list and backups on the auxiliary stream, beside the cache kernels
-      if (!h->aux) {
-        CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-      }
+      ensure_aux(h);
       CK(cudaEventRecord(h->ev_fork, h->stream));
       CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
       build_worklist(h, lo, hi, h->aux);
@@ -941,7 +1008,7 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     if (tc) {
       CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
       h->wl_ready = true;
-      launch_tc(h, lo, hi, evals_out, guard, verify, tiles, spec);
+      launch_tc(h, lo, hi, evals_out, guard, verify, tiles, spec, spec && defer_verify);
       h->timing.tc_used = 1;
       h->timing.tc_tiles = h->tc_tiles;
     } else {
@@ -980,36 +1047,14 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   }
   read_scalars(h);
   check_advance(h);  // the previous iteration's checkpoint advance (deferred check)
-  if (spec && h->h_scal->spec_bad) {
-    // a speculated decision differs from the reference policy: the iteration
-    // again from the backed-up window without speculation (every row within
-    // the guard re-evaluated in the sweep)
-    PhaseTimer tm(h);
-    tm.start();
-    const int W = (int)(hi64 - lo64);
-    CK(cudaMemcpyAsync(h->cache.p + lo64, h->cbak.p, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->written.p + lo64, h->wbak.p, (size_t)W, cudaMemcpyDeviceToDevice, h->stream));
-    const int J = h->J, wpb = 8, pgrid = (h->I + wpb - 1) / wpb;
-    k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, (int)lo64,
-                                                                 (int)hi64, h->ev.p, h->rid.p, h->tau.p, h->ckinv.p, J,
-                                                                 h->xloc.p);
-    reset_scalars(h, false);
-    CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->stream));
-    launch_tc(h, (int)lo64, (int)hi64, evals_out, guard, verify, tiles, false);
-    tm.stop(&h->timing.sweep_ms);
-    h->timing.tc_spec_reruns += 1;
-    h->timing.kernel_launches += 2;
-    read_scalars(h);
+  if (spec && defer_verify && (h->h_scal->err_nonfinite != ~0ull || h->h_scal->err_infeasible != ~0ull)) {
+    // an error on a speculated trajectory counts only once it is verified
+    if (finish_verify(h)) rerun_without_spec(h, lo64, hi64, evals_out, guard, verify, tiles);
+  } else if (spec && !defer_verify && h->h_scal->spec_bad) {
+    rerun_without_spec(h, lo64, hi64, evals_out, guard, verify, tiles);
   }
   throw_sweep_error(h);
-  const Scalars& s = *h->h_scal;
-  out.changed = (int64_t)s.changed;
-  out.first_changed = s.changed ? (int64_t)s.first_changed : -1;
-  out.conflicts = (int64_t)s.conflicts;
-  out.mismatch_delta = (int64_t)s.mismatch_delta;
-  out.max_evals = (int64_t)s.max_evals;
-  out.total_evals = (int64_t)s.total_evals;
-  return out;
+  return iter_out(h);
 }
 
 // advance_checkpoint (engine.hpp:514-526): subtract the stable prefix's
@@ -1068,6 +1113,20 @@ static void check_advance(pcd_handle* h) {
 }
 
 // the pending advance checked now (before returning or throwing otherwise)
+// Takes back the last checkpoint advance (its prefix held a speculated
+// decision that the verification rejected): the state before it, no pending
+// negativity flag.
+static void undo_advance(pcd_handle* h) {
+  if (h->adv_buf < 0) return;
+  const size_t IJ = (size_t)h->I * h->J;
+  const int* bak = h->ckbak.p + (size_t)h->adv_buf * (IJ + h->J);
+  CK(cudaMemcpyAsync(h->ckinv.p, bak, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->ckcap.p, bak + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
+  h->h_scal->neg_flag = 0;
+  h->adv_buf = -1;
+}
+
 static void flush_advance_check(pcd_handle* h) {
   if (h->adv_buf < 0) return;
   CK(cudaMemcpyAsync(&h->h_scal->neg_flag, &h->scal->neg_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -1118,6 +1177,8 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   if (cfg->tc_kernel < 0 || cfg->tc_kernel > 2) throw InvalidArgument("tc_kernel must be 0, 1 or 2");
   h->tc_kernel_req = cfg->tc_kernel;
   h->tlog.clear();  // (phases of an earlier call that threw: their fields are reset next)
+  if (h->aux) CK(cudaStreamSynchronize(h->aux));  // (a verification left by a call that threw)
+  h->verify_pending = false;
   h->evnext = 0;
   struct DeferTimers {
     pcd_handle* h;
@@ -1160,7 +1221,21 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
                            iteration, rows);
     }
     ++iteration;
-    IterOut it = run_iteration(h, engine, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify, cfg->tc_tiles);
+    IterOut it = run_iteration(h, engine, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify, cfg->tc_tiles, true);
+    // the checkpoint advance goes out while a deferred verification of
+    // speculated decisions still runs; a rejected one takes it back and the
+    // iteration is re-run without speculation
+    auto next_ws = [&](const IterOut& o) { return o.changed == 0 ? we : std::max(ws, o.first_changed); };
+    int64_t nws = next_ws(it);
+    if (nws > ws) advance_checkpoint(h, ws, nws);
+    if (finish_verify(h)) {
+      if (nws > ws) undo_advance(h);
+      rerun_without_spec(h, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify, cfg->tc_tiles);
+      throw_sweep_error(h);
+      it = iter_out(h);
+      nws = next_ws(it);
+      if (nws > ws) advance_checkpoint(h, ws, nws);
+    }
     res->iterations_to_converged += 1;
     res->policy_eval_count_sequential_equivalent += it.max_evals;
     res->total_policy_evals += it.total_evals;
@@ -1172,22 +1247,12 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
       CK(cudaMemcpy(h->history + (iteration - 1) * T, h->cache.p, (size_t)T * 4, cudaMemcpyDeviceToHost));
     h->timing.steps_critical += it.max_evals;
     h->timing.total_evals += it.total_evals;
-    if (it.changed == 0) {
-      advance_checkpoint(h, ws, we);
-      ws = we;
-      ++episodes;
-    } else if (it.first_changed > ws) {
-      advance_checkpoint(h, ws, it.first_changed);
-      ws = it.first_changed;
-    }
+    if (it.changed == 0) ++episodes;
+    ws = nws;
     // slots before the checkpoint are final: copy them out beside the next
     // iterations (batches of >= 1M slots)
     if (h->dl_out && ws - h->dl_done >= (1 << 20)) {
-      if (!h->aux) {
-        CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-      }
+      ensure_aux(h);
       CK(cudaEventRecord(h->ev_fork, h->stream));
       CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
       CK(cudaMemcpyAsync(h->dl_out + h->dl_done, h->cache.p + h->dl_done, sizeof(int32_t) * (size_t)(ws - h->dl_done),
