@@ -1,3 +1,7 @@
+"""C3 with debug flag sets (not a test): iterations, speculation re-runs,
+speculated rows, evaluations, and whether the actions equal the first run's.
+  python tools/spec_ab.py 8 0 16     # no speculation, default, forced re-runs
+"""
 import sys; sys.path.insert(0,'.')
 import numpy as np, paper_2406_01939_b200 as P
 inst = P.generate_instance(100, 10000, 10_000_000, 0.0, 0.8, 7)
