@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
             if (i < ni && 8 * (g + 4 * i) < J) ldg256_na_ef(hr + 8 * (g + 4 * i), hv[i], pol);
         }
         if (!xd && my_ci(xu) >= 0) {
-          xuv = __ldcg(S.xloc + (size_t)x * J + xu);  // (L2: the agents' REDs bypass this SM's L1)
+          xuv = S.xloc[(size_t)x * J + xu];
           xui = __ldg(a.inv_x0 + (size_t)p * J + xu);
         }
       }
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_sweep_pp(TcArgs a, const __grid_c
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (j0 + k >= J) break;
-            const int xj = __ldcg(xr + j0 + k);
+            const int xj = xr[j0 + k];
             put_feature(sAh, rowo + kc64(XO + j0 + k), (float)xj * __ldg(ix + j0 + k));
             nb |= (xj > 0 ? 1u : 0u) << (8 * i + k);
           }

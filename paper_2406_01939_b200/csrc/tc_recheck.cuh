@@ -269,7 +269,7 @@ __device__ inline void half_recheck_fast_batch(const DevModel& P, const int* xlo
       const int c0 = __ldg(P.pcap0 + j);
       f = c0 > 0 ? __ddiv_rn((double)caps[j], (double)c0) : 0.0;
     } else if (j < 2 * J) {
-      const int x = __ldcg(xloc + (size_t)ri[2] * J + (j - J));  // (L2: the agents' REDs bypass L1)
+      const int x = xloc[(size_t)ri[2] * J + (j - J)];
       const int x0 = __ldg(P.pinv0 + (size_t)ri[1] * J + (j - J));
       xrow[j - J] = x;
       f = x0 > 0 ? __ddiv_rn((double)x, (double)x0) : 0.0;
