@@ -1800,12 +1800,16 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
   if (in->order_t) h->order_t.upload(in->order_t, T, s);
   h->rrow.upload(in->reward_row, T, s);
   if (in->reward_rows > 0x7fffffffLL) throw InvalidArgument("too many reward rows");
-  {  // per-order range checks (first offending t, product before reward row)
-    const long long bp = first_out_of_range(h.get(), h->product.p, h->T, 0, h->I);
-    const long long br = first_out_of_range(h.get(), h->rrow.p, h->T, 0, (int)h->R);
-    if (bp >= 0 && (br < 0 || bp <= br))
-      throw InvalidArgument("order product out of range at t=" + std::to_string(bp));
-    if (br >= 0) throw InvalidArgument("reward row out of range at t=" + std::to_string(br));
+  // per-order range checks on the device, read back with create's final
+  // synchronisation (nothing below indexes with products or reward rows), so
+  // the uploads overlap the host-side bound computations
+  DBuf<unsigned long long> oor;
+  oor.alloc(2);
+  CK(cudaMemsetAsync(oor.p, 0xff, 2 * sizeof(unsigned long long), s));
+  if (h->T > 0) {
+    k_first_out_of_range<<<grid_for(h->T, 256), 256, 0, s>>>(h->product.p, h->T, 0, h->I, oor.p);
+    k_first_out_of_range<<<grid_for(h->T, 256), 256, 0, s>>>(h->rrow.p, h->T, 0, (int)h->R, oor.p + 1);
+    CK(cudaGetLastError());
   }
   h->rtab.upload(in->reward_table, (size_t)h->R * J, s);
   h->cap0.upload(in->capacity, J, s);
@@ -1890,6 +1894,14 @@ extern "C" int pcd_create(const pcd_instance* in, const pcd_policy* pol, int32_t
   CK(cudaMallocHost(&h->h_scal, sizeof(Scalars)));
   CK(cudaMalloc(&h->d_errt, sizeof(long long)));
   CK(cudaStreamSynchronize(s));
+  {  // the range checks (first offending t, product before reward row)
+    unsigned long long r[2];
+    CK(cudaMemcpy(r, oor.p, sizeof r, cudaMemcpyDeviceToHost));
+    const long long bp = r[0] == ~0ull ? -1 : (long long)r[0], br = r[1] == ~0ull ? -1 : (long long)r[1];
+    if (bp >= 0 && (br < 0 || bp <= br))
+      throw InvalidArgument("order product out of range at t=" + std::to_string(bp));
+    if (br >= 0) throw InvalidArgument("reward row out of range at t=" + std::to_string(br));
+  }
   *out = h.release();
   return PCD_OK;
   PCD_CATCH

@@ -94,6 +94,27 @@ def test_product_engine_is_used_for_product_partitions(golden):
     assert used >= 20
 
 
+def test_create_refuses_out_of_range_orders():
+    """pcd_create checks every order's product and reward row on the device and
+    reports the first offending time step (a product before a reward row at
+    the same step), like the reference's instance validation."""
+    base = P.generate_instance(4, 6, 200, 0.0, 0.8, 3)
+    pol = P.GreedyPolicy()
+
+    def inst(prod, rrow):
+        return P.Instance(base.nodes, base.products, base.horizon, prod, rrow, base.reward_table, base.capacity,
+                          base.inventory)
+    prod, rrow = np.array(base.product), np.array(base.reward_row)
+    p2 = prod.copy(); p2[57] = base.products
+    r2 = rrow.copy(); r2[31] = np.asarray(base.reward_table).shape[0]
+    for pr, rr, msg in ((p2, rrow, "order product out of range at t=57"), (prod, r2, "reward row out of range at t=31"),
+                        (p2, r2, "reward row out of range at t=31")):
+        with pytest.raises(P.InvalidArgument, match=msg):
+            P.Simulator(inst(pr, rr), pol)
+    with P.Simulator(inst(prod, rrow), pol):
+        pass
+
+
 def test_toy_iterate_once_hand_trace(golden):
     # test_engine.cpp:100-138
     toy = P.Instance(2, 1, 2, [0, 0], [0, 1], [[0.9, 0.1], [0.8, 0.2]], [1, 1], [[1, 1]])
