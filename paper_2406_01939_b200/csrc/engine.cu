@@ -376,6 +376,10 @@ struct pcd_handle {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool wl_ready = false;  // the work list of the coming sweep is already built (build_worklist)
+  // per-product window bounds carried across the iterations of simulate
+  // (windows only move forward there; kernels.cuh product_window)
+  pcd::DBuf<int2> qcur;
+  bool qcur_on = false;
   // post-sweep verification of speculated decisions running on `aux` while
   // the host reads the iteration's scalars and launches the checkpoint
   // advance (simulate: finish_verify); it reads the checkpoint capacities
@@ -822,7 +826,8 @@ static int build_hck(pcd_handle* h, int lo, int hi) {
   const int wpb = 8;  // warps (products) per block
   const int pgrid = (h->I + wpb - 1) / wpb;
   k_effective<<<pgrid, wpb * 32, (size_t)wpb * 2 * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi,
-                                                                   h->cache.p, h->ckinv.p, J, h->ev.p);
+                                                                   h->cache.p, h->ckinv.p, J, h->ev.p,
+                                                                   h->qcur_on ? h->qcur.p : nullptr);
   const int nb = hck_rows(lo, hi);
   const int nseg = (nb + kSegRows - 1) / kSegRows;
   const size_t hsm = (size_t)kSegRows * J * 4;
@@ -933,7 +938,7 @@ static void rerun_without_spec(pcd_handle* h, int64_t lo64, int64_t hi64, long l
   const int J = h->J, wpb = 8, pgrid = (h->I + wpb - 1) / wpb;
   k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, (int)lo64,
                                                                (int)hi64, h->ev.p, h->rid.p, h->tau.p, h->ckinv.p, J,
-                                                               h->xloc.p);
+                                                               h->xloc.p, h->qcur_on ? h->qcur.p : nullptr);
   reset_scalars(h, false);
   CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->stream));
   launch_tc(h, (int)lo64, (int)hi64, evals_out, guard, verify, tiles, false);
@@ -1000,7 +1005,8 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     const int nb = build_hck(h, lo, hi);
     k_tau<<<(32 * J + 127) / 128, 128, 0, h->stream>>>(h->hck.p, h->ev.p, h->ckcap.p, lo, hi, J, nb, h->tau.p);
     k_xinit<<<pgrid, wpb * 32, (size_t)(wpb + 1) * J * 4, h->stream>>>(h->qstart.p, h->qslots.p, h->I, lo, hi, h->ev.p,
-                                                                 h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p);
+                                                                 h->rid.p, h->tau.p, h->ckinv.p, J, h->xloc.p,
+                                                                 h->qcur_on ? h->qcur.p : nullptr);
     CK(cudaGetLastError());
     tm.stop(&h->timing.prep_ms);
     h->timing.kernel_launches += 2;
@@ -1179,6 +1185,13 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   h->tlog.clear();  // (phases of an earlier call that threw: their fields are reset next)
   if (h->aux) CK(cudaStreamSynchronize(h->aux));  // (a verification left by a call that threw)
   h->verify_pending = false;
+  struct CursorOff {
+    pcd_handle* h;
+    ~CursorOff() { h->qcur_on = false; }
+  } cursor_guard{h};
+  h->qcur.alloc((size_t)std::max(1, h->I));
+  CK(cudaMemsetAsync(h->qcur.p, 0, sizeof(int2) * (size_t)std::max(1, h->I), h->stream));
+  h->qcur_on = true;
   h->evnext = 0;
   struct DeferTimers {
     pcd_handle* h;

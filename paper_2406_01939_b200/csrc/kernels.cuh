@@ -117,18 +117,47 @@ __device__ __forceinline__ int warp_lower_bound(const int* __restrict__ a, int n
   return l;
 }
 
-// [k0, k1): product p's slots inside the window [lo, hi) (warp-uniform call)
+// first index >= from whose entry is >= key (a sorted; from <= the answer):
+// two 32-wide forward probes, then the 32-ary search of the rest
+__device__ __forceinline__ int warp_advance(const int* __restrict__ a, int n, int from, int key) {
+  const int lane = threadIdx.x & 31;
+  for (int r = 0; r < 2 && from < n; ++r, from += 32) {
+    const int k = from + lane;
+    const unsigned ge = __ballot_sync(0xffffffffu, k < n && a[k] >= key);
+    if (ge) return from + __ffs(ge) - 1;
+  }
+  return from >= n ? n : from + warp_lower_bound(a + from, n - from, key);
+}
+
+// [k0, k1): product p's slots inside the window [lo, hi) (warp-uniform call).
+// cur (or nullptr: 32-ary searches) holds per product the previous window's
+// bounds; inside simulate windows only move forward, so both bounds are
+// found by a short forward scan from them (mode 1 advances and stores them,
+// mode 2 reads this window's, stored by an earlier kernel of the iteration)
 __device__ __forceinline__ void product_window(const int* __restrict__ qstart, const int* __restrict__ qslots, int p,
-                                               int lo, int hi, const int*& sl, int& k0, int& k1) {
+                                               int lo, int hi, const int*& sl, int& k0, int& k1,
+                                               int2* cur = nullptr, int mode = 0) {
   const int beg = qstart[p], n = qstart[p + 1] - beg;
   sl = qslots + beg;
-  k0 = warp_lower_bound(sl, n, lo);
-  k1 = k0 + warp_lower_bound(sl + k0, n - k0, hi);
+  if (cur && mode == 2) {
+    const int2 c = cur[p];
+    k0 = c.x;
+    k1 = c.y;
+  } else if (cur) {
+    const int2 c = cur[p];
+    k0 = warp_advance(sl, n, c.x, lo);
+    k1 = warp_advance(sl, n, max(c.y, k0), hi);
+    if ((threadIdx.x & 31) == 0) cur[p] = make_int2(k0, k1);
+  } else {
+    k0 = warp_lower_bound(sl, n, lo);
+    k1 = k0 + warp_lower_bound(sl + k0, n - k0, hi);
+  }
 }
 
 static __global__ void k_effective(const int* __restrict__ qstart, const int* __restrict__ qslots, int I,
                                    int lo, int hi, const int* __restrict__ cache,
-                                   const int* __restrict__ ckinv, int J, int* __restrict__ ev) {
+                                   const int* __restrict__ ckinv, int J, int* __restrict__ ev,
+                                   int2* __restrict__ qcur = nullptr) {
   extern __shared__ int cnt_smem[];  // per warp: cnt[J], x0[J]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -141,7 +170,7 @@ static __global__ void k_effective(const int* __restrict__ qstart, const int* __
   }
   const int* sl;
   int k0, k1;
-  product_window(qstart, qslots, p, lo, hi, sl, k0, k1);
+  product_window(qstart, qslots, p, lo, hi, sl, k0, k1, qcur, 1);
   const unsigned lt = (1u << lane) - 1u;
   __syncwarp();
   // 64 slots per round, both halves' loads in flight before either is ranked
@@ -219,7 +248,7 @@ static __global__ void k_tau(const int* __restrict__ hck, const int* __restrict_
 static __global__ void k_xinit(const int* __restrict__ qstart, const int* __restrict__ qslots, int I, int lo,
                                int hi, const int* __restrict__ ev, const int* __restrict__ rid,
                                const int* __restrict__ tau, const int* __restrict__ ckinv, int J,
-                               int* __restrict__ xloc) {
+                               int* __restrict__ xloc, int2* __restrict__ qcur = nullptr) {
   extern __shared__ int cnt_smem[];  // tau[J] (block), then cnt[J] per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* stau = cnt_smem;
@@ -231,7 +260,7 @@ static __global__ void k_xinit(const int* __restrict__ qstart, const int* __rest
   for (int j = lane; j < J; j += 32) cnt[j] = 0;
   const int* sl;
   int k0, k1;
-  product_window(qstart, qslots, p, lo, hi, sl, k0, k1);
+  product_window(qstart, qslots, p, lo, hi, sl, k0, k1, qcur, 2);
   const int* x0 = ckinv + (size_t)p * J;
   int prev_run = -1;
   __syncwarp();
