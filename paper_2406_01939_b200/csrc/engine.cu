@@ -303,7 +303,7 @@ struct pcd_handle {
   pcd::DBuf<unsigned char> wtmp;
   // dynamic state
   pcd::DBuf<int> cache, ref, fresh, ev, ckcap, ckinv, ckbak, xloc, hck, seg, segtot, scratch, tau;
-  int adv_buf = -1;                      // backup of the last checkpoint advance (deferred check), -1 none
+  int adv_buf = -1;                      // 0: the last checkpoint advance is not yet checked (deferred), -1 none
   struct TimedPhase { cudaEvent_t a, b; double* acc; };
   std::vector<cudaEvent_t> evpool;       // phase-timer events (flush_timers), reused
   size_t evnext = 0;
@@ -387,6 +387,20 @@ struct pcd_handle {
   bool verify_pending = false;
   cudaEvent_t ev_sweep = nullptr;
   pcd::DBuf<int> ckcap_v;
+  // pipelined verification (simulate): the verification of iteration i runs
+  // on `aux` beside iteration i+1's checkpoint advance and cache kernels,
+  // which write the spare set of the per-iteration buffers the verification
+  // reads (ev, hck, xloc; swapped after each speculated sweep) and back up
+  // the next window into the spare backups; the host waits for the
+  // verdict (h_vbad, ev_vdone) only before iteration i+1's sweep. The work
+  // list and the backups then go on `aux2`, not behind the verification.
+  pcd::DBuf<int> ev2, hck2, xloc2, cbak2;
+  pcd::DBuf<unsigned char> wbak2;
+  cudaStream_t aux2 = nullptr;
+  cudaEvent_t ev_vdone = nullptr;
+  int* h_vbad = nullptr;  // pinned: the verification's verdict
+  bool pipe_verify = false;
+  bool nospec_once = false;  // the next iteration re-runs one whose speculation was rejected
   // pinned host destination of the actions (pcd_simulate): the committed
   // prefix streams out on `aux` while later iterations run
   int32_t* dl_out = nullptr;
@@ -394,7 +408,11 @@ struct pcd_handle {
   ~pcd_handle() {
     if (stream) cudaStreamSynchronize(stream);
     if (aux) cudaStreamSynchronize(aux);
+    if (aux2) cudaStreamSynchronize(aux2);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    if (ev_vdone) cudaEventDestroy(ev_vdone);
+    if (aux2) cudaStreamDestroy(aux2);
+    if (h_vbad) cudaFreeHost(h_vbad);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_sweep) cudaEventDestroy(ev_sweep);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -487,6 +505,7 @@ static void read_scalars(pcd_handle* h) {
 struct IterOut {
   int64_t changed = 0, first_changed = -1, conflicts = 0, mismatch_delta = 0;
   int64_t max_evals = 0, total_evals = 0;
+  bool aborted = false;  // the previous iteration's pipelined verification failed (simulate)
 };
 
 // Events used for the per-phase device timing (pcd_timing).
@@ -676,6 +695,10 @@ static void ensure_aux(pcd_handle* h) {
   CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_sweep, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&h->aux2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&h->ev_vdone, cudaEventDisableTiming));
+  CK(cudaHostAlloc((void**)&h->h_vbad, sizeof(int), cudaHostAllocDefault));
+  *h->h_vbad = 0;
 }
 
 static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, double guard, int verify,
@@ -768,6 +791,11 @@ static void launch_tc(pcd_handle* h, int lo, int hi, long long* evals_out, doubl
       SweepArgs sv = a.s;
       sv.ckcap = h->ckcap_v.p;
       CK(launch_spec_verify(sv, a.spec_q, a.spec_n, a.spec_cap, (h->debug & PCD_DEBUG_SPEC_RERUN) ? 1 : 0, h->aux));
+      // the verdict to pinned memory, the flag cleared for the next
+      // verification (same stream), an event the host waits on
+      CK(cudaMemcpyAsync(h->h_vbad, &h->scal->spec_bad, sizeof(int), cudaMemcpyDeviceToHost, h->aux));
+      CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->aux));
+      CK(cudaEventRecord(h->ev_vdone, h->aux));
       h->verify_pending = true;
       h->timing.kernel_launches += 1;
     } else if (a.spec) {  // the speculated decisions checked against the reference policy
@@ -952,9 +980,8 @@ static void rerun_without_spec(pcd_handle* h, int64_t lo64, int64_t hi64, long l
 static bool finish_verify(pcd_handle* h) {
   if (!h->verify_pending) return false;
   h->verify_pending = false;
-  CK(cudaMemcpyAsync(&h->h_scal->spec_bad, &h->scal->spec_bad, sizeof(int), cudaMemcpyDeviceToHost, h->aux));
-  CK(cudaStreamSynchronize(h->aux));
-  return h->h_scal->spec_bad != 0;
+  CK(cudaEventSynchronize(h->ev_vdone));
+  return *h->h_vbad != 0;
 }
 
 static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi64, long long* evals_out,
@@ -962,6 +989,10 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
   IterOut out;
   bool spec = false;  // the tensor-core sweep speculated (tc_spec.cu)
   const int lo = (int)lo64, hi = (int)hi64, W = hi - lo;
+  if (h->verify_pending && (W <= 0 || engine != PCD_ENGINE_PRODUCT) && finish_verify(h)) {
+    out.aborted = true;  // (a pipelined verification outside the tensor-core path: settled first)
+    return out;
+  }
   reset_scalars(h, false);
   if (W <= 0) return out;
   PhaseTimer tm(h);
@@ -982,21 +1013,23 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     // speculation (tc_spec.cu) needs the derived per-node guards and a
     // single rank; the window's cache / written flags are backed up for the
     // re-run a wrong speculated decision triggers
-    spec = tc && !(h->debug & PCD_DEBUG_NO_SPEC) && !verify && !(guard > 0) && !h->nocache && !h->comm &&
-           h->tc_gnode.n > 0 && h->J % 2 == 0;  // (the verification's paired loads)
-    if (tc) {  // work list and backups on the auxiliary stream, beside the cache kernels
+    spec = tc && !(h->debug & PCD_DEBUG_NO_SPEC) && !h->nospec_once && !verify && !(guard > 0) && !h->nocache &&
+           !h->comm && h->tc_gnode.n > 0 && h->J % 2 == 0;  // (the verification's paired loads)
+    h->nospec_once = false;
+    if (tc) {  // work list and backups on the second auxiliary stream, beside the cache kernels
       ensure_aux(h);
       CK(cudaEventRecord(h->ev_fork, h->stream));
-      CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
-      build_worklist(h, lo, hi, h->aux);
+      CK(cudaStreamWaitEvent(h->aux2, h->ev_fork, 0));
+      build_worklist(h, lo, hi, h->aux2);
       if (spec) {
         h->cbak.alloc((size_t)W);
         h->wbak.alloc((size_t)W);
-        CK(cudaMemcpyAsync(h->cbak.p, h->cache.p + lo, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->aux));
-        CK(cudaMemcpyAsync(h->wbak.p, h->written.p + lo, (size_t)W, cudaMemcpyDeviceToDevice, h->aux));
-        CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->aux));
+        CK(cudaMemcpyAsync(h->cbak.p, h->cache.p + lo, sizeof(int) * (size_t)W, cudaMemcpyDeviceToDevice, h->aux2));
+        CK(cudaMemcpyAsync(h->wbak.p, h->written.p + lo, (size_t)W, cudaMemcpyDeviceToDevice, h->aux2));
+        // (a verification in flight clears the flag on `aux` after its verdict)
+        if (!h->verify_pending) CK(cudaMemsetAsync(&h->scal->spec_bad, 0, sizeof(int), h->aux2));
       }
-      CK(cudaEventRecord(h->ev_join, h->aux));
+      CK(cudaEventRecord(h->ev_join, h->aux2));
     }
     tm.start();
     const int J = h->J;
@@ -1010,6 +1043,14 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
     CK(cudaGetLastError());
     tm.stop(&h->timing.prep_ms);
     h->timing.kernel_launches += 2;
+    // the previous iteration's pipelined verification: its verdict is needed
+    // before this sweep publishes anything; a rejected one abandons this
+    // iteration (its cache kernels wrote only per-iteration buffers)
+    if (h->verify_pending && finish_verify(h)) {
+      h->wl_ready = false;
+      out.aborted = true;
+      return out;
+    }
     tm.start();
     if (tc) {
       CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
@@ -1068,21 +1109,16 @@ static IterOut run_iteration(pcd_handle* h, int engine, int64_t lo64, int64_t hi
 // cached action, for which the reference throws ContractViolation at the
 // first such order. The check is deferred: the flag stays set on the device
 // and is read with the next iteration's scalars (no extra host round trip per
-// iteration); the state before the advance is kept in one of two backup
-// buffers so the serial error search can replay it. defer = false checks now.
+// iteration); the state before the advance is recovered by the exact inverse
+// (unadvance) so the serial error search can replay it. defer = false checks now.
 static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to, bool defer = true) {
   if (to <= from) return;
   PhaseTimer tm(h);
   tm.start();
-  const size_t IJ = (size_t)h->I * h->J;
-  const int buf = h->adv_buf < 0 ? 0 : 1 - h->adv_buf;
-  int* bak = h->ckbak.p + (size_t)buf * (IJ + h->J);
-  CK(cudaMemcpyAsync(bak, h->ckinv.p, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
-  CK(cudaMemcpyAsync(bak + IJ, h->ckcap.p, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
   k_advance<<<grid_for(to - from, 256), 256, (size_t)h->J * 4, h->stream>>>(
       h->cache.p, h->product.p, (int)from, (int)to, h->J, h->ckcap.p, h->ckinv.p, &h->scal->neg_flag);
   CK(cudaGetLastError());
-  h->adv_buf = buf;
+  h->adv_buf = 0;
   h->adv_from = from;
   h->adv_to = to;
   tm.stop(&h->timing.advance_ms);
@@ -1094,6 +1130,17 @@ static void advance_checkpoint(pcd_handle* h, int64_t from, int64_t to, bool def
   }
 }
 
+// The checkpoint before the last advance: k_advance's atomic subtractions
+// added back (exact integer inverse; the advanced slots of the cache are
+// unchanged until the next sweep, which starts at the advance's end).
+static void unadvance(pcd_handle* h) {
+  const int from = (int)h->adv_from, to = (int)h->adv_to;
+  k_unadvance<<<grid_for(to - from, 256), 256, (size_t)h->J * 4, h->stream>>>(h->cache.p, h->product.p, from, to,
+                                                                             h->J, h->ckcap.p, h->ckinv.p);
+  CK(cudaGetLastError());
+  h->timing.kernel_launches += 1;
+}
+
 // h_scal->neg_flag was just read from the device: a set flag belongs to the
 // last advance (earlier ones were checked at earlier reads)
 static void check_advance(pcd_handle* h) {
@@ -1103,10 +1150,7 @@ static void check_advance(pcd_handle* h) {
     h->h_scal->neg_flag = 0;
     return;
   }
-  const size_t IJ = (size_t)h->I * h->J;
-  const int* bak = h->ckbak.p + (size_t)h->adv_buf * (IJ + h->J);
-  CK(cudaMemcpyAsync(h->ckinv.p, bak, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->ckcap.p, bak + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  unadvance(h);
   CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
   k_advance_serial<<<1, 1, 0, h->stream>>>(h->cache.p, h->product.p, h->order_t.n ? h->order_t.p : nullptr,
                                            (int)h->adv_from, (int)h->adv_to, h->J, h->ckcap.p, h->ckinv.p,
@@ -1124,10 +1168,7 @@ static void check_advance(pcd_handle* h) {
 // negativity flag.
 static void undo_advance(pcd_handle* h) {
   if (h->adv_buf < 0) return;
-  const size_t IJ = (size_t)h->I * h->J;
-  const int* bak = h->ckbak.p + (size_t)h->adv_buf * (IJ + h->J);
-  CK(cudaMemcpyAsync(h->ckinv.p, bak, sizeof(int) * IJ, cudaMemcpyDeviceToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->ckcap.p, bak + IJ, sizeof(int) * h->J, cudaMemcpyDeviceToDevice, h->stream));
+  unadvance(h);
   CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
   h->h_scal->neg_flag = 0;
   h->adv_buf = -1;
@@ -1160,7 +1201,7 @@ static void ensure_state_buffers(pcd_handle* h) {
   h->written.alloc(T + 4);  // + 4: the incremental sweep copies whole 4-byte words
   h->ckcap.alloc(std::max(1, h->J));
   h->ckinv.alloc(IJ);
-  h->ckbak.alloc(2 * (IJ + h->J));  // two backups: the deferred advance check
+  h->ckbak.alloc(IJ + h->J);  // Time Warp's merge backup
   h->xloc.alloc(std::max<size_t>(1, (size_t)h->runs * std::max(1, h->J)));
   h->tau.alloc(std::max(1, h->J));
   const size_t nb = (T + kK - 1) / kK + 1;  // + 1: blocks start at lo & ~(K-1)
@@ -1184,6 +1225,7 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   h->tc_kernel_req = cfg->tc_kernel;
   h->tlog.clear();  // (phases of an earlier call that threw: their fields are reset next)
   if (h->aux) CK(cudaStreamSynchronize(h->aux));  // (a verification left by a call that threw)
+  if (h->aux2) CK(cudaStreamSynchronize(h->aux2));
   h->verify_pending = false;
   struct CursorOff {
     pcd_handle* h;
@@ -1223,9 +1265,57 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   int64_t ws = 0, iteration = 0, episodes = 0;
   h->adv_buf = -1;
   CK(cudaMemsetAsync(&h->scal->neg_flag, 0, sizeof(int), h->stream));
-  while (ws < T) {
+  // Pipelined verification (engine_used PRODUCT with speculation): iteration
+  // i's verification runs beside iteration i+1's advance and cache kernels
+  // and is settled before i+1's sweep (run_iteration). Until then iteration
+  // i's bookkeeping is provisional: `pend` keeps what a rejection takes back
+  // (its window, whether it advanced the checkpoint, the counters before it).
+  // Not with a per-iteration history (it copies each iteration's cache).
+  h->pipe_verify = !h->history;
+  struct Acc {
+    pcd_result res;
+    int64_t mismatches, episodes, rows, steps_critical, total_evals;
+  };
+  struct Pending {
+    bool on = false, advanced = false;
+    int64_t ws = 0, W = 0, iteration = 0;
+    Acc acc{};
+  } pend;
+  auto settle = [&](const IterOut* aborted_by) -> bool {  // true: iteration pend.iteration must re-run
+    if (!pend.on) return false;
+    const bool bad = aborted_by ? aborted_by->aborted : finish_verify(h);
+    if (!bad) {
+      pend.on = false;
+      return false;
+    }
+    // rejected: back to the state before iteration pend.iteration
+    *res = pend.acc.res;
+    mismatches = pend.acc.mismatches;
+    episodes = pend.acc.episodes;
+    rows.resize((size_t)pend.acc.rows);
+    h->timing.steps_critical = pend.acc.steps_critical;
+    h->timing.total_evals = pend.acc.total_evals;
+    if (pend.advanced) undo_advance(h);
+    // (the pending window's backups were swapped out to the spares)
+    CK(cudaMemcpyAsync(h->cache.p + pend.ws, h->cbak2.p, sizeof(int) * (size_t)pend.W, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    CK(cudaMemcpyAsync(h->written.p + pend.ws, h->wbak2.p, (size_t)pend.W, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemsetAsync(h->qcur.p, 0, sizeof(int2) * (size_t)std::max(1, h->I), h->stream));  // windows back
+    ws = pend.ws;
+    iteration = pend.iteration - 1;
+    h->nospec_once = true;
+    h->timing.tc_spec_reruns += 1;
+    pend.on = false;
+    return true;
+  };
+  for (;;) {
+    if (ws >= T) {
+      if (settle(nullptr)) continue;
+      break;
+    }
     const int64_t we = cfg->max_steps > 0 ? std::min(T, ws + cfg->max_steps) : T;
     if (iteration >= cap_it) {
+      if (settle(nullptr)) continue;
       flush_advance_check(h);  // the reference throws from the advance before reaching the cap
       res->iterations_run = iteration;
       res->trace_rows = (int64_t)rows.size();
@@ -1234,14 +1324,38 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
                            iteration, rows);
     }
     ++iteration;
+    const Acc before{*res, mismatches, episodes, (int64_t)rows.size(), h->timing.steps_critical,
+                     h->timing.total_evals};
     IterOut it = run_iteration(h, engine, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify, cfg->tc_tiles, true);
+    if (it.aborted) {  // the previous iteration's speculation was rejected: re-run it
+      settle(&it);
+      continue;
+    }
+    pend.on = false;  // (run_iteration settled the previous verification)
     // the checkpoint advance goes out while a deferred verification of
     // speculated decisions still runs; a rejected one takes it back and the
     // iteration is re-run without speculation
     auto next_ws = [&](const IterOut& o) { return o.changed == 0 ? we : std::max(ws, o.first_changed); };
     int64_t nws = next_ws(it);
     if (nws > ws) advance_checkpoint(h, ws, nws);
-    if (finish_verify(h)) {
+    if (h->verify_pending && h->pipe_verify) {
+      // verdict later: the next iteration's cache kernels and backups go to
+      // the spare buffers
+      h->ev2.alloc(h->ev.n);
+      h->hck2.alloc(h->hck.n);
+      h->xloc2.alloc(h->xloc.n);
+      h->ev.swap(h->ev2);
+      h->hck.swap(h->hck2);
+      h->xloc.swap(h->xloc2);
+      h->cbak.swap(h->cbak2);
+      h->wbak.swap(h->wbak2);
+      pend.on = true;
+      pend.W = we - ws;
+      pend.advanced = nws > ws;
+      pend.ws = ws;
+      pend.iteration = iteration;
+      pend.acc = before;
+    } else if (finish_verify(h)) {
       if (nws > ws) undo_advance(h);
       rerun_without_spec(h, ws, we, nullptr, cfg->tc_guard, cfg->tc_verify, cfg->tc_tiles);
       throw_sweep_error(h);
@@ -1262,15 +1376,17 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
     h->timing.total_evals += it.total_evals;
     if (it.changed == 0) ++episodes;
     ws = nws;
-    // slots before the checkpoint are final: copy them out beside the next
+    // slots before the checkpoint are final (before the pending iteration's
+    // window while its verification runs): copy them out beside the next
     // iterations (batches of >= 1M slots)
-    if (h->dl_out && ws - h->dl_done >= (1 << 20)) {
+    const int64_t fin = pend.on ? pend.ws : ws;
+    if (h->dl_out && fin - h->dl_done >= (1 << 20)) {
       ensure_aux(h);
       CK(cudaEventRecord(h->ev_fork, h->stream));
       CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
-      CK(cudaMemcpyAsync(h->dl_out + h->dl_done, h->cache.p + h->dl_done, sizeof(int32_t) * (size_t)(ws - h->dl_done),
+      CK(cudaMemcpyAsync(h->dl_out + h->dl_done, h->cache.p + h->dl_done, sizeof(int32_t) * (size_t)(fin - h->dl_done),
                          cudaMemcpyDeviceToHost, h->aux));
-      h->dl_done = ws;
+      h->dl_done = fin;
     }
   }
   flush_advance_check(h);

@@ -831,6 +831,25 @@ static __global__ void k_advance(const int* __restrict__ cache, const int* __res
 }
 
 
+// k_advance taken back (a rejected speculation, or the error path's replay):
+// the same fulfilments added back, so the checkpoint is exactly the one before.
+static __global__ void k_unadvance(const int* __restrict__ cache, const int* __restrict__ product, int lo, int hi,
+                                   int J, int* __restrict__ ckcap, int* __restrict__ ckinv) {
+  extern __shared__ int hcap[];
+  for (int j = threadIdx.x; j < J; j += blockDim.x) hcap[j] = 0;
+  __syncthreads();
+  for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
+    const int a = cache[t];
+    if (a >= 0 && a < J) {
+      atomicAdd(&hcap[a], 1);
+      atomicAdd(&ckinv[(size_t)product[t] * J + a], 1);
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < J; j += blockDim.x)
+    if (hcap[j]) atomicAdd(&ckcap[j], hcap[j]);
+}
+
 // Error path only: serial re-application to find the first infeasible order.
 static __global__ void k_advance_serial(const int* __restrict__ cache, const int* __restrict__ product,
                                  const int* __restrict__ order_t, int lo, int hi, int J,
