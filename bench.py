@@ -8,11 +8,14 @@ T=10^7 orders (generate_instance recipe, seed 7, beta 0, coverage 0.8, the
 seeded synthetic 100-node geometry), dual-price MLP policy {201,64,64,200}
 with theta seed 5, M=65536 processes, max_steps = 300,000 (the window; the
 CLI default 300*M = the whole horizon is timed beside it, same trajectory).
-Partition (--partition): "chunk" (default) =
-make_product_chunk_partition(M): every product's orders cut into contiguous
-chunks, one process each, so all 65536 processes carry work; "product" = the
+Partition (--partition): "window" (default) =
+make_product_window_partition(M, max_steps): every product's orders cut into
+contiguous chunks, one process each, so that no window of max_steps orders
+holds more than L orders of one process (L minimal for <= M chunks: 39 at the
+C3 window, where equal chunks leave ~52); "chunk" =
+make_product_chunk_partition(M): equal-count contiguous chunks; "product" = the
 reference's make_product_partition(M, seed 1), which activates only I=10^4 of
-them. Both reach the same (serial) trajectory. One "step" = one full
+them. All reach the same (serial) trajectory. One "step" = one full
 picard_simulate to convergence. Synthetic data, random-init weights.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -156,6 +159,8 @@ class ClockSampler:
 PARTITIONS = {
     "product": "make_product_partition(M, seed 1) (the reference's partitioner)",
     "chunk": "make_product_chunk_partition(M): each product's orders cut into contiguous chunks, one process each",
+    "window": "make_product_window_partition(M, max_steps): each product's orders cut into contiguous chunks so "
+              "that no max_steps-long interval holds more than L orders of one chunk, L minimal for <= M chunks",
 }
 DTYPE = ("f64 decisions (fp16x3 tcgen05 MLP; rows whose decision margin is within the derived error bound "
          "2B are re-evaluated in exact FP64)")
@@ -182,12 +187,14 @@ def trajectory_hash(actions) -> str:
     return hashlib.blake2b(np.ascontiguousarray(actions, np.int32).tobytes(), digest_size=8).hexdigest()
 
 
-def make_workload(name: str, partition: str = "product"):
+def make_workload(name: str, partition: str = "product", window: int = 0):
     import paper_2406_01939_b200 as P
     J, I, T, M, theta = WORKLOADS[name]
     inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
     pol = P.DualNetworkPolicy.seeded(inst, theta)
-    if partition == "chunk":
+    if partition == "window":
+        plan = P.make_product_window_partition(inst, M, window or default_window(name), 1)
+    elif partition == "chunk":
         plan = P.make_product_chunk_partition(inst, M, 1)
     else:
         plan = P.make_product_partition(inst, M, 1)
@@ -372,7 +379,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
-    ap.add_argument("--partition", default="chunk", choices=sorted(PARTITIONS))
+    ap.add_argument("--partition", default="window", choices=sorted(PARTITIONS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-picard", action="store_true")
@@ -392,9 +399,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2406_01939_b200 as P
-    inst, pol, plan, w = make_workload(args.workload, args.partition)
-    T = w["T"]
     max_steps = default_window(args.workload) if args.max_steps is None else args.max_steps
+    inst, pol, plan, w = make_workload(args.workload, args.partition, max_steps)
+    T = w["T"]
     cfg = P.PicardConfig(max_steps=max_steps)
     sim = P.Simulator(inst, pol, device=local)
     sim.set_plan(plan)

@@ -364,6 +364,16 @@ int pcd_product_partition(const pcd_instance* inst, int32_t processes,
  * products. A run partition, so PCD_ENGINE_PRODUCT applies. owner[T]. */
 int pcd_product_chunk_partition(const pcd_instance* inst, int32_t processes,
                                 uint64_t seed, int32_t* owner);
+/* Window-aware product chunks (no reference counterpart): each product's
+ * orders in time order are cut greedily so that no `window`-long interval
+ * (PicardConfig::max_steps, engine.hpp:120-126) holds more than L orders of
+ * one chunk, L the smallest bound with at most `processes` chunks; products
+ * sparse in time stay whole. Bounds every iteration's per-process chain by L
+ * at that window. window <= 0: the whole horizon. Falls back to
+ * pcd_product_partition(seed) when processes < ordered products. A run
+ * partition, so PCD_ENGINE_PRODUCT applies. owner[T]. */
+int pcd_product_window_partition(const pcd_instance* inst, int32_t processes,
+                                 int64_t window, uint64_t seed, int32_t* owner);
 /* make_uniform_time_partition (engine.hpp:99-114): owner[T]. */
 int pcd_uniform_partition(int64_t horizon, int32_t processes, uint64_t seed,
                           int32_t* owner);

@@ -508,4 +508,21 @@ inline PartitionPlan make_product_chunk_partition(const fo::FoEnv& env, std::spa
   return plan;
 }
 
+// Window-aware product chunks (no reference counterpart;
+// pcd_product_window_partition): every window of `window` slots holds at most
+// L orders of any one process, L minimal for `processes` chunks. A valid
+// PartitionPlan for picard_simulate (same trajectory), tuned for
+// PicardConfig::max_steps = window.
+inline PartitionPlan make_product_window_partition(const fo::FoEnv& env, std::span<const fo::Order> orders,
+                                                   std::int32_t processes, std::int64_t window,
+                                                   std::uint64_t seed = 1) {
+  auto m = detail::marshal(env, orders);
+  PartitionPlan plan;
+  plan.processes = processes;
+  plan.owner.assign(orders.size(), 0);
+  const int rc = pcd_product_window_partition(&m.view, processes, window, seed, plan.owner.data());
+  if (rc) detail::raise(rc);
+  return plan;
+}
+
 }  // namespace picard::b200

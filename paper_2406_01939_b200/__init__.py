@@ -12,7 +12,7 @@ from .api import (  # noqa: F401
     Instance, InvalidArgument, IterationLimitError, IterationOutcome, MlpParams, NullOnlyPolicy,
     PartitionPlan, PicardConfig, PicardError, PicardResult, PicardTraceRow, Policy, SequentialOutput,
     Simulator, compare_to_oracle, device_count, fo_total_reward, generate_instance,
-    make_product_chunk_partition, make_product_partition, make_uniform_time_partition, nccl_unique_id, picard_iterate_once,
+    make_product_chunk_partition, make_product_partition, make_product_window_partition, make_uniform_time_partition, nccl_unique_id, picard_iterate_once,
     LoopbackGroup, tc_error_bound,
     picard_simulate, sequential_simulate, shard_processes)
 

@@ -122,6 +122,7 @@ SIGNATURES = {
     "pcd_host_alloc": (C.c_void_p, [C.c_size_t]),
     "pcd_host_free": (None, [C.c_void_p]),
     "pcd_product_chunk_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_uint64, I32P]),
+    "pcd_product_window_partition": (C.c_int, [C.POINTER(pcd_instance), C.c_int32, C.c_int64, C.c_uint64, I32P]),
     "pcd_uniform_partition": (C.c_int, [C.c_int64, C.c_int32, C.c_uint64, I32P]),
     "pcd_seeded_mlp": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_int32,
                                  F64P, F64P, F64P, F64P, F64P, F64P]),

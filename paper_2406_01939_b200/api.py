@@ -9,6 +9,7 @@ fo::Instance (instance.hpp:25-37)      :class:`Instance`
 fo::generate_instance (instance.cpp:80) :func:`generate_instance`
 fo::make_product_partition (:142-186)  :func:`make_product_partition`
 (ours, no reference counterpart)       :func:`make_product_chunk_partition`
+(ours, no reference counterpart)       :func:`make_product_window_partition`
 make_uniform_time_partition (engine.hpp:99-114) :func:`make_uniform_time_partition`
 linear::make_contractive_spec (linear.cpp:126) :func:`make_contractive_spec`
 linear::picard_convergence_curve (linear.cpp:279) :func:`picard_convergence_curve`
@@ -239,6 +240,22 @@ def make_product_chunk_partition(instance: Instance, processes: int, seed: int =
     owner = np.zeros(max(int(instance.horizon), 1), np.int32)
     c = instance.to_c()
     _check(LIB.pcd_product_chunk_partition(C.byref(c), int(processes), int(seed) & (2**64 - 1), _ptr(owner)))
+    return PartitionPlan(int(processes), owner[:int(instance.horizon)])
+
+
+def make_product_window_partition(instance: Instance, processes: int, window: int,
+                                  seed: int = 1) -> PartitionPlan:
+    """Window-aware product chunks (ours, ``pcd_product_window_partition``):
+    each product's orders cut greedily so that no ``window``-long interval
+    holds more than L orders of one process, L minimal for ``processes``
+    chunks. An iteration's critical path at ``PicardConfig(max_steps=window)``
+    is then at most L steps; products sparse in time stay whole. Falls back
+    to :func:`make_product_partition` when ``processes`` is below the number
+    of ordered products."""
+    owner = np.zeros(max(int(instance.horizon), 1), np.int32)
+    c = instance.to_c()
+    _check(LIB.pcd_product_window_partition(C.byref(c), int(processes), int(window), int(seed) & (2**64 - 1),
+                                            _ptr(owner)))
     return PartitionPlan(int(processes), owner[:int(instance.horizon)])
 
 

@@ -96,6 +96,18 @@ int pcd_product_chunk_partition(const pcd_instance* inst, int32_t processes, uin
   PCD_CATCH
 }
 
+int pcd_product_window_partition(const pcd_instance* inst, int32_t processes, int64_t window, uint64_t seed,
+                                 int32_t* owner) {
+  PCD_TRY
+  if (!inst || !owner) throw pcd::InvalidArgument("null argument");
+  for (int64_t t = 0; t < inst->horizon; ++t)
+    if (inst->product[t] < 0 || inst->product[t] >= inst->products)
+      throw pcd::InvalidArgument("order product out of range");
+  pcd::product_window_partition(inst->product, inst->horizon, inst->products, processes, window, seed, owner);
+  return PCD_OK;
+  PCD_CATCH
+}
+
 int pcd_linear_contractive_spec(int32_t state_dim, int32_t input_dim, int64_t horizon, double rho, uint64_t seed,
                                 double state_coupling, double* dynamics, double* input, double* disturbances,
                                 double* gain, double* contraction) {

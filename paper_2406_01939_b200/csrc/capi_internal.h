@@ -40,6 +40,8 @@ void product_partition(const int32_t* product, int64_t T, int32_t I, int32_t M, 
                        int32_t* owner);
 void product_chunk_partition(const int32_t* product, int64_t T, int32_t I, int32_t M, uint64_t seed,
                              int32_t* owner);
+void product_window_partition(const int32_t* product, int64_t T, int32_t I, int32_t M, int64_t W,
+                              uint64_t seed, int32_t* owner);
 void uniform_partition(int64_t T, int32_t M, uint64_t seed, int32_t* owner);
 void seeded_mlp(int32_t in, int32_t out, uint64_t seed, int32_t h, double* w1, double* b1,
                 double* w2, double* b2, double* w3, double* b3);

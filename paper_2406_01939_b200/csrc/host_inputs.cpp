@@ -244,6 +244,78 @@ void product_chunk_partition(const int32_t* product, int64_t T, int32_t I, int32
   }
 }
 
+// Window-aware product chunks (ours; no reference counterpart). A Picard
+// iteration's critical path is its busiest process's own slots inside the
+// window [ws, ws + W) (engine.hpp:120-126, max_steps = W), so cutting a
+// product whose orders are sparse in time buys nothing, while a product with a
+// dense stretch bounds every window. Each product's orders, in time order,
+// are cut greedily: a chunk grows while no W-long interval holds more than L
+// of its orders (checked at every new order against the chunk's orders in
+// (t - W, t]); greedy is minimal per product since the constraint holds for
+// every sub-run of a valid chunk. L is the smallest bound with at most M
+// chunks in total, so every window's per-process chain is <= L. W <= 0 or
+// W >= T: the whole horizon is one window (chunks of at most L orders).
+// Falls back to make_product_partition when M is below the ordered products.
+void product_window_partition(const int32_t* product, int64_t T, int32_t I, int32_t M, int64_t W,
+                              uint64_t seed, int32_t* owner) {
+  if (M < 1) throw InvalidArgument("process count must be >= 1");
+  if (W <= 0 || W > T) W = T;
+  std::vector<int64_t> start((size_t)I + 1, 0);
+  for (int64_t t = 0; t < T; ++t) start[(size_t)product[t] + 1] += 1;
+  int64_t used = 0, qmax = 0;
+  for (int32_t i = 0; i < I; ++i) {
+    used += start[(size_t)i + 1] > 0;
+    qmax = std::max(qmax, start[(size_t)i + 1]);
+    start[(size_t)i + 1] += start[(size_t)i];
+  }
+  if (used > M || T == 0) return product_partition(product, T, I, M, seed, owner);
+  std::vector<int64_t> ts((size_t)T);  // each product's order times, ascending
+  {
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t t = 0; t < T; ++t) ts[(size_t)fill[(size_t)product[t]]++] = t;
+  }
+  // chunks of product i under bound L; cut[] (optional) receives each chunk's
+  // first rank within the product
+  auto cut_product = [&](int32_t i, int64_t L, std::vector<int64_t>* cut) {
+    const int64_t* a = ts.data() + start[(size_t)i];
+    const int64_t q = start[(size_t)i + 1] - start[(size_t)i];
+    int64_t n = q > 0, k0 = 0, j = 0;  // j: first rank with time > a[k] - W
+    if (cut && q > 0) cut->push_back(0);
+    for (int64_t k = 0; k < q; ++k) {
+      while (a[j] <= a[k] - W) ++j;
+      if (k - std::max(k0, j) + 1 > L) {
+        k0 = k;
+        ++n;
+        if (cut) cut->push_back(k);
+      }
+    }
+    return n;
+  };
+  auto chunks = [&](int64_t L) {
+    int64_t k = 0;
+    for (int32_t i = 0; i < I && k <= M; ++i) k += cut_product(i, L, nullptr);
+    return k;
+  };
+  int64_t lo = 1, hi = qmax;  // chunks(qmax) = used <= M
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (chunks(mid) <= M) hi = mid; else lo = mid + 1;
+  }
+  int32_t next = 0;
+  std::vector<int64_t> cut;
+  for (int32_t i = 0; i < I; ++i) {
+    cut.clear();
+    cut_product(i, lo, &cut);
+    const int64_t b = start[(size_t)i], q = start[(size_t)i + 1] - b;
+    size_t c = 0;
+    for (int64_t k = 0; k < q; ++k) {
+      while (c + 1 < cut.size() && cut[c + 1] <= k) ++c;
+      owner[ts[(size_t)(b + k)]] = next + (int32_t)c;
+    }
+    next += (int32_t)cut.size();
+  }
+}
+
 void uniform_partition(int64_t T, int32_t M, uint64_t seed, int32_t* owner) {
   if (M < 1) throw ContractViolation("uniform partition: process count must be >= 1");
   Engine gen(seed);

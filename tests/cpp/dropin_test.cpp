@@ -171,6 +171,18 @@ int main() {
     cfg.max_steps = 700;
     compare(inst, GreedyPolicy{}, plan, cfg);
   }
+  // window-aware product chunks (b200::make_product_window_partition), at the
+  // window they are cut for and at the whole horizon
+  {
+    const auto inst = generate_instance(30, 200, 6000, -0.3, 0.8, 7);
+    const auto env = inst.make_env();
+    const auto plan = b200::make_product_window_partition(env, std::span<const Order>(inst.orders), 900, 700);
+    PicardConfig cfg;
+    cfg.max_steps = 700;
+    compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, 5), plan, cfg);
+    compare(inst, DualNetworkPolicy::seeded(inst.shared_initial(), inst.horizon, 5), plan, {});
+    compare(inst, CapacityPenalizedPolicy{0.7}, plan, cfg);
+  }
   for (std::uint64_t seed = 300; seed < 316; ++seed) {
     const auto inst = small_random(seed);
     const auto env = inst.make_env();

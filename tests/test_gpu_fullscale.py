@@ -4,7 +4,8 @@
   processes): the instance and policy built by the product equal the
   reference generator's; the whole 1e7-step trajectory equals the
   reference's sequential_simulate (engine.hpp:237-267) action for action, on
-  the tensor-core engine at the bench's window and at the CLI-default window,
+  the tensor-core engine at the bench's window and at the CLI-default window
+  (equal-count chunks and the bench's window-aware chunks),
   and on the FP64 SIMT engine; fo_total_reward agrees (rel. 1e-4 is the
   north-star bar; the difference is printed); the final FoState (the device
   checkpoint after convergence) equals the reference's state after the
@@ -14,7 +15,7 @@
   and trace (iterations to converged / correct, conflicts, evaluation
   counters, every trace row) equal the reference's picard_simulate
   (engine.hpp:458-590, threads = every host core) on the reference's
-  product partition and on the product-chunk plan.
+  product partition, the product-chunk plan and the window-aware chunk plan.
 
 The reference serial run at C3 takes ~2-3 min on one host core.
 """
@@ -59,17 +60,21 @@ def c3():
     sess.close()
     print(f"\nreference sequential_simulate over the full C3 horizon: {sec:.1f} s")
     plan = P.make_product_chunk_partition(inst, M, 1)
-    return NS(ref=ref, inst=inst, pol=pol, seq=seq, cap=cap, inv=inv, reward=reward, plan=plan)
+    wplan = P.make_product_window_partition(inst, M, C3_WINDOW, 1)  # the bench's plan
+    return NS(ref=ref, inst=inst, pol=pol, seq=seq, cap=cap, inv=inv, reward=reward, plan=plan, wplan=wplan)
 
 
-@pytest.mark.parametrize("window,engine,kernel", [(C3_WINDOW, "auto", "fused"), (C3_WINDOW, "auto", "incremental"),
-                                                  (500_000, "auto", "fused"),
-                                                  (300 * 65536, "auto", "fused"),
-                                                  (300 * 65536, "auto", "incremental"),
-                                                  (300 * 65536, "product_fp64", "auto")])
-def test_c3_full_trajectory_equals_reference_serial(c3, window, engine, kernel):
+@pytest.mark.parametrize("window,engine,kernel,plan", [(C3_WINDOW, "auto", "fused", "window"),
+                                                       (C3_WINDOW, "auto", "fused", "chunk"),
+                                                       (C3_WINDOW, "auto", "incremental", "chunk"),
+                                                       (500_000, "auto", "fused", "chunk"),
+                                                       (300 * 65536, "auto", "fused", "chunk"),
+                                                       (300 * 65536, "auto", "fused", "window"),
+                                                       (300 * 65536, "auto", "incremental", "chunk"),
+                                                       (300 * 65536, "product_fp64", "auto", "chunk")])
+def test_c3_full_trajectory_equals_reference_serial(c3, window, engine, kernel, plan):
     with P.Simulator(c3.inst, c3.pol) as sim:
-        sim.set_plan(c3.plan)
+        sim.set_plan(c3.wplan if plan == "window" else c3.plan)
         r = sim.simulate(P.PicardConfig(max_steps=window, engine=engine, tc_kernel=kernel))
         cap, inv = sim.checkpoint_state()
     assert r.timing["tc_used"] == (1 if engine == "auto" else 0)
@@ -84,14 +89,14 @@ def test_c3_full_trajectory_equals_reference_serial(c3, window, engine, kernel):
     assert rel <= 1e-4
 
 
-@pytest.mark.parametrize("window,kernel", [(C3_WINDOW, "fused"), (C3_WINDOW, "incremental"),
-                                           (300 * 65536, "fused")])
-def test_c3_verify_mode_every_row_rechecked(c3, window, kernel):
+@pytest.mark.parametrize("window,kernel,plan", [(C3_WINDOW, "fused", "window"), (C3_WINDOW, "fused", "chunk"),
+                                                (C3_WINDOW, "incremental", "chunk"), (300 * 65536, "fused", "chunk")])
+def test_c3_verify_mode_every_row_rechecked(c3, window, kernel, plan):
     """tc_verify: every tensor-core row is also evaluated in exact FP64; no row
     outside the guard may disagree (tc_unflagged_bad == 0) and the trajectory
     is the reference's."""
     with P.Simulator(c3.inst, c3.pol) as sim:
-        sim.set_plan(c3.plan)
+        sim.set_plan(c3.wplan if plan == "window" else c3.plan)
         r = sim.simulate(P.PicardConfig(max_steps=window, tc_verify=True, tc_kernel=kernel))
     t = r.timing
     assert t["tc_used"] == 1 and t["tc_rows"] > 3e7
@@ -112,11 +117,13 @@ def c2():
     return NS(inst=inst, ref=ref, pol=pol, seq=seq, M=M, T=T)
 
 
-@pytest.mark.parametrize("part,window", [("product", 0), ("chunk", 0), ("chunk", 100_000)])
+@pytest.mark.parametrize("part,window", [("product", 0), ("chunk", 0), ("chunk", 100_000), ("window", 100_000)])
 def test_c2_counters_and_trace_equal_reference_picard(c2, part, window):
     if part == "product":
         plan = P.make_product_partition(c2.inst, c2.M, 1)
         assert np.array_equal(plan.owner, REF.product_partition(c2.ref, c2.M, 1))
+    elif part == "window":
+        plan = P.make_product_window_partition(c2.inst, c2.M, window, 1)
     else:
         plan = P.make_product_chunk_partition(c2.inst, c2.M, 1)
     ms = window or 300 * c2.M

@@ -117,6 +117,56 @@ def test_product_chunk_partition_is_a_balanced_run_partition(J, I, T, M):
             c = np.bincount(own - own.min())
             c = c[c > 0]
             assert c.max() - c.min() <= 1
+def _window_cuts(times, W, L):
+    """Greedy restatement: a chunk grows while no W-long interval holds more
+    than L of its orders (tested at each new order)."""
+    cuts, k0, j = [0], 0, 0
+    for k in range(len(times)):
+        while times[j] <= times[k] - W:
+            j += 1
+        if k - max(k0, j) + 1 > L:
+            k0 = k
+            cuts.append(k)
+    return cuts
+
+
+@pytest.mark.parametrize("J,I,T,M,W", [(5, 20, 3000, 64, 300), (5, 20, 3000, 200, 100), (8, 50, 5000, 30, 500),
+                                       (3, 7, 2000, 5, 0), (4, 12, 1500, 40, 1500), (6, 30, 4000, 97, 257)])
+def test_product_window_partition_bounds_every_window(J, I, T, M, W):
+    inst = P.generate_instance(J, I, T, -0.5, 0.8, 13)
+    plan = P.make_product_window_partition(inst, M, W)
+    assert plan.processes == M and plan.owner.min() >= 0 and plan.owner.max() < M
+    assert is_run_partition(plan.owner, inst.product)
+    q = np.bincount(inst.product, minlength=I)
+    used = int((q > 0).sum())
+    if M < used:  # falls back to the reference's product partition
+        assert np.array_equal(plan.owner, P.make_product_partition(inst, M, 1).owner)
+        return
+    Wn = T if W <= 0 or W > T else W
+    times = [np.flatnonzero(inst.product == p) for p in range(I)]
+    # the bound: the largest count of one process's orders in any Wn-interval
+    L = 0
+    for p in range(I):
+        for proc in np.unique(plan.owner[times[p]]):
+            ts = np.flatnonzero(plan.owner == proc)
+            L = max(L, int((np.searchsorted(ts, ts + Wn) - np.arange(ts.size)).max()))
+    # same cuts as the greedy restatement at L, and L is minimal for M chunks
+    for p in range(I):
+        own = plan.owner[times[p]]
+        if own.size:
+            assert (np.diff(own) >= 0).all()
+            assert list(np.flatnonzero(np.diff(own)) + 1) == _window_cuts(times[p], Wn, L)[1:]
+    assert sum(len(_window_cuts(t, Wn, L)) for t in times if t.size) <= M
+    if L > 1:
+        assert sum(len(_window_cuts(t, Wn, L - 1)) for t in times if t.size) > M
+
+
+def test_product_window_partition_rejects_bad_input():
+    inst = P.generate_instance(3, 5, 100, 0.0, 0.8, 1)
+    with pytest.raises(P.InvalidArgument):
+        P.make_product_window_partition(inst, 0, 10)
+
+
 
 
 def test_product_partition_hand_trace(golden):
