@@ -6,7 +6,7 @@ Workload (default "c3", BASELINE.json configs[2], the north-star target and the
 largest config; it fits one B200): SCO with J=100 nodes, I=10^4 products,
 T=10^7 orders (generate_instance recipe, seed 7, beta 0, coverage 0.8, the
 seeded synthetic 100-node geometry), dual-price MLP policy {201,64,64,200}
-with theta seed 5, M=65536 processes, max_steps = 300,000 (the window; the
+with theta seed 5, M=65536 processes, max_steps = 350,000 (the window; the
 CLI default 300*M = the whole horizon is timed beside it, same trajectory).
 Partition (--partition): "window" (default) =
 make_product_window_partition(M, max_steps): every product's orders cut into
@@ -53,11 +53,12 @@ WORKLOADS = {
 # workload. Every window reaches the same serial trajectory (Prop. 1; the
 # reference's window-width invariance test, test_engine.cpp:455-477); the
 # width only changes how much of the horizon each iteration re-evaluates.
-# C3: 300,000 (profiles/r02_window_sweep_c3_derived.jsonl, derived guard:
-# 168 ms vs 174 ms at 500k, 222 ms at 1M and 749 ms for the CLI default 300*M,
-# which is the whole horizon here); C2/C1: the CLI default (cli.cpp:225-227),
-# narrower windows are slower there.
-WINDOWS = {"c1": None, "c2": None, "c3": 300_000}
+# C3: 350,000 with the window-aware plan cut for it
+# (profiles/r02_window_partition_sweep_c3.jsonl: 73.6 ms vs 75.0 at 300k,
+# 73.8 at 400k, 77.2 at 500k, 93 at 1M; the CLI default 300*M is the whole
+# horizon here); C2/C1: the CLI default (cli.cpp:225-227), narrower windows
+# are slower there.
+WINDOWS = {"c1": None, "c2": None, "c3": 350_000}
 
 
 def default_window(name: str) -> int:
@@ -164,7 +165,7 @@ PARTITIONS = {
 }
 DTYPE = ("f64 decisions (fp16x3 tcgen05 MLP; rows whose decision margin is within the derived error bound "
          "2B are re-evaluated in exact FP64)")
-NCU_PROFILE = os.path.join("profiles", "r02_ncu_sweep_pp.json")  # ncu --set full of the sweep (tools/ncu_summary.py)
+NCU_PROFILE = os.path.join("profiles", "r02_ncu_sweep_pp_wplan.json")  # ncu --set full of the sweep (tools/ncu_summary.py)
 
 
 def workload_config(args, world: int) -> dict:

@@ -1,6 +1,6 @@
 """Small driver for ncu captures / phase profiles of the sweep kernels (not a test).
 
-  python tools/tc_ncu_target.py J I T M [engine] [--cap K] [--chunk] [--window W] [--evals K]
+  python tools/tc_ncu_target.py J I T M [engine] [--cap K] [--chunk | --wplan] [--window W] [--evals K]
 
 --cap K    stop after K iterations (IterationLimitError is expected)
 --evals K  also print the evaluations (all / tensor-core rows) of iteration K,
@@ -21,7 +21,12 @@ engine = sys.argv[5] if len(sys.argv) > 5 and not sys.argv[5].startswith("--") e
 window = arg("--window", 0)
 inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
 pol = P.DualNetworkPolicy.seeded(inst, 5)
-plan = P.make_product_chunk_partition(inst, M, 1) if "--chunk" in sys.argv else P.make_product_partition(inst, M, 1)
+if "--wplan" in sys.argv:  # the bench's plan: window-aware chunks for this window
+    plan = P.make_product_window_partition(inst, M, window, 1)
+elif "--chunk" in sys.argv:
+    plan = P.make_product_chunk_partition(inst, M, 1)
+else:
+    plan = P.make_product_partition(inst, M, 1)
 
 
 def run(sim, cap):

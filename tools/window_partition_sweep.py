@@ -5,7 +5,7 @@
 (Prop. 1); the window-aware plan bounds each iteration's per-process chain.
 
   python tools/window_partition_sweep.py [W ...]      (default 200k 300k 400k)
-  WS_M=65536  WS_PARTS=window,chunk
+  WS_M=65536  WS_PARTS=window,chunk  WS_SHAPE=J,I,T (default the C3 shape 100,10000,1e7)
   -> one JSON line per (window, partition); ms = best of two resident runs
 """
 import json
@@ -18,7 +18,7 @@ sys.path.insert(0, ".")
 import paper_2406_01939_b200 as P  # noqa: E402
 
 Ws = [int(float(x)) for x in sys.argv[1:]] or [200_000, 300_000, 400_000]
-J, I, T = 100, 10_000, 10_000_000
+J, I, T = (int(float(x)) for x in os.environ.get("WS_SHAPE", "100,10000,1e7").split(","))  # C2: 10,1000,1e6
 M = int(os.environ.get("WS_M", "65536"))
 inst = P.generate_instance(J, I, T, 0.0, 0.8, 7)
 pol = P.DualNetworkPolicy.seeded(inst, 5)
