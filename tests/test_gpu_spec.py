@@ -45,10 +45,14 @@ def _run(inst, pol, plan, cfg, flags, seq=None):
                                                         (30, 200, 12000, 256, "chunk", 2000, 2.0),
                                                         (100, 300, 30000, 512, "chunk", 0, 1.0),
                                                         (100, 300, 30000, 512, "chunk", 5000, 1.0),
-                                                        (10, 1000, 200000, 2048, "chunk", 20000, 1.0)])
+                                                        (10, 1000, 200000, 2048, "chunk", 20000, 1.0),
+                                                        (30, 200, 12000, 512, "window", 2000, 1.0),
+                                                        (100, 300, 30000, 1024, "window", 5000, 1.0)])
 def test_speculation_equals_the_non_speculative_sweep(J, I, T, M, part, window, scale):
     ons, inst, pol, opol = _case(J, I, T, scale=scale)
-    plan = (P.make_product_chunk_partition(inst, M, 1) if part == "chunk" else P.make_product_partition(inst, M, 1))
+    plan = (P.make_product_chunk_partition(inst, M, 1) if part == "chunk"
+            else P.make_product_window_partition(inst, M, window, 1) if part == "window"
+            else P.make_product_partition(inst, M, 1))
     seq, _ = ORC.sequential(ons, opol)
     cfg = P.PicardConfig(max_steps=window, record_trace=True)
     runs = {f: _run(inst, pol, plan, cfg, f, seq) for f in (0, NO_SPEC, SPEC_RERUN, SPEC_FLIP)}
