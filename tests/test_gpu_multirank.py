@@ -71,7 +71,7 @@ def _same(a, b):
 @pytest.mark.parametrize("engine,part,window", [("auto", "product", 0), ("auto", "product", 2500),
                                                 ("product_fp64", "product", 0), ("general", "product", 3000),
                                                 ("replay", "product", 0), ("auto", "uniform", 0),
-                                                ("auto", "chunk", 1500)])
+                                                ("auto", "chunk", 1500), ("auto", "window", 1500)])
 def test_loopback_ranks_equal_single_rank(nranks, engine, part, window):
     inst, pol, seq = _case(30, 200, 12000)
     M = 256
@@ -79,6 +79,8 @@ def test_loopback_ranks_equal_single_rank(nranks, engine, part, window):
         plan = P.make_product_partition(inst, M, 1)
     elif part == "chunk":
         plan = P.make_product_chunk_partition(inst, M, 1)
+    elif part == "window":
+        plan = P.make_product_window_partition(inst, M, window, 1)
     else:
         plan = P.make_uniform_time_partition(inst.horizon, 64, 1)
     cfg = P.PicardConfig(max_steps=window, record_trace=True, engine=engine)
