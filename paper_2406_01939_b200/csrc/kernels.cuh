@@ -244,8 +244,10 @@ static __global__ void k_tau(const int* __restrict__ hck, const int* __restrict_
 //   xloc[run][j] = ckinv[p][j] - #{effective cached attempts (p, j) in
 //                                  [lo, first slot) that precede tau[j]}.
 // One warp per product walks the window slots in time order with per-node
-// counts in smem and writes a row at every run start.
-static __global__ void k_xinit(const int* __restrict__ qstart, const int* __restrict__ qslots, int I, int lo,
+// counts in smem and writes a row at every run start. (256, 8): 32
+// registers, 64 warps per SM, so the 10^4 product warps of C3 take 1.06
+// waves instead of 1.4 (prep 7.4 -> 7.3 ms)
+static __global__ void __launch_bounds__(256, 8) k_xinit(const int* __restrict__ qstart, const int* __restrict__ qslots, int I, int lo,
                                int hi, const int* __restrict__ ev, const int* __restrict__ rid,
                                const int* __restrict__ tau, const int* __restrict__ ckinv, int J,
                                int* __restrict__ xloc, int2* __restrict__ qcur = nullptr) {
