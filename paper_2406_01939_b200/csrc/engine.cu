@@ -400,6 +400,7 @@ struct pcd_handle {
   cudaEvent_t ev_vdone = nullptr;
   int* h_vbad = nullptr;  // pinned: the verification's verdict
   bool pipe_verify = false;
+  int64_t wl_hint = 0;       // busiest window load of the last iteration (build_worklist's sort width)
   bool nospec_once = false;  // the next iteration re-runs one whose speculation was rejected
   // pinned host destination of the actions (pcd_simulate): the committed
   // prefix streams out on `aux` while later iterations run
@@ -679,6 +680,18 @@ static void build_worklist(pcd_handle* h, int lo, int hi, cudaStream_t st) {
                                                  h->wbeg.p);
   int bits = 1;
   while ((1LL << bits) <= (long long)h->max_load) ++bits;
+  // (simulate) sort on the bits the previous iteration's busiest window load
+  // needs, with headroom, instead of the plan's whole-horizon maximum: one
+  // radix pass instead of two at C3. A heavier load would only be dealt out
+  // of LPT order (the sweep's results do not depend on the order); the
+  // incremental sweep reads the maximum off the sorted list, so it keeps
+  // every bit.
+  const bool inc = h->tc_kernel_req == 2 || (h->debug & PCD_DEBUG_TC_INC) || kIncDefault;
+  if (h->wl_hint > 0 && !inc) {
+    int hb = 1;
+    while ((1LL << hb) <= 4 * h->wl_hint) ++hb;
+    bits = std::min(bits, hb);
+  }
   size_t tb = 0;
   CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->wload.p, h->wload_s.p, h->wids.p, h->wq.p, M, 0,
                                                bits, st));
@@ -1234,6 +1247,11 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
   h->qcur.alloc((size_t)std::max(1, h->I));
   CK(cudaMemsetAsync(h->qcur.p, 0, sizeof(int2) * (size_t)std::max(1, h->I), h->stream));
   h->qcur_on = true;
+  h->wl_hint = 0;
+  struct HintOff {
+    pcd_handle* h;
+    ~HintOff() { h->wl_hint = 0; }
+  } hint_guard{h};
   h->evnext = 0;
   struct DeferTimers {
     pcd_handle* h;
@@ -1363,6 +1381,7 @@ static void simulate(pcd_handle* h, const pcd_config* cfg, bool track, pcd_resul
       nws = next_ws(it);
       if (nws > ws) advance_checkpoint(h, ws, nws);
     }
+    h->wl_hint = it.max_evals;
     res->iterations_to_converged += 1;
     res->policy_eval_count_sequential_equivalent += it.max_evals;
     res->total_policy_evals += it.total_evals;
