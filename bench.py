@@ -11,8 +11,8 @@ CLI default 300*M = the whole horizon is timed beside it, same trajectory).
 Partition (--partition): "window" (default) =
 make_product_window_partition(M, max_steps): every product's orders cut into
 contiguous chunks, one process each, so that no window of max_steps orders
-holds more than L orders of one process (L minimal for <= M chunks: 39 at the
-C3 window, where equal chunks leave ~52); "chunk" =
+holds more than L orders of one process (L minimal for <= M chunks: 44 at the
+C3 window of 350k, where equal chunks leave ~58); "chunk" =
 make_product_chunk_partition(M): equal-count contiguous chunks; "product" = the
 reference's make_product_partition(M, seed 1), which activates only I=10^4 of
 them. All reach the same (serial) trajectory. One "step" = one full
